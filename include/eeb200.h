@@ -1,0 +1,137 @@
+/*
+ * eeb200.h — C ABI of the B200 (sm_100a) early-exit decision kernels.
+ *
+ * This is the drop-in boundary for the exit-decision seam of the reference
+ * package `eesim` (arXiv 2312.05385, "Apparate"): the module
+ * `eesim._kernels` (pkg/src/eesim/_kernels/__init__.py:14-48) exposes two
+ * callables, `exit_sites` and `eval_thresholds`, implemented in Cython
+ * (pkg/src/eesim/_kernels/_exitcore.pyx:11-56) with a numpy twin
+ * (pkg/src/eesim/_kernels/_ref.py:17-62). Every entry point below names the
+ * reference function it replaces.
+ *
+ * Conventions
+ *   - Plain C types only. Pointers prefixed d_ are DEVICE pointers (caller
+ *     owned, any allocator); pointers prefixed h_ are HOST pointers. Control
+ *     data (thresholds, serve table) is host-side: it is at most C*R doubles and
+ *     the library derives its device tables from it.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *     Every call is asynchronous with respect to the host unless stated.
+ *   - Return value: 0 on success, a negative EE_ERR_* code otherwise;
+ *     ee_last_error() returns a thread-local message for the last failure.
+ *     Shapes are validated here; nothing is undefined behaviour (the Cython
+ *     reference silently reads out of bounds on a short threshold vector).
+ *   - Semantics (pkg/src/eesim/_kernels/_ref.py:1-6, _exitcore.pyx:19-21):
+ *     a record exits at the first ramp j with scores[i,j] < thresholds[j]
+ *     (strict IEEE compare, so NaN never exits); site R means "no exit".
+ */
+#ifndef EEB200_H
+#define EEB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EE_OK 0
+#define EE_ERR_ARG (-1)        /* bad shape / size / null pointer */
+#define EE_ERR_CUDA (-2)       /* CUDA runtime failure */
+#define EE_ERR_NOT_BINARY (-3) /* correct_ext holds a value other than 0.0 / 1.0 */
+#define EE_ERR_RAMPS (-4)      /* more ramps than the kernels support (R > 31) */
+
+#define EE_MODE_AUTO 0  /* exact below EE_EXACT_N_MAX samples, histogram above */
+#define EE_MODE_EXACT 1 /* per-candidate in-order fp64 sums: bit-identical to _exitcore.pyx:43-55 */
+#define EE_MODE_HIST 2  /* integer exit-site histograms; acc exact, sav exactly rounded */
+#define EE_EXACT_N_MAX 4096
+
+#define EE_MAX_RAMPS 31
+
+typedef struct ee_workspace ee_workspace;
+
+/* Library / device information. */
+const char* ee_version(void);
+const char* ee_last_error(void);
+int ee_device_sm_count(int32_t* out_sms);
+
+/* Scratch owner: device buffers for keys, histograms and threshold tables, a
+ * pinned staging area and an event. One workspace per host thread (calls on
+ * one workspace are serialised by an internal mutex). */
+int ee_workspace_create(ee_workspace** out);
+int ee_workspace_destroy(ee_workspace* ws);
+
+/* Replaces _exitcore.exit_sites (pkg/src/eesim/_kernels/_exitcore.pyx:11-24)
+ * and _ref.exit_sites (_ref.py:17-27).
+ *   d_scores  f64 [n, r] row-major, d_th f64 [r], d_out i64 [n] in [0, r]. */
+int ee_exit_sites(const double* d_scores, int64_t n, int32_t r, const double* d_th,
+                  int64_t* d_out, void* stream);
+
+/* Packs the reference's correctness matrix correct_ext f64 [n, r1] (r1 = r+1,
+ * built at pkg/src/eesim/engine.py:154-159) into one uint32 bit row per
+ * sample (bit j = column j). Every entry must be exactly 0.0 or 1.0; any other
+ * value sets *d_flag to 1 (the host maps that to EE_ERR_NOT_BINARY). */
+int ee_pack_correct(const double* d_correct_ext, int64_t n, int32_t r1, uint32_t* d_bits,
+                    int32_t* d_flag, void* stream);
+
+/* Replaces engine.decision_scores (pkg/src/eesim/engine.py:106-121) for k > 1:
+ * trailing mean of the last k active-ramp scores via the same cumulative-sum
+ * difference, bit-identical to numpy. d_out may alias nothing. */
+int ee_decision_scores(const double* d_errs, int64_t n, int32_t r, int32_t k, double* d_out,
+                       void* stream);
+
+/* Replaces _exitcore.eval_thresholds (pkg/src/eesim/_kernels/_exitcore.pyx:27-56),
+ * _ref.eval_thresholds (_ref.py:30-62) as called by
+ * WindowEvaluator.evaluate_many (pkg/src/eesim/engine.py:165-170).
+ *   d_scores  f64 [n, r]; d_bits u32 [n] (from ee_pack_correct, r+1 columns)
+ *   h_serve   f64 [r+1] (engine._serve_table, engine.py:124-132), vanilla f64
+ *   h_th      f64 [c, r] candidate threshold rows
+ *   outputs (device, nullable except acc/sav):
+ *     d_hist  i64 [c, r+1] exit-site histogram (HIST mode only; zero-filled in EXACT)
+ *     d_ok    i64 [c]      correct releases
+ *     d_acc   f64 [c]      ok / n
+ *     d_sav   f64 [c]      vanilla - (sum_i serve[site_i]) / n
+ * n == 0 yields NaN acc/sav exactly like the reference's 0/0. */
+int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits,
+                       int64_t n, int32_t r, const double* h_serve, double vanilla,
+                       const double* h_th, int64_t c, int32_t mode, int64_t* d_hist,
+                       int64_t* d_ok, double* d_acc, double* d_sav, void* stream);
+
+/* Scores the full lattice vals^r in lexicographic (meshgrid 'ij') row order
+ * without materialising it — the candidate set of tuner.grid_oracle
+ * (pkg/src/eesim/tuner.py:213-223) — and returns acc/sav per lattice point
+ * (device, length L^r), computed in EXACT mode. h_vals must be ascending. */
+int ee_eval_lattice(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                    int32_t r, const double* h_serve, double vanilla, const double* h_vals,
+                    int32_t n_vals, double* d_acc, double* d_sav, void* stream);
+
+/* Finalises externally reduced histograms (e.g. after an all-reduce across
+ * ranks of per-shard d_hist/d_ok from ee_eval_thresholds in HIST mode):
+ * d_hist i64 [c, r+1], d_ok i64 [c], n = total samples -> d_acc, d_sav with
+ * the same arithmetic as HIST mode (acc = ok/n, exactly rounded savings). */
+int ee_finalize_hist(ee_workspace* ws, const int64_t* d_hist, const int64_t* d_ok, int64_t c,
+                     int32_t r, int64_t n, const double* h_serve, double vanilla, double* d_acc,
+                     double* d_sav, void* stream);
+
+/* Per-launch timing: while enabled, every kernel launched through `ws` is
+ * bracketed by CUDA events on its stream. ee_profile_read synchronises, writes
+ * {"kernel": {"launches": L, "ms": T}, ...} (JSON) into buf and resets. */
+int ee_profile_enable(ee_workspace* ws, int32_t on);
+int ee_profile_read(ee_workspace* ws, char* buf, int64_t cap);
+
+/* Host-side columnar window ingest (no GPU): replays the reference workload
+ * generator (pkg/src/eesim/trace.py:164-227) over a caller-provided raw PCG64
+ * stream (numpy Generator.bit_generator.random_raw), writing errs f64 [n, s],
+ * labels i32 [n, s] and finals i32 [n] for records [t_begin, *t_end). Stops
+ * early (returning *t_end < n) when the raw buffer runs out; the io_* stream
+ * state is updated so the caller can refill and resume. */
+int ee_synth_columns(const uint64_t* raw, int64_t n_raw, int64_t* io_pos, int32_t* io_has32,
+                     uint32_t* io_buf, const double* u, int64_t n, int64_t t_begin,
+                     int64_t* t_end, double* io_d_prev, int32_t n_sites, const double* agree_early,
+                     const double* agree_late, int32_t use_late, double continuity, double miscal,
+                     double miscal_late, int32_t n_labels, double* errs, int32_t* labels,
+                     int32_t* finals);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EEB200_H */

@@ -1,0 +1,977 @@
+// eeb200.cu — sm_100a kernels behind the C ABI in include/eeb200.h.
+//
+// The path replaced is the exit-decision scan of the reference `eesim`
+// (pkg/src/eesim/_kernels/_exitcore.pyx:11-56, _ref.py:17-62) and its callers'
+// arithmetic (engine.decision_scores, engine.py:106-121). See DESIGN.md for the
+// data layout and the roofline of every kernel.
+//
+// Kernels
+//   k_exit_sites        K1  first-exit index per sample (one config)
+//   k_pack_correct          correct_ext f64 [n, r+1] -> u32 bit rows
+//   k_decision_scores   K3  trailing k-mean (bit-identical to numpy)
+//   k_eval_exact        K2e candidate-parallel, sample-sequential fp64 sums
+//                           (bit-identical to the Cython loop order)
+//   k_keys              K2a fp64 score -> 7-bit bucket key per (sample, ramp)
+//   k_count             K2b SWAR first-exit histograms, 4 candidates / 32-bit word
+//   k_finalize          K2c histograms -> acc / sav (exactly rounded)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/eeb200.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define EE_CUDA(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(EE_ERR_CUDA, std::string(#x) + " failed: " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define EE_LAUNCH_CHECK()                                                                \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(EE_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+int g_sms = 0;
+
+int sm_count() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// K1: exit_sites. One thread per sample, strict fp64 compare, early break.
+// Reference: _exitcore.pyx:11-24 (loop), _ref.py:17-27 (r == 0 -> zeros).
+// ---------------------------------------------------------------------------
+__global__ void k_exit_sites(const double* __restrict__ s, int64_t n, int r,
+                             const double* __restrict__ th, int64_t* __restrict__ out) {
+  extern __shared__ double sth[];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) sth[j] = th[j];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double* row = s + i * r;
+    int site = r;
+    for (int j = 0; j < r; ++j) {
+      if (__ldg(row + j) < sth[j]) {
+        site = j;
+        break;
+      }
+    }
+    out[i] = site;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// correct_ext f64 [n, r1] -> bit rows. engine.py:154-159 builds correct_ext
+// with 0.0/1.0 only; anything else is rejected rather than silently rounded.
+// ---------------------------------------------------------------------------
+__global__ void k_pack_correct(const double* __restrict__ c, int64_t n, int r1,
+                               uint32_t* __restrict__ bits, int* __restrict__ flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint32_t b = 0;
+    bool bad = false;
+    for (int j = 0; j < r1; ++j) {
+      double v = c[i * r1 + j];
+      if (v == 1.0)
+        b |= 1u << j;
+      else if (v != 0.0)
+        bad = true;
+    }
+    bits[i] = b;
+    if (bad) atomicOr(flag, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: decision scores, engine.py:106-121. csum is numpy's sequential
+// add.accumulate along the row; out[j] = (csum[j] - csum[lo-1]) / width with
+// lo = max(0, j-k+1). Computed right-to-left in place over the cumulative sums
+// so the subtrahend is still a cumulative sum. _rn intrinsics forbid FMA
+// contraction so every operation rounds exactly as numpy's does.
+// ---------------------------------------------------------------------------
+__global__ void k_decision_scores(const double* __restrict__ e, int64_t n, int r, int k,
+                                  double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double* row = e + i * r;
+    double* o = out + i * r;
+    double acc = 0.0;
+    for (int j = 0; j < r; ++j) {
+      acc = (j == 0) ? row[0] : __dadd_rn(acc, row[j]);
+      o[j] = acc;
+    }
+    for (int j = r - 1; j >= 0; --j) {
+      int lo = j - k + 1;
+      if (lo < 0) lo = 0;
+      const double width = (double)(j - lo + 1);
+      const double sub = lo > 0 ? o[lo - 1] : 0.0;
+      o[j] = __ddiv_rn(__dsub_rn(o[j], sub), width);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2e: exact evaluation. Candidate-parallel, sample-sequential: every CTA owns
+// `cpb` candidates; sample tiles are staged in shared memory, all threads find
+// first-exit sites for (candidate, sample) pairs in parallel, then one thread
+// per candidate folds the tile in sample order:
+//     ok += correct[i, site];  ms = ms + serve[site]        (_exitcore.pyx:43-53)
+// and finally acc = ok / n, sav = vanilla - ms / n (_exitcore.pyx:54-55).
+// Same IEEE operations in the same order -> bit-identical to the Cython path.
+// Threshold rows come either from a dense matrix or from a lattice index.
+// ---------------------------------------------------------------------------
+
+template <bool LATTICE>
+__global__ void k_eval_exact(const double* __restrict__ s, const uint32_t* __restrict__ bits,
+                             int64_t n, int r, const double* __restrict__ serve, double vanilla,
+                             const double* __restrict__ th, const double* __restrict__ vals,
+                             int n_vals, int64_t C, int cpb, int T, int tstride,
+                             int64_t* __restrict__ ok_out, double* __restrict__ acc,
+                             double* __restrict__ sav) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sth = reinterpret_cast<double*>(smem);        // [cpb][r]
+  double* sserve = sth + (size_t)cpb * r;               // [r+1]
+  double* sscore = sserve + (r + 1);                    // [T][r]
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(sscore + (size_t)T * r);  // [T]
+  unsigned char* ssite = reinterpret_cast<unsigned char*>(sbits + T);      // [cpb][tstride]
+
+  const int64_t c0 = (int64_t)blockIdx.x * cpb;
+  const int nc = (int)imin64((int64_t)cpb, C - c0);
+  for (int idx = threadIdx.x; idx < nc * r; idx += blockDim.x) {
+    const int cl = idx / r, j = idx % r;
+    double t;
+    if (LATTICE) {
+      // lexicographic meshgrid('ij') order: digit of ramp 0 is most significant
+      int64_t q = c0 + cl;
+      for (int jj = r - 1; jj > j; --jj) q /= n_vals;
+      t = vals[q % n_vals];
+    } else {
+      t = th[(c0 + cl) * r + j];
+    }
+    sth[idx] = t;
+  }
+  for (int j = threadIdx.x; j <= r; j += blockDim.x) sserve[j] = serve[j];
+
+  int64_t ok = 0;
+  double ms = 0.0;
+  for (int64_t base = 0; base < n; base += T) {
+    const int tn = (int)imin64((int64_t)T, n - base);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < tn * r; idx += blockDim.x) sscore[idx] = s[base * r + idx];
+    for (int idx = threadIdx.x; idx < tn; idx += blockDim.x) sbits[idx] = bits[base + idx];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nc * tn; idx += blockDim.x) {
+      const int cl = idx / tn, i = idx % tn;
+      const double* row = sscore + (size_t)i * r;
+      const double* t = sth + (size_t)cl * r;
+      int site = r;
+      for (int j = 0; j < r; ++j) {
+        if (row[j] < t[j]) {
+          site = j;
+          break;
+        }
+      }
+      ssite[cl * tstride + i] = (unsigned char)site;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      const unsigned char* sites = ssite + threadIdx.x * tstride;
+      for (int i = 0; i < tn; ++i) {
+        const int site = sites[i];
+        ok += (sbits[i] >> site) & 1u;
+        ms = __dadd_rn(ms, sserve[site]);
+      }
+    }
+  }
+  if (threadIdx.x < nc) {
+    const int64_t c = c0 + threadIdx.x;
+    const double dn = (double)n;
+    if (ok_out) ok_out[c] = ok;
+    acc[c] = __ddiv_rn((double)ok, dn);
+    sav[c] = __dsub_rn(vanilla, __ddiv_rn(ms, dn));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2a: bucket keys. For ramp j the candidate chunk has m_j <= 127 distinct
+// non-NaN thresholds u_j[0] < ... < u_j[m_j-1]. key(s) = #{k : u_j[k] <= s}
+// (NaN -> 127). Then  s < t  <=>  key(s) <= pos(t)  with pos(t) the index of
+// t in u_j, so the exit test becomes a 7-bit integer compare.
+// Thread per (sample, padded ramp); scores are read fully coalesced.
+// ---------------------------------------------------------------------------
+constexpr int KEY_SLOTS = 128;  // per-ramp table size (NaN padded)
+
+__global__ void k_keys(const double* __restrict__ s, int64_t n, int r, int rp,
+                       const double* __restrict__ utab, uint8_t* __restrict__ keys) {
+  extern __shared__ double su[];  // [r][KEY_SLOTS]
+  for (int idx = threadIdx.x; idx < r * KEY_SLOTS; idx += blockDim.x) su[idx] = utab[idx];
+  __syncthreads();
+  const int64_t total = n * rp;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t i = e / rp;
+    const int j = (int)(e - i * rp);
+    uint32_t b = 0;
+    if (j < r) {
+      const double v = __ldg(s + i * r + j);
+      const double* u = su + j * KEY_SLOTS;
+      // branchless upper_bound over 128 NaN-padded slots
+#pragma unroll
+      for (int step = 64; step >= 1; step >>= 1)
+        if (u[b + step - 1] <= v) b += step;
+      if (v != v) b = 127;
+    }
+    keys[e] = (uint8_t)b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2b: SWAR first-exit histograms.
+// A 32-bit word packs 4 candidates; byte q of P[w][j] is 0x80 + pos_j(c) (or
+// 0x7F for "never", i.e. NaN thresholds and padding). With the sample key b
+// broadcast into all 4 bytes, (P - B) has bit 7 of byte q set iff pos >= b,
+// i.e. iff the candidate's threshold exceeds the score — no borrow crosses a
+// byte because 0x80 + pos - b >= 1. A per-word `alive` mask keeps only the
+// first exit; byte counters accumulate (E >> 7) and are flushed to shared
+// memory before they can overflow (255). One CTA handles a 64-candidate block
+// and steals 256-sample tiles from a global counter.
+// ---------------------------------------------------------------------------
+constexpr int CB = 64;       // candidates per block
+constexpr int CB_WORDS = 16; // 32-bit words per block
+constexpr int TS = 256;      // samples per tile
+constexpr int COUNT_THREADS = 256;
+
+template <int RW, int WPT>
+__global__ void __launch_bounds__(COUNT_THREADS, 2)
+    k_count(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ bits, int64_t n,
+            int r, const uint32_t* __restrict__ pwords, unsigned long long* __restrict__ hist,
+            unsigned long long* __restrict__ okc, unsigned int* __restrict__ tile_ctr,
+            int64_t ncand) {
+  constexpr int RMAX = 4 * RW;
+  constexpr int NSLOT = RMAX + 2;  // RMAX ramps, "no exit", ok
+  constexpr int WG = CB_WORDS / WPT;
+  constexpr int SG = COUNT_THREADS / WG;
+  constexpr int SPT = TS / SG;  // samples per thread per tile
+  __shared__ uint32_t skeys[TS * RW];
+  __shared__ uint32_t sbits[TS];
+  __shared__ uint32_t shist[CB * NSLOT];
+  __shared__ int64_t stile;
+
+  const int cb = blockIdx.y;
+  const int wg = threadIdx.x % WG;
+  const int sg = threadIdx.x / WG;
+
+  uint32_t P[WPT][RMAX];
+#pragma unroll
+  for (int w = 0; w < WPT; ++w)
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j)
+      P[w][j] = pwords[((size_t)cb * CB_WORDS + wg * WPT + w) * RMAX + j];
+
+  for (int idx = threadIdx.x; idx < CB * NSLOT; idx += COUNT_THREADS) shist[idx] = 0;
+
+  uint32_t cnt[WPT][RMAX + 1];
+  uint32_t okb[WPT];
+#pragma unroll
+  for (int w = 0; w < WPT; ++w) {
+    okb[w] = 0;
+#pragma unroll
+    for (int j = 0; j <= RMAX; ++j) cnt[w][j] = 0;
+  }
+  int pending = 0;
+
+  auto flush = [&]() {
+#pragma unroll
+    for (int w = 0; w < WPT; ++w) {
+      const int cbase = (wg * WPT + w) * 4;
+#pragma unroll
+      for (int j = 0; j <= RMAX; ++j) {
+        const uint32_t v = cnt[w][j];
+        if (v) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t x = (v >> (8 * q)) & 0xFFu;
+            if (x) atomicAdd(&shist[(cbase + q) * NSLOT + j], x);
+          }
+        }
+        cnt[w][j] = 0;
+      }
+      const uint32_t v = okb[w];
+      if (v) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t x = (v >> (8 * q)) & 0xFFu;
+          if (x) atomicAdd(&shist[(cbase + q) * NSLOT + RMAX + 1], x);
+        }
+      }
+      okb[w] = 0;
+    }
+  };
+
+  const int64_t ntiles = ceil_div(n, TS);
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) stile = (int64_t)atomicAdd(tile_ctr + cb, 1u);
+    __syncthreads();
+    const int64_t tile = stile;
+    if (tile >= ntiles) break;
+    const int64_t base = tile * TS;
+    const int tn = (int)imin64((int64_t)TS, n - base);
+    // stage keys (tn*RW words, contiguous) and correctness bits
+    const uint32_t* gk = keys + base * RW;
+    for (int idx = threadIdx.x; idx < tn * RW; idx += COUNT_THREADS) skeys[idx] = gk[idx];
+    for (int idx = threadIdx.x; idx < tn; idx += COUNT_THREADS) sbits[idx] = bits[base + idx];
+    __syncthreads();
+
+    if (pending + SPT > 255) {
+      flush();
+      pending = 0;
+    }
+    pending += SPT;
+#pragma unroll 1
+    for (int i = sg; i < tn; i += SG) {
+      uint32_t kw[RW];
+#pragma unroll
+      for (int q = 0; q < RW; ++q) kw[q] = skeys[i * RW + q];
+      const uint32_t cbits = sbits[i];
+      uint32_t alive[WPT], okw[WPT];
+#pragma unroll
+      for (int w = 0; w < WPT; ++w) {
+        alive[w] = 0x80808080u;
+        okw[w] = 0;
+      }
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j) {
+        const uint32_t B = __byte_perm(kw[j >> 2], 0, (j & 3) * 0x1111);
+        const uint32_t Cm = (uint32_t)((int32_t)(cbits << (31 - j)) >> 31);
+#pragma unroll
+        for (int w = 0; w < WPT; ++w) {
+          const uint32_t d = P[w][j] - B;
+          const uint32_t E = d & alive[w];
+          alive[w] &= ~d;
+          cnt[w][j] += E >> 7;
+          okw[w] |= E & Cm;
+        }
+      }
+      const uint32_t CR = (uint32_t)(-(int32_t)((cbits >> r) & 1u));
+#pragma unroll
+      for (int w = 0; w < WPT; ++w) {
+        cnt[w][RMAX] += alive[w] >> 7;
+        okw[w] |= alive[w] & CR;
+        okb[w] += okw[w] >> 7;
+      }
+    }
+  }
+  flush();
+  __syncthreads();
+  const int64_t cglob = (int64_t)cb * CB;
+  for (int idx = threadIdx.x; idx < CB * NSLOT; idx += COUNT_THREADS) {
+    const int cl = idx / NSLOT, slot = idx % NSLOT;
+    const int64_t c = cglob + cl;
+    const uint32_t v = shist[idx];
+    if (c < ncand && v) {
+      if (slot == RMAX + 1)
+        atomicAdd(okc + c, (unsigned long long)v);
+      else
+        atomicAdd(hist + c * (RMAX + 1) + slot, (unsigned long long)v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2c: finalize. hist slot RMAX is the "no exit" site r. acc = ok / n exactly as
+// the reference (ok is an exact integer there too). The serve-time total
+// sum_j cnt_j * serve_j is accumulated error-free (TwoProduct via FMA +
+// TwoSum) and rounded once, so it is the correctly rounded total; the
+// reference's sequential sum differs from it by its own rounding.
+// ---------------------------------------------------------------------------
+__device__ inline void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+__global__ void k_finalize(const unsigned long long* __restrict__ hist,
+                           const unsigned long long* __restrict__ okc, int64_t C, int r,
+                           int rmax, int64_t n, const double* __restrict__ serve,
+                           double vanilla, int64_t* __restrict__ hist_out,
+                           int64_t* __restrict__ ok_out, double* __restrict__ acc,
+                           double* __restrict__ sav) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const unsigned long long* h = hist + c * (rmax + 1);
+  double hi = 0.0, lo = 0.0;
+  for (int site = 0; site <= r; ++site) {
+    const unsigned long long cnt = (site == r) ? h[rmax] : h[site];
+    if (hist_out) hist_out[c * (r + 1) + site] = (int64_t)cnt;
+    const double x = (double)cnt;
+    const double p = __dmul_rn(x, serve[site]);
+    const double pe = __fma_rn(x, serve[site], -p);
+    double s, e;
+    two_sum(hi, p, s, e);
+    hi = s;
+    lo = __dadd_rn(lo, __dadd_rn(e, pe));
+  }
+  double s, e;
+  two_sum(hi, lo, s, e);
+  const double dn = (double)n;
+  const unsigned long long ok = okc[c];
+  if (ok_out) ok_out[c] = (int64_t)ok;
+  acc[c] = __ddiv_rn((double)ok, dn);
+  sav[c] = __dsub_rn(vanilla, __ddiv_rn(s, dn));
+}
+
+__global__ void k_fill_nan(double* a, double* b, int64_t C) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) {
+    a[c] = __longlong_as_double(0x7ff8000000000000LL);
+    b[c] = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Workspace
+// ---------------------------------------------------------------------------
+struct ee_workspace {
+  std::mutex mu;
+  void* d_buf = nullptr;  // device scratch
+  size_t d_cap = 0;
+  void* h_stage = nullptr;  // pinned staging for threshold tables
+  size_t h_cap = 0;
+  cudaEvent_t staged = nullptr;  // last async copy out of h_stage
+  // optional per-launch timing (ee_profile_enable): events bracket every kernel
+  // this workspace launches, on the launching stream
+  bool profiling = false;
+  struct Mark {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Mark> marks;
+};
+
+namespace {
+
+struct ProfScope {
+  ee_workspace* ws;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  const char* name;
+  ProfScope(ee_workspace* w, cudaStream_t s, const char* n) : ws(w), st(s), name(n) {
+    if (ws && ws->profiling) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      ws->marks.push_back({name, a, b});
+    }
+  }
+};
+
+}  // namespace
+
+namespace {
+
+int ws_reserve(ee_workspace* ws, size_t dev_bytes, size_t host_bytes) {
+  if (dev_bytes > ws->d_cap) {
+    if (ws->d_buf) EE_CUDA(cudaFree(ws->d_buf));
+    ws->d_buf = nullptr;
+    size_t cap = std::max(dev_bytes, ws->d_cap * 2);
+    EE_CUDA(cudaMalloc(&ws->d_buf, cap));
+    ws->d_cap = cap;
+  }
+  if (ws->staged) EE_CUDA(cudaEventSynchronize(ws->staged));
+  if (host_bytes > ws->h_cap) {
+    if (ws->h_stage) EE_CUDA(cudaFreeHost(ws->h_stage));
+    ws->h_stage = nullptr;
+    size_t cap = std::max(host_bytes, ws->h_cap * 2);
+    EE_CUDA(cudaHostAlloc(&ws->h_stage, cap, cudaHostAllocDefault));
+    ws->h_cap = cap;
+  }
+  if (!ws->staged) EE_CUDA(cudaEventCreateWithFlags(&ws->staged, cudaEventDisableTiming));
+  return EE_OK;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Sort key that makes -0.0 and +0.0 one value (they compare equal).
+inline double canon(double v) { return v == 0.0 ? 0.0 : v; }
+
+struct Chunk {
+  int64_t c0, c1;  // candidate rows [c0, c1)
+};
+
+// Greedy row chunks whose per-ramp distinct non-NaN count stays <= 127.
+std::vector<Chunk> make_chunks(const double* th, int64_t C, int r) {
+  std::vector<Chunk> out;
+  std::vector<std::unordered_set<uint64_t>> seen(r);
+  int64_t start = 0;
+  for (int64_t c = 0; c < C; ++c) {
+    bool fits = true;
+    for (int j = 0; j < r && fits; ++j) {
+      const double v = th[c * r + j];
+      if (v != v) continue;
+      double cv = canon(v);
+      uint64_t key;
+      std::memcpy(&key, &cv, 8);
+      if (!seen[j].count(key) && seen[j].size() >= 127) fits = false;
+    }
+    if (!fits) {
+      out.push_back({start, c});
+      start = c;
+      for (auto& s : seen) s.clear();
+    }
+    for (int j = 0; j < r; ++j) {
+      const double v = th[c * r + j];
+      if (v != v) continue;
+      double cv = canon(v);
+      uint64_t key;
+      std::memcpy(&key, &cv, 8);
+      seen[j].insert(key);
+    }
+  }
+  out.push_back({start, C});
+  return out;
+}
+
+template <int RW, int WPT>
+int launch_count(const uint32_t* keys, const uint32_t* bits, int64_t n, int r,
+                 const uint32_t* pw, unsigned long long* hist, unsigned long long* okc,
+                 unsigned int* ctr, int64_t ncand, int ncb, cudaStream_t st) {
+  const int64_t ntiles = ceil_div(n, TS);
+  int64_t gx = std::max<int64_t>(1, (int64_t)sm_count() * 2 / ncb);
+  gx = imin64(gx, ntiles);
+  dim3 grid((unsigned)gx, (unsigned)ncb);
+  k_count<RW, WPT><<<grid, COUNT_THREADS, 0, st>>>(keys, bits, n, r, pw, hist, okc, ctr, ncand);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int dispatch_count(int rw, const uint32_t* keys, const uint32_t* bits, int64_t n, int r,
+                   const uint32_t* pw, unsigned long long* hist, unsigned long long* okc,
+                   unsigned int* ctr, int64_t ncand, int ncb, cudaStream_t st) {
+  switch (rw) {
+    case 1: return launch_count<1, 4>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    case 2: return launch_count<2, 4>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    case 3: return launch_count<3, 4>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    case 4: return launch_count<4, 4>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    case 5: return launch_count<5, 2>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    case 6: return launch_count<6, 2>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    case 7: return launch_count<7, 2>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    case 8: return launch_count<8, 2>(keys, bits, n, r, pw, hist, okc, ctr, ncand, ncb, st);
+    default: return fail(EE_ERR_RAMPS, "unsupported ramp count");
+  }
+}
+
+int exact_layout(int64_t n, int r, int64_t C, int* cpb, int* T, int* tstride, size_t* smem) {
+  int cp = (int)imin64(C, 256);
+  if (cp < 1) cp = 1;
+  // budget ~96 KB: thresholds cp*r*8 + serve + tile T*(8r + 4 + cp)
+  const size_t fixed = (size_t)cp * r * 8 + (size_t)(r + 1) * 8;
+  const size_t budget = 96 * 1024;
+  if (fixed + 64 * (8 * r + 4 + cp + 1) > budget) return fail(EE_ERR_RAMPS, "tile does not fit");
+  int64_t t = (int64_t)((budget - fixed) / (size_t)(8 * r + 4 + cp + 1));
+  t = imin64(t, 4096);
+  t = std::max<int64_t>(t, 32);
+  t = imin64(t, std::max<int64_t>(n, 1));
+  *cpb = cp;
+  *T = (int)t;
+  *tstride = (int)(t | 1);
+  *smem = fixed + (size_t)t * r * 8 + (size_t)t * 4 + (size_t)cp * (t | 1);
+  *smem = align_up(*smem, 16);
+  return EE_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* ee_version(void) { return "eeb200 0.1.0 sm_100a"; }
+
+const char* ee_last_error(void) { return g_err.c_str(); }
+
+int ee_device_sm_count(int32_t* out) {
+  if (!out) return fail(EE_ERR_ARG, "null output");
+  *out = sm_count();
+  return EE_OK;
+}
+
+int ee_workspace_create(ee_workspace** out) {
+  if (!out) return fail(EE_ERR_ARG, "null output");
+  *out = new ee_workspace();
+  return EE_OK;
+}
+
+int ee_workspace_destroy(ee_workspace* ws) {
+  if (!ws) return EE_OK;
+  if (ws->staged) cudaEventSynchronize(ws->staged);
+  if (ws->d_buf) cudaFree(ws->d_buf);
+  if (ws->h_stage) cudaFreeHost(ws->h_stage);
+  if (ws->staged) cudaEventDestroy(ws->staged);
+  delete ws;
+  return EE_OK;
+}
+
+int ee_exit_sites(const double* d_scores, int64_t n, int32_t r, const double* d_th,
+                  int64_t* d_out, void* stream) {
+  if (n < 0 || r < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (n == 0) return EE_OK;
+  if (!d_out || (r > 0 && (!d_scores || !d_th))) return fail(EE_ERR_ARG, "null pointer");
+  auto st = (cudaStream_t)stream;
+  const int threads = 256;
+  const int64_t blocks = imin64(ceil_div(n, threads), (int64_t)sm_count() * 16);
+  k_exit_sites<<<(unsigned)blocks, threads, (size_t)std::max(r, 1) * 8, st>>>(d_scores, n, r, d_th,
+                                                                            d_out);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_pack_correct(const double* d_correct_ext, int64_t n, int32_t r1, uint32_t* d_bits,
+                    int32_t* d_flag, void* stream) {
+  if (n < 0 || r1 < 1) return fail(EE_ERR_ARG, "bad shape");
+  if (r1 > EE_MAX_RAMPS + 1) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (n == 0) return EE_OK;
+  if (!d_correct_ext || !d_bits || !d_flag) return fail(EE_ERR_ARG, "null pointer");
+  auto st = (cudaStream_t)stream;
+  const int threads = 256;
+  const int64_t blocks = imin64(ceil_div(n, threads), (int64_t)sm_count() * 16);
+  k_pack_correct<<<(unsigned)blocks, threads, 0, st>>>(d_correct_ext, n, r1, d_bits, d_flag);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_decision_scores(const double* d_errs, int64_t n, int32_t r, int32_t k, double* d_out,
+                       void* stream) {
+  if (n < 0 || r < 0 || k < 1) return fail(EE_ERR_ARG, "bad shape");
+  if (n == 0 || r == 0) return EE_OK;
+  if (!d_errs || !d_out) return fail(EE_ERR_ARG, "null pointer");
+  auto st = (cudaStream_t)stream;
+  const int threads = 256;
+  const int64_t blocks = imin64(ceil_div(n, threads), (int64_t)sm_count() * 16);
+  k_decision_scores<<<(unsigned)blocks, threads, 0, st>>>(d_errs, n, r, k, d_out);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+static int eval_exact(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                      int r, const double* h_serve, double vanilla, const double* h_th,
+                      const double* h_vals, int n_vals, int64_t C, int64_t* d_hist,
+                      int64_t* d_ok, double* d_acc, double* d_sav, cudaStream_t st) {
+  const bool lattice = h_vals != nullptr;
+  const size_t th_bytes = lattice ? (size_t)n_vals * 8 : (size_t)C * r * 8;
+  const size_t serve_off = align_up(th_bytes, 256);
+  const size_t need = serve_off + align_up((size_t)(r + 1) * 8, 256);
+  int rc = ws_reserve(ws, need, need);
+  if (rc) return rc;
+  auto* hs = static_cast<unsigned char*>(ws->h_stage);
+  std::memcpy(hs, lattice ? h_vals : h_th, th_bytes);
+  std::memcpy(hs + serve_off, h_serve, (size_t)(r + 1) * 8);
+  EE_CUDA(cudaMemcpyAsync(ws->d_buf, hs, need, cudaMemcpyHostToDevice, st));
+  EE_CUDA(cudaEventRecord(ws->staged, st));
+  auto* dbase = static_cast<unsigned char*>(ws->d_buf);
+  const double* d_th = reinterpret_cast<const double*>(dbase);
+  const double* d_serve = reinterpret_cast<const double*>(dbase + serve_off);
+  if (d_hist) EE_CUDA(cudaMemsetAsync(d_hist, 0, (size_t)C * (r + 1) * 8, st));
+
+  int cpb, T, tstride;
+  size_t smem;
+  rc = exact_layout(n, r, C, &cpb, &T, &tstride, &smem);
+  if (rc) return rc;
+  const int64_t blocks = ceil_div(C, cpb);
+  if (blocks > 0x7fffffff) return fail(EE_ERR_ARG, "too many candidates");
+  ProfScope ps(ws, st, "k_eval_exact");
+  if (lattice) {
+    EE_CUDA(cudaFuncSetAttribute(k_eval_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_eval_exact<true><<<(unsigned)blocks, 256, smem, st>>>(d_scores, d_bits, n, r, d_serve,
+                                                           vanilla, nullptr, d_th, n_vals, C, cpb,
+                                                           T, tstride, d_ok, d_acc, d_sav);
+  } else {
+    EE_CUDA(cudaFuncSetAttribute(k_eval_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_eval_exact<false><<<(unsigned)blocks, 256, smem, st>>>(d_scores, d_bits, n, r, d_serve,
+                                                            vanilla, d_th, nullptr, 0, C, cpb, T,
+                                                            tstride, d_ok, d_acc, d_sav);
+  }
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                     int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
+                     int64_t* d_hist, int64_t* d_ok, double* d_acc, double* d_sav,
+                     cudaStream_t st) {
+  const int rw = std::max(1, (r + 3) / 4);
+  const int rp = 4 * rw;
+  const int rmax = rp;
+  std::vector<Chunk> chunks = make_chunks(h_th, C, r);
+
+  // device layout: [hist u64 C*(rmax+1)][ok u64 C][ctr u32 per block per chunk]
+  //                [keys u8 n*rp][serve f64 r+1][per chunk: utab f64 r*128, pwords u32]
+  int64_t total_blocks = 0;
+  for (auto& ch : chunks) total_blocks += ceil_div(ch.c1 - ch.c0, CB);
+  const size_t hist_b = align_up((size_t)C * (rmax + 1) * 8, 256);
+  const size_t ok_b = align_up((size_t)C * 8, 256);
+  const size_t ctr_b = align_up((size_t)total_blocks * 4, 256);
+  const size_t keys_b = align_up((size_t)n * rp, 256);
+  const size_t serve_b = align_up((size_t)(r + 1) * 8, 256);
+  size_t tab_b = 0;
+  for (auto& ch : chunks) {
+    tab_b += align_up((size_t)std::max(r, 1) * KEY_SLOTS * 8, 256);
+    tab_b += align_up((size_t)ceil_div(ch.c1 - ch.c0, CB) * CB_WORDS * rmax * 4, 256);
+  }
+  const size_t zero_b = hist_b + ok_b + ctr_b;
+  const size_t need = zero_b + keys_b + serve_b + tab_b;
+  const size_t host_need = serve_b + tab_b;
+  int rc = ws_reserve(ws, need, host_need);
+  if (rc) return rc;
+
+  auto* d0 = static_cast<unsigned char*>(ws->d_buf);
+  auto* hist = reinterpret_cast<unsigned long long*>(d0);
+  auto* okc = reinterpret_cast<unsigned long long*>(d0 + hist_b);
+  auto* ctr = reinterpret_cast<unsigned int*>(d0 + hist_b + ok_b);
+  auto* keys = d0 + zero_b;
+  unsigned char* dtab = keys + keys_b;  // serve then tables (mirrors host staging)
+  auto* hs = static_cast<unsigned char*>(ws->h_stage);
+
+  std::memcpy(hs, h_serve, (size_t)(r + 1) * 8);
+  size_t off = serve_b;
+  std::vector<size_t> utab_off, pw_off;
+  std::vector<double> col;
+  for (auto& ch : chunks) {
+    const int64_t cc = ch.c1 - ch.c0;
+    const int64_t nb = ceil_div(cc, CB);
+    double* utab = reinterpret_cast<double*>(hs + off);
+    utab_off.push_back(off);
+    off += align_up((size_t)std::max(r, 1) * KEY_SLOTS * 8, 256);
+    uint32_t* pw = reinterpret_cast<uint32_t*>(hs + off);
+    pw_off.push_back(off);
+    off += align_up((size_t)nb * CB_WORDS * rmax * 4, 256);
+    // padding: 0x7F bytes never exit
+    std::memset(pw, 0x7F, (size_t)nb * CB_WORDS * rmax * 4);
+    for (int j = 0; j < r; ++j) {
+      col.clear();
+      for (int64_t c = ch.c0; c < ch.c1; ++c) {
+        const double v = h_th[c * r + j];
+        if (v == v) col.push_back(canon(v));
+      }
+      std::sort(col.begin(), col.end());
+      col.erase(std::unique(col.begin(), col.end()), col.end());
+      const double qnan = std::numeric_limits<double>::quiet_NaN();
+      for (int k = 0; k < KEY_SLOTS; ++k) utab[j * KEY_SLOTS + k] = k < (int)col.size() ? col[k] : qnan;
+      for (int64_t c = ch.c0; c < ch.c1; ++c) {
+        const double v = h_th[c * r + j];
+        uint8_t code = 0x7F;
+        if (v == v) {
+          const int64_t pos = std::lower_bound(col.begin(), col.end(), canon(v)) - col.begin();
+          code = (uint8_t)(0x80 + pos);
+        }
+        const int64_t cl = c - ch.c0;
+        const int64_t word = cl / 4, q = cl % 4;
+        auto* bytes = reinterpret_cast<uint8_t*>(pw + word * rmax + j);
+        bytes[q] = code;
+      }
+    }
+  }
+  EE_CUDA(cudaMemcpyAsync(dtab, hs, host_need, cudaMemcpyHostToDevice, st));
+  EE_CUDA(cudaEventRecord(ws->staged, st));
+  EE_CUDA(cudaMemsetAsync(d0, 0, zero_b, st));
+  const double* d_serve = reinterpret_cast<const double*>(dtab);
+
+  int64_t blk_off = 0;
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    const Chunk& ch = chunks[ci];
+    const int64_t cc = ch.c1 - ch.c0;
+    if (cc == 0) continue;
+    const int64_t nb = ceil_div(cc, CB);
+    const double* d_utab = reinterpret_cast<const double*>(dtab + utab_off[ci]);
+    const uint32_t* d_pw = reinterpret_cast<const uint32_t*>(dtab + pw_off[ci]);
+    {
+      const int threads = 256;
+      const int64_t total = n * rp;
+      const int64_t blocks = imin64(ceil_div(total, threads), (int64_t)sm_count() * 8);
+      const size_t smem = (size_t)std::max(r, 1) * KEY_SLOTS * 8;
+      if (smem > 48 * 1024)
+        EE_CUDA(cudaFuncSetAttribute(k_keys, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      {
+        ProfScope ps(ws, st, "k_keys");
+        k_keys<<<(unsigned)blocks, threads, smem, st>>>(d_scores, n, r, rp, d_utab, keys);
+      }
+      EE_LAUNCH_CHECK();
+    }
+    ProfScope ps(ws, st, "k_count");
+    rc = dispatch_count(rw, reinterpret_cast<const uint32_t*>(keys), d_bits, n, r, d_pw,
+                        hist + ch.c0 * (rmax + 1), okc + ch.c0, ctr + blk_off, cc, (int)nb, st);
+    if (rc) return rc;
+    blk_off += nb;
+  }
+  {
+    ProfScope ps(ws, st, "k_finalize");
+    k_finalize<<<(unsigned)ceil_div(C, 128), 128, 0, st>>>(hist, okc, C, r, rmax, n, d_serve,
+                                                            vanilla, d_hist, d_ok, d_acc, d_sav);
+  }
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits,
+                       int64_t n, int32_t r, const double* h_serve, double vanilla,
+                       const double* h_th, int64_t c, int32_t mode, int64_t* d_hist,
+                       int64_t* d_ok, double* d_acc, double* d_sav, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (n < 0 || r < 0 || c < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (c == 0) return EE_OK;
+  if (!d_acc || !d_sav || !h_serve) return fail(EE_ERR_ARG, "null pointer");
+  if (n > 0 && (!d_scores && r > 0)) return fail(EE_ERR_ARG, "null scores");
+  if (n > 0 && !d_bits) return fail(EE_ERR_ARG, "null correctness bits");
+  if (r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  if (n == 0) {
+    k_fill_nan<<<(unsigned)ceil_div(c, 256), 256, 0, st>>>(d_acc, d_sav, c);
+    EE_LAUNCH_CHECK();
+    if (d_ok) EE_CUDA(cudaMemsetAsync(d_ok, 0, (size_t)c * 8, st));
+    if (d_hist) EE_CUDA(cudaMemsetAsync(d_hist, 0, (size_t)c * (r + 1) * 8, st));
+    return EE_OK;
+  }
+  int m = mode;
+  if (m == EE_MODE_AUTO) m = (n <= EE_EXACT_N_MAX || r == 0) ? EE_MODE_EXACT : EE_MODE_HIST;
+  if (r == 0) m = EE_MODE_EXACT;
+  if (m == EE_MODE_EXACT)
+    return eval_exact(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, nullptr, 0, c, d_hist,
+                      d_ok, d_acc, d_sav, st);
+  if (m == EE_MODE_HIST)
+    return eval_hist(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, d_hist, d_ok, d_acc,
+                     d_sav, st);
+  return fail(EE_ERR_ARG, "unknown mode");
+}
+
+int ee_finalize_hist(ee_workspace* ws, const int64_t* d_hist, const int64_t* d_ok, int64_t c,
+                     int32_t r, int64_t n, const double* h_serve, double vanilla, double* d_acc,
+                     double* d_sav, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (c < 0 || r < 0 || n < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (c == 0) return EE_OK;
+  if (!d_hist || !d_ok || !h_serve || !d_acc || !d_sav) return fail(EE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  const size_t need = align_up((size_t)(r + 1) * 8, 256);
+  int rc = ws_reserve(ws, need, need);
+  if (rc) return rc;
+  std::memcpy(ws->h_stage, h_serve, (size_t)(r + 1) * 8);
+  EE_CUDA(cudaMemcpyAsync(ws->d_buf, ws->h_stage, need, cudaMemcpyHostToDevice, st));
+  EE_CUDA(cudaEventRecord(ws->staged, st));
+  {
+    ProfScope ps(ws, st, "k_finalize");
+    // histogram rows are dense [c][r+1] here: slot r is the no-exit site
+    k_finalize<<<(unsigned)ceil_div(c, 128), 128, 0, st>>>(
+        reinterpret_cast<const unsigned long long*>(d_hist),
+        reinterpret_cast<const unsigned long long*>(d_ok), c, r, r, n,
+        static_cast<const double*>(ws->d_buf), vanilla, nullptr, nullptr, d_acc, d_sav);
+  }
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_profile_enable(ee_workspace* ws, int32_t on) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  ws->profiling = on != 0;
+  return EE_OK;
+}
+
+int ee_profile_read(ee_workspace* ws, char* buf, int64_t cap) {
+  if (!ws || !buf || cap < 3) return fail(EE_ERR_ARG, "bad arguments");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  struct Agg {
+    std::string name;
+    int64_t launches = 0;
+    double ms = 0.0;
+  };
+  std::vector<Agg> agg;
+  for (auto& m : ws->marks) {
+    EE_CUDA(cudaEventSynchronize(m.b));
+    float ms = 0.f;
+    EE_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+    auto it = std::find_if(agg.begin(), agg.end(), [&](const Agg& x) { return x.name == m.name; });
+    if (it == agg.end()) {
+      agg.push_back({m.name, 0, 0.0});
+      it = agg.end() - 1;
+    }
+    it->launches += 1;
+    it->ms += ms;
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  ws->marks.clear();
+  std::string js = "{";
+  for (size_t i = 0; i < agg.size(); ++i) {
+    char item[256];
+    std::snprintf(item, sizeof item, "%s\"%s\": {\"launches\": %lld, \"ms\": %.6f}",
+                  i ? ", " : "", agg[i].name.c_str(), (long long)agg[i].launches, agg[i].ms);
+    js += item;
+  }
+  js += "}";
+  if ((int64_t)js.size() + 1 > cap) return fail(EE_ERR_ARG, "profile buffer too small");
+  std::memcpy(buf, js.c_str(), js.size() + 1);
+  return EE_OK;
+}
+
+int ee_eval_lattice(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                    int32_t r, const double* h_serve, double vanilla, const double* h_vals,
+                    int32_t n_vals, double* d_acc, double* d_sav, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (n < 1 || r < 1 || n_vals < 1) return fail(EE_ERR_ARG, "bad shape");
+  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (!d_scores || !d_bits || !h_serve || !h_vals || !d_acc || !d_sav)
+    return fail(EE_ERR_ARG, "null pointer");
+  double points = std::pow((double)n_vals, (double)r);
+  if (points > 9.0e15) return fail(EE_ERR_ARG, "lattice too large");
+  int64_t C = 1;
+  for (int j = 0; j < r; ++j) C *= n_vals;
+  std::lock_guard<std::mutex> lock(ws->mu);
+  return eval_exact(ws, d_scores, d_bits, n, r, h_serve, vanilla, nullptr, h_vals, n_vals, C,
+                    nullptr, nullptr, d_acc, d_sav, (cudaStream_t)stream);
+}
+
+}  // extern "C"

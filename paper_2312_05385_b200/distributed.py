@@ -1,0 +1,119 @@
+"""Sample-sharded threshold sweep across GPUs.
+
+Samples are independent, so rank g owns rows [g*N/G, (g+1)*N/G) of the window
+and computes integer exit-site histograms for every candidate on its shard
+(HIST mode). The only exchange is one all-reduce (sum) of C*(R+2) int64
+counters — histograms plus correct counts — over NCCL; every rank then
+finalises identical acc/sav from the global counts, so results are
+bit-identical for any world size. One process per GPU, torch.distributed for
+the plumbing.
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import numpy as np
+
+from paper_2312_05385_b200 import _native as nat
+from paper_2312_05385_b200.engine import WindowEvaluator
+from paper_2312_05385_b200.errors import ParameterError
+from paper_2312_05385_b200.graph import ModelProfile, RampSite
+from paper_2312_05385_b200.trace import WindowArrays
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced [lo, hi) sample range of `rank` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ParameterError(f"bad rank {rank} for world size {world}")
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def reduce_counts(hist, ok, group=None):
+    """Sum per-shard int64 histograms and correct counts across ranks (in place).
+
+    One collective: the two tensors are packed into a single buffer so the
+    exchange is a single all-reduce of C*(R+2) int64."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return hist, ok
+    c, r1 = hist.shape
+    buf = torch.cat([hist.reshape(-1), ok.reshape(-1)])
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf[: c * r1].view(c, r1), buf[c * r1:]
+
+
+class ShardedSweep:
+    """Per-rank device window over this rank's sample shard plus the reduction."""
+
+    def __init__(self, arrays: WindowArrays, sites: Sequence[RampSite], profile: ModelProfile,
+                 *, rank: int = 0, world: int = 1, n_total: int | None = None, group=None,
+                 already_sharded: bool = False):
+        self.n_total = int(n_total if n_total is not None else arrays.n)
+        if not already_sharded:
+            lo, hi = shard_range(arrays.n, rank, world)
+            arrays = WindowArrays(arrays.errs[lo:hi], arrays.correct[lo:hi])
+        self.group = group
+        self.local = WindowEvaluator.from_arrays(arrays, sites, profile, mode="hist")
+        self.r = len(sites)
+
+    def counts(self, thresholds: np.ndarray):
+        """Global (hist [C, R+1], ok [C]) as int64 device tensors."""
+        torch = self.local._torch
+        th = np.ascontiguousarray(thresholds, dtype=np.float64)
+        _, _, ok, hist = self.local._eval_device(th, want_hist=True, mode_code=nat.MODE_HIST)
+        return reduce_counts(hist, ok, self.group)
+
+    def evaluate_many(self, thresholds: np.ndarray, *, to_host: bool = True):
+        torch = self.local._torch
+        hist, ok = self.counts(thresholds)
+        c = hist.shape[0]
+        acc = torch.empty(c, dtype=torch.float64, device="cuda")
+        sav = torch.empty(c, dtype=torch.float64, device="cuda")
+        ev = self.local
+        nat.check(nat.load_library().ee_finalize_hist(
+            nat.workspace(), hist.data_ptr(), ok.data_ptr(), c, self.r, self.n_total,
+            ev.serve.ctypes.data, float(ev.vanilla_ms), acc.data_ptr(), sav.data_ptr(),
+            nat.stream_handle(torch)))
+        if to_host:
+            return acc.cpu().numpy(), sav.cpu().numpy()
+        return acc, sav
+
+
+def eval_thresholds_host_sharded(scores, correct_ext, serve, vanilla, thresholds, *, n_total: int,
+                                 group=None):
+    """Drop-in `eval_thresholds` over this rank's host-resident sample shard:
+    H2D of the shard, per-shard histograms, one all-reduce, identical
+    finalisation on every rank; returns host (acc, sav) for all candidates."""
+    from paper_2312_05385_b200 import kernels
+
+    torch = nat.torch_cuda()
+    lib = nat.load_library()
+    scores = kernels._check_view(scores, 2, "scores")
+    correct_ext = kernels._check_view(correct_ext, 2, "correct_ext")
+    th = np.ascontiguousarray(thresholds, dtype=np.float64)
+    serve = np.ascontiguousarray(serve, dtype=np.float64)
+    n, r = scores.shape
+    c = th.shape[0]
+    d_s = kernels._to_device(torch, scores)
+    bits, flag = kernels.pack_correct(correct_ext, torch)
+    hist = torch.empty((c, r + 1), dtype=torch.int64, device="cuda")
+    ok = torch.empty(c, dtype=torch.int64, device="cuda")
+    acc = torch.empty(c, dtype=torch.float64, device="cuda")
+    sav = torch.empty(c, dtype=torch.float64, device="cuda")
+    st = nat.stream_handle(torch)
+    nat.check(lib.ee_eval_thresholds(nat.workspace(), nat.ptr(d_s), nat.ptr(bits), n, r,
+                                     serve.ctypes.data, float(vanilla), th.ctypes.data, c,
+                                     nat.MODE_HIST, hist.data_ptr(), ok.data_ptr(),
+                                     acc.data_ptr(), sav.data_ptr(), st))
+    hist, ok = reduce_counts(hist, ok, group)
+    nat.check(lib.ee_finalize_hist(nat.workspace(), hist.data_ptr(), ok.data_ptr(), c, r, n_total,
+                                   serve.ctypes.data, float(vanilla), acc.data_ptr(),
+                                   sav.data_ptr(), st))
+    if int(flag.item()):
+        raise ValueError("correct_ext must contain only 0.0 and 1.0")
+    return acc.cpu().numpy(), sav.cpu().numpy()

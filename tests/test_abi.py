@@ -1,0 +1,104 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports every
+entry point include/eeb200.h declares (no compute calls here)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2312_05385_b200 import _native, kernels
+from paper_2312_05385_b200.errors import ParameterError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "eeb200.h")).read()
+    return sorted(set(re.findall(r"\b(ee_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_expected_entry_points():
+    syms = header_symbols()
+    for name in ("ee_exit_sites", "ee_eval_thresholds", "ee_eval_lattice", "ee_pack_correct",
+                 "ee_decision_scores", "ee_workspace_create", "ee_workspace_destroy"):
+        assert name in syms
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.load_library()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+        assert name in _native.SIGNATURES, f"{name} has no ctypes signature"
+    assert set(_native.SIGNATURES) == set(header_symbols())
+
+
+def test_version_string_without_gpu():
+    lib = _native.load_library()
+    assert b"sm_100a" in lib.ee_version()
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_shape_errors_are_raised_before_any_device_work():
+    import numpy as np
+
+    s = np.zeros((3, 2))
+    with pytest.raises(ParameterError):
+        kernels.exit_sites(s, np.zeros(3))
+    with pytest.raises(ParameterError):
+        kernels.eval_thresholds(s, np.ones((3, 2)), np.ones(3), 1.0, np.zeros((2, 2)))
+    with pytest.raises(ParameterError):
+        kernels.eval_thresholds(s, np.ones((3, 3)), np.ones(2), 1.0, np.zeros((2, 2)))
+    with pytest.raises(ParameterError):
+        kernels.eval_thresholds(s, np.ones((3, 3)), np.ones(3), 1.0, np.zeros((2, 3)))
+
+
+def test_buffer_errors_follow_cython_memoryview_types():
+    import numpy as np
+
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        kernels.exit_sites(np.zeros((3, 2), dtype=np.int64), np.zeros(2))
+    with pytest.raises(ValueError, match="C-contiguous"):
+        kernels.exit_sites(np.zeros((3, 4))[:, ::2], np.zeros(2))
+    with pytest.raises(ValueError, match="dimensions"):
+        kernels.exit_sites(np.zeros(3), np.zeros(2))
+    with pytest.raises(TypeError):
+        kernels.exit_sites([[0.1, 0.2]], np.zeros(2))
+    with pytest.raises(TypeError):
+        kernels.exit_sites(np.zeros((3, 2)), [0.1, 0.2])
+
+
+def test_backend_surface_mirrors_reference_seam():
+    assert kernels.BACKEND == "cuda"
+    assert kernels.available_backends() == ["cuda"]
+    assert kernels.get_backend("cuda") is kernels
+    with pytest.raises(ValueError):
+        kernels.get_backend("python")  # no CPU fallback exists
+
+    class Seam:
+        pass
+
+    seam = Seam()
+    kernels.install_into(seam)
+    assert seam.eval_thresholds is kernels.eval_thresholds
+    assert seam.exit_sites is kernels.exit_sites
+
+
+def test_no_gpu_means_loud_failure(monkeypatch):
+    import numpy as np
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(Exception, match="CUDA device"):
+        kernels.exit_sites(np.zeros((3, 2)), np.zeros(2))

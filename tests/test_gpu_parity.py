@@ -1,0 +1,260 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle and
+the reference's golden vectors. Bit-exact for indices, histograms, accuracy
+and — in exact mode — savings; histogram-mode savings within 1e-12 relative
+(correctly rounded vs the reference's sequential sum)."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, make_chain
+from helpers import axis_sweep, config4_curve, config4_profile, diagonal
+from oracle import oracle as O
+from paper_2312_05385_b200 import kernels
+from paper_2312_05385_b200.engine import WindowEvaluator
+from paper_2312_05385_b200.graph import find_feasible_sites
+from paper_2312_05385_b200.trace import WindowArrays, synthesize_workload, window_arrays
+from paper_2312_05385_b200.tuner import TunerParams, grid_oracle, tune
+
+pytestmark = pytest.mark.gpu
+
+SAV_RTOL = 1e-12  # histogram mode: correctly rounded total vs sequential fp64 sum
+
+
+def random_window(rng, n, r, c, nan_frac=0.0, ties=False):
+    scores = rng.random((n, r))
+    if ties:
+        scores = np.round(scores * 16) / 16
+    if nan_frac:
+        scores[rng.random((n, r)) < nan_frac] = np.nan
+    cext = np.hstack([rng.integers(0, 2, size=(n, r)).astype(np.float64),
+                      rng.integers(0, 2, size=(n, 1)).astype(np.float64)])
+    serve = np.sort(rng.uniform(1.0, 50.0, size=r + 1))
+    vanilla = float(serve[-1] + rng.uniform(0.0, 5.0))
+    th = rng.random((c, r))
+    if ties:
+        th = np.round(th * 16) / 16
+    return scores, cext, serve, vanilla, th
+
+
+def check_hist(scores, cext, serve, vanilla, th, mode="hist"):
+    acc, sav = kernels.eval_thresholds(scores, cext, serve, vanilla, th, mode=mode)
+    acc_o, sav_o = O.eval_thresholds(scores, cext, serve, vanilla, th)
+    assert np.array_equal(acc, acc_o)
+    np.testing.assert_allclose(sav, sav_o, rtol=SAV_RTOL, atol=1e-12)
+    return acc, sav
+
+
+def test_golden_random_windows_exact_bitwise(cuda, kernels_random):
+    for w in kernels_random:
+        acc, sav = kernels.eval_thresholds(w["scores"], w["cext"], w["serve"], float(w["vanilla"]),
+                                           w["th"])
+        assert np.array_equal(acc, w["acc"]) and np.array_equal(sav, w["sav"])
+        for row, want in zip(w["th"][:5], w["sites"]):
+            assert np.array_equal(kernels.exit_sites(w["scores"], row), want)
+
+
+def test_golden_random_windows_hist_mode(cuda, kernels_random):
+    for w in kernels_random:
+        acc, sav = kernels.eval_thresholds(w["scores"], w["cext"], w["serve"], float(w["vanilla"]),
+                                           w["th"], mode="hist")
+        assert np.array_equal(acc, w["acc"])
+        np.testing.assert_allclose(sav, w["sav"], rtol=0, atol=1e-12)
+
+
+def test_edge_semantics(cuda, golden):
+    e = golden["edge"]
+    s = np.array([[0.5, 0.1], [0.9, 0.9], [0.0, 0.9]])
+    assert kernels.exit_sites(s, np.array([0.4, 0.2])).tolist() == e["semantics_sites"]
+    s_nan = np.array([[np.nan, 0.1], [0.3, np.nan], [np.nan, np.nan], [0.2, 0.2]])
+    assert kernels.exit_sites(s_nan, np.array([0.5, 0.5])).tolist() == e["nan_sites"]
+    assert kernels.exit_sites(np.array([[0.5, 0.5]]), np.array([0.5, 0.6])).tolist() == e["tie_sites"]
+    a, sv = kernels.eval_thresholds(np.zeros((4, 0)), np.ones((4, 1)), np.array([12.0]), 12.0,
+                                    np.zeros((3, 0)))
+    assert [a.tolist(), sv.tolist()] == e["zero_ramps_compiled"]
+    a, sv = kernels.eval_thresholds(np.zeros((0, 2)), np.ones((0, 3)), np.ones(3), 1.0,
+                                    np.zeros((2, 2)))
+    assert np.isnan(a).all() and np.isnan(sv).all()
+    a, sv = kernels.eval_thresholds(np.zeros((2, 2)), np.ones((2, 3)), np.ones(3), 1.0,
+                                    np.zeros((0, 2)))
+    assert a.shape == (0,) and sv.shape == (0,)
+    assert kernels.exit_sites(np.zeros((3, 0)), np.zeros(0)).tolist() == [0, 0, 0]
+
+
+def test_nan_ties_and_signed_zero_both_modes(cuda):
+    rng = np.random.default_rng(11)
+    for mode in ("exact", "hist"):
+        scores, cext, serve, vanilla, th = random_window(rng, 3001, 5, 70, nan_frac=0.05, ties=True)
+        th[3, 2] = np.nan  # NaN threshold never exits
+        th[4, :] = -0.0
+        scores[:10, 0] = 0.0
+        th[5, 0] = np.inf
+        scores[10:20, 1] = -np.inf
+        check_hist(scores, cext, serve, vanilla, th, mode=mode)
+        for row in th[:8]:
+            assert np.array_equal(kernels.exit_sites(scores, row), O.exit_sites(scores, row))
+
+
+def test_not_binary_correct_ext_is_rejected(cuda):
+    scores = np.zeros((4, 2))
+    cext = np.ones((4, 3))
+    cext[1, 1] = 0.5
+    with pytest.raises(ValueError, match="0.0 and 1.0"):
+        kernels.eval_thresholds(scores, cext, np.ones(3), 1.0, np.zeros((1, 2)))
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 4, 5, 8, 12, 13, 16, 17, 24, 31])
+def test_hist_histograms_exact_across_ramp_counts(cuda, r):
+    rng = np.random.default_rng(100 + r)
+    n = 5000 + 37 * r  # not a multiple of the 256-sample tile
+    scores, cext, serve, vanilla, th = random_window(rng, n, r, 150, ties=(r % 2 == 0))
+    arrays = WindowArrays(scores, cext.astype(np.uint8))
+    prof = make_chain(r + 1)
+    ev = WindowEvaluator.from_arrays(arrays, find_feasible_sites(prof)[:r], prof, mode="hist")
+    hist, ok = ev.histograms(th)
+    hist_o, ok_o = O.eval_hist(scores, cext, th)
+    assert np.array_equal(hist, hist_o) and np.array_equal(ok, ok_o)
+    check_hist(scores, cext, serve, vanilla, th)
+
+
+def test_more_than_127_distinct_thresholds_per_ramp(cuda):
+    rng = np.random.default_rng(3)
+    scores, cext, serve, vanilla, th = random_window(rng, 8000, 6, 700)  # forces several chunks
+    check_hist(scores, cext, serve, vanilla, th)
+
+
+def test_exact_mode_bitwise_vs_oracle_large_grid(cuda):
+    rng = np.random.default_rng(4)
+    scores, cext, serve, vanilla, th = random_window(rng, 64, 3, 20000)
+    acc, sav = kernels.eval_thresholds(scores, cext, serve, vanilla, th, mode="exact")
+    acc_o, sav_o = O.eval_thresholds(scores, cext, serve, vanilla, th)
+    assert np.array_equal(acc, acc_o) and np.array_equal(sav, sav_o)
+
+
+def test_exact_mode_long_window_bitwise(cuda):
+    rng = np.random.default_rng(6)
+    scores, cext, serve, vanilla, th = random_window(rng, 20000, 12, 7)
+    acc, sav = kernels.eval_thresholds(scores, cext, serve, vanilla, th, mode="exact")
+    acc_o, sav_o = O.eval_thresholds(scores, cext, serve, vanilla, th)
+    assert np.array_equal(acc, acc_o) and np.array_equal(sav, sav_o)
+
+
+def test_device_decision_scores_bitwise(cuda, golden):
+    e = golden["edge"]
+    errs = np.random.default_rng(e["decision_scores_rand_input_seed"]).random((64, 7))
+    prof = make_chain(8)
+    arrays = WindowArrays(errs, np.ones((64, 8), dtype=np.uint8))
+    ev = WindowEvaluator.from_arrays(arrays, find_feasible_sites(prof)[:7], prof, k=3)
+    assert [x.hex() for x in ev.scores.ravel()] == e["decision_scores_rand_k3_hex"]
+
+
+def _tune_case(entry):
+    chain8 = make_chain(8)
+    s8 = find_feasible_sites(chain8)
+    w = synthesize_workload(chain8, 64, entry["continuity"], entry["curve"], seed=entry["seed"],
+                            miscalibration=entry["miscal"])
+    return chain8, [s8[1], s8[3], s8[5]], list(w.records)
+
+
+def test_tune_matches_reference_bitwise(cuda, golden):
+    for entry in golden["tunes"]:
+        prof, ramps, recs = _tune_case(entry)
+        res = tune(recs, ramps, TunerParams(), prof)
+        want = entry["tune"]
+        assert dict(res.thresholds) == want["thresholds"]
+        assert res.savings_ms.hex() == want["savings"]
+        assert res.accuracy == want["accuracy"]
+        assert (res.rounds, res.evals) == (want["rounds"], want["evals"])
+        assert [list(t) for t in res.step_trace] == want["trace"]
+        for k in (2, 3):
+            rk = tune(recs, ramps, TunerParams(acc_loss_budget=0.05), prof, k=k)
+            assert dict(rk.thresholds) == entry[f"tune_k{k}_b0.05"]["thresholds"]
+            assert rk.savings_ms.hex() == entry[f"tune_k{k}_b0.05"]["savings"]
+
+
+def test_grid_oracle_matches_reference_bitwise(cuda, golden):
+    for entry in golden["tunes"]:
+        prof, ramps, recs = _tune_case(entry)
+        for key, step in (("grid_0.1", 0.1), ("grid_0.01", 0.01)):
+            if key not in entry:
+                continue
+            res = grid_oracle(recs, ramps, 0.01, step, prof)
+            want = entry[key]
+            assert dict(res.thresholds) == want["thresholds"]
+            assert res.savings_ms.hex() == want["savings"]
+            assert res.accuracy == want["accuracy"] and res.n_points == want["n_points"]
+
+
+def test_tune_config1_window(cuda, golden):
+    chain13 = config4_profile()
+    s13 = find_feasible_sites(chain13)
+    w = synthesize_workload(chain13, 1000, 0.7, config4_curve(s13), seed=42, miscalibration=0.1)
+    ramps = [s13[0], s13[2], s13[4], s13[6], s13[8], s13[10]]
+    res = tune(list(w.records), ramps, TunerParams(), chain13)
+    want = golden["tune_1k"]
+    assert dict(res.thresholds) == want["thresholds"]
+    assert res.savings_ms.hex() == want["savings"]
+    assert (res.accuracy, res.rounds, res.evals) == (want["accuracy"], want["rounds"], want["evals"])
+
+
+def test_estimate_utilities_golden(cuda, golden):
+    from conftest import make_record
+    from paper_2312_05385_b200.engine import EEConfig
+    from paper_2312_05385_b200.ramps import estimate_utilities
+
+    chain4 = make_chain(4)
+    sites = {x.position: x for x in find_feasible_sites(chain4)}
+    recs = [
+        make_record(0, 0, {"n0": (0.3, 1), "n1": (0.1, 1), "n2": (0.9, 1)}, 1),
+        make_record(1, 1, {"n0": (0.5, 2), "n1": (0.5, 0), "n2": (0.9, 0)}, 0),
+        make_record(2, 2, {"n0": (0.9, 5), "n1": (0.7, 5), "n2": (0.9, 5)}, 4),
+        make_record(3, 3, {"n0": (0.2, 9), "n1": (0.0, 4), "n2": (0.9, 4)}, 4),
+    ]
+    cfg = EEConfig(((sites["n0"], 0.4), (sites["n1"], 0.6)))
+    assert estimate_utilities(recs, cfg, chain4).to_dict() == golden["edge"]["utilities"]
+
+
+def test_medium_sweep_window_against_reference(cuda):
+    gold = np.load(os.path.join(GOLDEN, "sweep_medium.npz"))
+    chain13 = config4_profile()
+    s13 = find_feasible_sites(chain13)
+    w = synthesize_workload(chain13, 5000, 0.9, config4_curve(s13), seed=0, miscalibration=0.05)
+    arrays = window_arrays(w.records, s13)
+    for mode in ("exact", "hist"):
+        ev = WindowEvaluator.from_arrays(arrays, s13, chain13, mode=mode)
+        assert np.array_equal(ev.serve, gold["serve"])
+        for fam, th in (("diag", diagonal()), ("axis", axis_sweep())):
+            acc, sav = ev.evaluate_many(th)
+            assert np.array_equal(acc, gold[f"{fam}_acc"])
+            if mode == "exact":
+                assert np.array_equal(sav, gold[f"{fam}_sav"])
+            else:
+                np.testing.assert_allclose(sav, gold[f"{fam}_sav"], rtol=SAV_RTOL, atol=0)
+
+
+def test_full_size_config4_histograms(cuda):
+    """1M x 12 at full size: exact histograms against the C oracle on a subset
+    of candidates, plus size-independent invariants on all of them."""
+    from paper_2312_05385_b200 import synth
+
+    prof = config4_profile()
+    sites = find_feasible_sites(prof)
+    arrays = synth.config4_window(1_000_000)
+    ev = WindowEvaluator.from_arrays(arrays, sites, prof, mode="hist")
+    th = diagonal()
+    hist, ok = ev.histograms(th)
+    n = arrays.n
+    assert (hist.sum(axis=1) == n).all()
+    # raising every threshold never delays an exit: exits at ramp 0 are monotone
+    assert (np.diff(hist[:, 0]) >= 0).all()
+    sel = [0, 17, 40, 63]
+    cext = arrays.correct_ext()
+    hist_o, ok_o = O.eval_hist(arrays.errs, cext, th[sel])
+    assert np.array_equal(hist[sel], hist_o) and np.array_equal(ok[sel], ok_o)
+    acc, sav = ev.evaluate_many(th[sel])
+    acc_o, sav_o = O.eval_thresholds(arrays.errs, cext, ev.serve, ev.vanilla_ms, th[sel])
+    assert np.array_equal(acc, acc_o)
+    np.testing.assert_allclose(sav, sav_o, rtol=1e-9)
