@@ -283,6 +283,23 @@ def run_ours(args):
     # parity spot check of what was timed (rank-count invariant integers)
     acc, sav = sweep.evaluate_many(th)
 
+    # the generic SWAR path on the same candidates (family specialisation off)
+    nat.set_special(False)
+    g_steps = max(10, args.steps // 5)
+    gs = [torch.cuda.Event(enable_timing=True) for _ in range(g_steps)]
+    ge = [torch.cuda.Event(enable_timing=True) for _ in range(g_steps)]
+    step()
+    for i in range(g_steps):
+        flush.zero_()
+        gs[i].record()
+        step()
+        ge[i].record()
+    torch.cuda.synchronize()
+    nat.set_special(True)
+    g_ms = sum(a.elapsed_time(b) for a, b in zip(gs, ge)) / g_steps
+    generic = {"ms_per_step": g_ms, "value": c / (g_ms / 1e3), "unit": UNIT,
+               "path": "generic SWAR scan (k_keys + k_count), family specialisation off"}
+
     # ------------- end to end: the reference-facing plugin call with host buffers
     e2e = e2e_run(args, arrays, prof, sites, th, rank, world)
 
@@ -310,6 +327,7 @@ def run_ours(args):
         "data": "synthetic (reference workload generator replayed, seed 0)",
         "config": config_block(args, r, c), "roofline": roofline,
         "gpu_launches": launches, "clocks": clocks.summary(), "e2e": e2e,
+        "generic_sweep": generic,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, arrays, prof, sites, th, acc, sav)

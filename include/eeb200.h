@@ -84,7 +84,8 @@ int ee_decision_scores(const double* d_errs, int64_t n, int32_t r, int32_t k, do
  *   d_scores  f64 [n, r]; d_bits u32 [n] (from ee_pack_correct, r+1 columns)
  *   h_serve   f64 [r+1] (engine._serve_table, engine.py:124-132), vanilla f64
  *   h_th      f64 [c, r] candidate threshold rows
- *   outputs (device, nullable except acc/sav):
+ *   outputs (device; acc/sav may both be NULL in HIST mode with d_hist/d_ok
+ *   given — counts only, e.g. before a cross-rank all-reduce):
  *     d_hist  i64 [c, r+1] exit-site histogram (HIST mode only; zero-filled in EXACT)
  *     d_ok    i64 [c]      correct releases
  *     d_acc   f64 [c]      ok / n
@@ -110,6 +111,12 @@ int ee_eval_lattice(ee_workspace* ws, const double* d_scores, const uint32_t* d_
 int ee_finalize_hist(ee_workspace* ws, const int64_t* d_hist, const int64_t* d_ok, int64_t c,
                      int32_t r, int64_t n, const double* h_serve, double vanilla, double* d_acc,
                      double* d_sav, void* stream);
+
+/* Family-specialised sweeps (default on): HIST-mode evaluations whose rows
+ * are diagonal (one threshold repeated on every ramp, <= 256 distinct values)
+ * run the single-pass difference-array kernel instead of the generic SWAR
+ * scan. Results are identical; 0 forces the generic path (tests, A/B). */
+int ee_workspace_set_special(ee_workspace* ws, int32_t on);
 
 /* Per-launch timing: while enabled, every kernel launched through `ws` is
  * bracketed by CUDA events on its stream. ee_profile_read synchronises, writes

@@ -58,6 +58,7 @@ SIGNATURES = {
         [_vp, _vp, _vp, _c_i64, _c_i32, _c_i64, _vp, ctypes.c_double, _vp, _vp, _vp],
     ),
     "ee_profile_enable": (ctypes.c_int, [_vp, _c_i32]),
+    "ee_workspace_set_special": (ctypes.c_int, [_vp, _c_i32]),
     "ee_profile_read": (ctypes.c_int, [_vp, ctypes.c_char_p, _c_i64]),
     "ee_eval_lattice": (
         ctypes.c_int,
@@ -132,6 +133,11 @@ def workspace() -> ctypes.c_void_p:
         ws = _Workspace()
         _tls.ws = ws
     return ws.handle
+
+
+def set_special(on: bool = True) -> None:
+    """Enable/disable family-specialised sweeps on this thread's workspace."""
+    check(load_library().ee_workspace_set_special(workspace(), int(on)))
 
 
 def profile_enable(on: bool = True) -> None:

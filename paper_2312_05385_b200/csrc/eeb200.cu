@@ -229,12 +229,12 @@ __global__ void k_eval_exact(const double* __restrict__ s, const uint32_t* __res
 // t in u_j, so the exit test becomes a 7-bit integer compare.
 // Thread per (sample, padded ramp); scores are read fully coalesced.
 // ---------------------------------------------------------------------------
-constexpr int KEY_SLOTS = 128;  // per-ramp table size (NaN padded)
+constexpr int KEY_STRIDE = 129;  // padded so lanes on different ramps hit different banks
 
-__global__ void k_keys(const double* __restrict__ s, int64_t n, int r, int rp,
+__global__ void k_keys(const double* __restrict__ s, int64_t n, int r, int rp, int top,
                        const double* __restrict__ utab, uint8_t* __restrict__ keys) {
-  extern __shared__ double su[];  // [r][KEY_SLOTS]
-  for (int idx = threadIdx.x; idx < r * KEY_SLOTS; idx += blockDim.x) su[idx] = utab[idx];
+  extern __shared__ double su[];  // [r][KEY_STRIDE]
+  for (int idx = threadIdx.x; idx < r * KEY_STRIDE; idx += blockDim.x) su[idx] = utab[idx];
   __syncthreads();
   const int64_t total = n * rp;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -244,10 +244,9 @@ __global__ void k_keys(const double* __restrict__ s, int64_t n, int r, int rp,
     uint32_t b = 0;
     if (j < r) {
       const double v = __ldg(s + i * r + j);
-      const double* u = su + j * KEY_SLOTS;
-      // branchless upper_bound over 128 NaN-padded slots
-#pragma unroll
-      for (int step = 64; step >= 1; step >>= 1)
+      const double* u = su + j * KEY_STRIDE;
+      // branchless upper_bound over NaN-padded slots; top = pow2 with 2*top-1 >= max m_j
+      for (int step = top; step >= 1; step >>= 1)
         if (u[b + step - 1] <= v) b += step;
       if (v != v) b = 127;
     }
@@ -275,17 +274,16 @@ template <int RW, int WPT>
 __global__ void __launch_bounds__(COUNT_THREADS, 2)
     k_count(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ bits, int64_t n,
             int r, const uint32_t* __restrict__ pwords, unsigned long long* __restrict__ hist,
-            unsigned long long* __restrict__ okc, unsigned int* __restrict__ tile_ctr,
-            int64_t ncand) {
+            unsigned long long* __restrict__ okc, int64_t ncand) {
   constexpr int RMAX = 4 * RW;
   constexpr int NSLOT = RMAX + 2;  // RMAX ramps, "no exit", ok
   constexpr int WG = CB_WORDS / WPT;
   constexpr int SG = COUNT_THREADS / WG;
   constexpr int SPT = TS / SG;  // samples per thread per tile
+  static_assert(TS == COUNT_THREADS, "one prefetched bits word per thread");
   __shared__ uint32_t skeys[TS * RW];
   __shared__ uint32_t sbits[TS];
   __shared__ uint32_t shist[CB * NSLOT];
-  __shared__ int64_t stile;
 
   const int cb = blockIdx.y;
   const int wg = threadIdx.x % WG;
@@ -339,19 +337,30 @@ __global__ void __launch_bounds__(COUNT_THREADS, 2)
   };
 
   const int64_t ntiles = ceil_div(n, TS);
-  while (true) {
-    __syncthreads();
-    if (threadIdx.x == 0) stile = (int64_t)atomicAdd(tile_ctr + cb, 1u);
-    __syncthreads();
-    const int64_t tile = stile;
-    if (tile >= ntiles) break;
-    const int64_t base = tile * TS;
+  // static round-robin tiles; the next tile is prefetched into registers while
+  // the current one is counted out of shared memory
+  uint32_t rk[RW], rb = 0;
+  auto fetch = [&](int64_t t) {
+    const int64_t base = t * TS;
     const int tn = (int)imin64((int64_t)TS, n - base);
-    // stage keys (tn*RW words, contiguous) and correctness bits
     const uint32_t* gk = keys + base * RW;
-    for (int idx = threadIdx.x; idx < tn * RW; idx += COUNT_THREADS) skeys[idx] = gk[idx];
-    for (int idx = threadIdx.x; idx < tn; idx += COUNT_THREADS) sbits[idx] = bits[base + idx];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      const int idx = q * COUNT_THREADS + threadIdx.x;
+      rk[q] = idx < tn * RW ? __ldg(gk + idx) : 0u;
+    }
+    rb = (int)threadIdx.x < tn ? __ldg(bits + base + threadIdx.x) : 0u;
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) fetch(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int tn = (int)imin64((int64_t)TS, n - tile * TS);
     __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RW; ++q) skeys[q * COUNT_THREADS + threadIdx.x] = rk[q];
+    sbits[threadIdx.x] = rb;
+    __syncthreads();
+    if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
 
     if (pending + SPT > 255) {
       flush();
@@ -447,9 +456,15 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
   const double dn = (double)n;
   const unsigned long long ok = okc[c];
   if (ok_out) ok_out[c] = (int64_t)ok;
-  acc[c] = __ddiv_rn((double)ok, dn);
-  sav[c] = __dsub_rn(vanilla, __ddiv_rn(s, dn));
+  if (acc) {
+    acc[c] = __ddiv_rn((double)ok, dn);
+    sav[c] = __dsub_rn(vanilla, __ddiv_rn(s, dn));
+  }
 }
+
+}  // namespace
+#include "sweep_diag.cuh"
+namespace {
 
 __global__ void k_fill_nan(double* a, double* b, int64_t C) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -474,6 +489,7 @@ struct ee_workspace {
   // optional per-launch timing (ee_profile_enable): events bracket every kernel
   // this workspace launches, on the launching stream
   bool profiling = false;
+  bool allow_special = true;  // family-specialised sweeps (diagonal); off = generic SWAR path
   struct Mark {
     const char* name;
     cudaEvent_t a, b;
@@ -577,7 +593,7 @@ int launch_count(const uint32_t* keys, const uint32_t* bits, int64_t n, int r,
   int64_t gx = std::max<int64_t>(1, (int64_t)sm_count() * 2 / ncb);
   gx = imin64(gx, ntiles);
   dim3 grid((unsigned)gx, (unsigned)ncb);
-  k_count<RW, WPT><<<grid, COUNT_THREADS, 0, st>>>(keys, bits, n, r, pw, hist, okc, ctr, ncand);
+  k_count<RW, WPT><<<grid, COUNT_THREADS, 0, st>>>(keys, bits, n, r, pw, hist, okc, ncand);
   EE_LAUNCH_CHECK();
   return EE_OK;
 }
@@ -735,10 +751,207 @@ static int eval_exact(ee_workspace* ws, const double* d_scores, const uint32_t* 
   return EE_OK;
 }
 
+// Diagonal family: every row repeats one threshold (NaN rows allowed).
+static bool diagonal_rows(const double* th, int64_t C, int r, std::vector<double>& distinct) {
+  if (r < 1) return false;
+  distinct.clear();
+  for (int64_t c = 0; c < C; ++c) {
+    const double first = th[c * r];
+    for (int j = 1; j < r; ++j) {
+      const double v = th[c * r + j];
+      if (!(v == first || (v != v && first != first))) return false;
+    }
+    if (first == first) distinct.push_back(canon(first));
+  }
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  return (int)distinct.size() <= diag::MAX_M;
+}
+
+// Host side of the bucket grid (diag::grid_bin is shared host/device code):
+// lo[k] = #{u_j : bin(u_j) < k}, th[k] = u[lo[k]] (NaN past the end), and
+// whether every bin holds at most one threshold.
+static diag::Grid make_grid(const std::vector<double>& u, int nbins, std::vector<uint16_t>& lo,
+                            std::vector<double>& th, bool* single) {
+  diag::Grid g{0.0, 0.0, nbins - 1, nbins};
+  double f0 = 0.0, f1 = 0.0;
+  bool any = false;
+  for (double x : u)
+    if (std::isfinite(x)) {
+      if (!any) f0 = x;
+      f1 = x;
+      any = true;
+    }
+  if (any && f1 > f0) {
+    // finite range maps to bins [1, nbins-2]: -inf / +inf thresholds get bins of their own
+    const double w = (f1 - f0) / (double)(nbins - 3);
+    g.base = f0 - w;
+    g.inv_w = 1.0 / w;
+  } else {
+    g.base = any ? f0 : 0.0;
+    g.inv_w = 0.0;
+  }
+  const int m = (int)u.size();
+  std::vector<int> cnt(nbins + 1, 0);
+  for (double x : u) cnt[diag::grid_bin(g, x) + 1] += 1;
+  lo.assign(nbins, 0);
+  th.assign(nbins, std::numeric_limits<double>::quiet_NaN());
+  int acc = 0;
+  *single = true;
+  for (int k = 0; k < nbins; ++k) {
+    acc += cnt[k];
+    lo[k] = (uint16_t)acc;
+    if (acc < m) th[k] = u[acc];
+    if (cnt[k + 1] > 1) *single = false;
+  }
+  return g;
+}
+
+}  // extern "C"
+struct DiagArgs {
+  const double* s;
+  const uint32_t* bits;
+  int64_t n;
+  int r;
+  const double* u;
+  const unsigned short* lo;
+  const double* th;
+  diag::Grid g;
+  int m, copies;
+  long long* gD;
+  unsigned* done;
+  const int* pos;
+  int64_t C;
+  const double* serve;
+  double vanilla;
+  int64_t* hist;
+  int64_t* ok;
+  double* acc;
+  double* sav;
+};
+
+template <int RMAX, int W, bool EVEN, bool SINGLE>
+static cudaError_t launch_diag4(dim3 grid, size_t smem, cudaStream_t st, const DiagArgs& a) {
+  auto k = diag::k_diag<RMAX, W, EVEN, SINGLE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // one full wave of persistent CTAs: resident CTAs per SM x SMs
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, diag::THREADS, smem);
+  if (e != cudaSuccess) return e;
+  grid.x = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)std::max(occ, 1) * sm_count(), ceil_div(a.n, diag::THREADS)));
+  k<<<grid, diag::THREADS, smem, st>>>(a.s, a.bits, a.n, a.r, a.u, a.lo, a.th, a.g, a.m, a.copies,
+                                        a.gD,
+                                        a.done, a.pos, a.C, a.serve, a.vanilla, a.hist, a.ok,
+                                        a.acc, a.sav);
+  return cudaGetLastError();
+}
+
+template <int RMAX, int W, bool EVEN>
+static cudaError_t launch_diag3(bool single, dim3 grid, size_t smem, cudaStream_t st,
+                                const DiagArgs& a) {
+  return single ? launch_diag4<RMAX, W, EVEN, true>(grid, smem, st, a)
+                : launch_diag4<RMAX, W, EVEN, false>(grid, smem, st, a);
+}
+
+template <int RMAX>
+static cudaError_t launch_diag(bool even, bool single, int W, dim3 grid, size_t smem,
+                               cudaStream_t st, const DiagArgs& a) {
+  if (W == 65)
+    return even ? launch_diag3<RMAX, 65, true>(single, grid, smem, st, a)
+                : launch_diag3<RMAX, 65, false>(single, grid, smem, st, a);
+  return even ? launch_diag3<RMAX, 257, true>(single, grid, smem, st, a)
+              : launch_diag3<RMAX, 257, false>(single, grid, smem, st, a);
+}
+extern "C" {
+
+static int eval_diag(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                     int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
+                     const std::vector<double>& u, int64_t* d_hist, int64_t* d_ok, double* d_acc,
+                     double* d_sav, cudaStream_t st) {
+  const int m = (int)u.size();
+  std::vector<uint16_t> lo;
+  std::vector<double> thb;
+  bool single = false;
+  const diag::Grid g = make_grid(u, diag::NBINS, lo, thb, &single);
+  const int W = m + 1 <= 65 ? 65 : 257;
+  const int rows = 2 * (r + 1);
+  const int dstride = rows * W;
+  const size_t gd_b = align_up((size_t)(dstride + 1) * 8 + 8, 256);  // D, corrR, done counter
+  const size_t serve_b = align_up((size_t)(r + 1) * 8, 256);
+  const size_t u_b = align_up((size_t)(m + 1) * 8, 256);
+  const size_t lo_b = align_up((size_t)diag::NBINS * 2, 256);
+  const size_t pos_b = align_up((size_t)C * 4, 256);
+  const size_t th_b = align_up((size_t)diag::NBINS * 8, 256);
+  const size_t host_need = serve_b + u_b + lo_b + pos_b + th_b;
+  int rc = ws_reserve(ws, gd_b + host_need, host_need);
+  if (rc) return rc;
+  auto* d0 = static_cast<unsigned char*>(ws->d_buf);
+  auto* gD = reinterpret_cast<long long*>(d0);
+  auto* done = reinterpret_cast<unsigned*>(d0 + (size_t)(dstride + 1) * 8);
+  unsigned char* dtab = d0 + gd_b;
+  auto* hs = static_cast<unsigned char*>(ws->h_stage);
+  std::memcpy(hs, h_serve, (size_t)(r + 1) * 8);
+  double* hu = reinterpret_cast<double*>(hs + serve_b);
+  for (int k = 0; k < m; ++k) hu[k] = u[k];
+  hu[m] = std::numeric_limits<double>::quiet_NaN();
+  std::memcpy(hs + serve_b + u_b, lo.data(), lo.size() * 2);
+  int* hpos = reinterpret_cast<int*>(hs + serve_b + u_b + lo_b);
+  for (int64_t c = 0; c < C; ++c) {
+    const double v = h_th[c * r];
+    hpos[c] = v == v ? (int)(std::lower_bound(u.begin(), u.end(), canon(v)) - u.begin()) : -1;
+  }
+  std::memcpy(hs + serve_b + u_b + lo_b + pos_b, thb.data(), thb.size() * 8);
+  EE_CUDA(cudaMemcpyAsync(dtab, hs, host_need, cudaMemcpyHostToDevice, st));
+  EE_CUDA(cudaEventRecord(ws->staged, st));
+  EE_CUDA(cudaMemsetAsync(d0, 0, (size_t)(dstride + 1) * 8 + 8, st));
+
+  DiagArgs a{d_scores, d_bits, n, r,
+             reinterpret_cast<const double*>(dtab + serve_b),
+             reinterpret_cast<const unsigned short*>(dtab + serve_b + u_b),
+             reinterpret_cast<const double*>(dtab + serve_b + u_b + lo_b + pos_b), g, m, 1, gD,
+             done,
+             reinterpret_cast<const int*>(dtab + serve_b + u_b + lo_b), C,
+             reinterpret_cast<const double*>(dtab), vanilla, d_hist, d_ok, d_acc, d_sav};
+  const size_t copy_b = (size_t)dstride * 4;
+  a.copies = (int)std::max<size_t>(1, std::min<size_t>(4, (28 * 1024) / copy_b));
+  const size_t fin_b = (size_t)rows * std::max(m, 1) * 8;  // last-CTA prefix buffer
+  const size_t dbytes = std::max(a.copies * copy_b, fin_b);
+  const size_t smem = (size_t)diag::NBINS * 8 + (size_t)(m + 1) * 8 +
+                      (size_t)((diag::NBINS + 7) & ~7) * 2 + dbytes;
+  if (smem > 200 * 1024) return fail(EE_ERR_ARG, "diagonal tables do not fit in shared memory");
+  const int64_t want = (int64_t)sm_count() * 4;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(n, diag::THREADS))));
+  const bool even = (r % 2 == 0) && ((reinterpret_cast<uintptr_t>(d_scores) & 15) == 0);
+  cudaError_t e;
+  {
+    ProfScope ps(ws, st, "k_diag");
+    if (r <= 4)
+      e = launch_diag<4>(even, single, W, grid, smem, st, a);
+    else if (r <= 8)
+      e = launch_diag<8>(even, single, W, grid, smem, st, a);
+    else if (r <= 12)
+      e = launch_diag<12>(even, single, W, grid, smem, st, a);
+    else if (r <= 16)
+      e = launch_diag<16>(even, single, W, grid, smem, st, a);
+    else
+      e = launch_diag<32>(even, single, W, grid, smem, st, a);
+  }
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_diag: ") + cudaGetErrorString(e));
+  return EE_OK;
+}
+
 static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
                      int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
                      int64_t* d_hist, int64_t* d_ok, double* d_acc, double* d_sav,
                      cudaStream_t st) {
+  {
+    std::vector<double> u;
+    if (ws->allow_special && diagonal_rows(h_th, C, r, u))
+      return eval_diag(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, C, u, d_hist, d_ok,
+                       d_acc, d_sav, st);
+  }
   const int rw = std::max(1, (r + 3) / 4);
   const int rp = 4 * rw;
   const int rmax = rp;
@@ -755,7 +968,7 @@ static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d
   const size_t serve_b = align_up((size_t)(r + 1) * 8, 256);
   size_t tab_b = 0;
   for (auto& ch : chunks) {
-    tab_b += align_up((size_t)std::max(r, 1) * KEY_SLOTS * 8, 256);
+    tab_b += align_up((size_t)std::max(r, 1) * KEY_STRIDE * 8, 256);
     tab_b += align_up((size_t)ceil_div(ch.c1 - ch.c0, CB) * CB_WORDS * rmax * 4, 256);
   }
   const size_t zero_b = hist_b + ok_b + ctr_b;
@@ -775,13 +988,15 @@ static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d
   std::memcpy(hs, h_serve, (size_t)(r + 1) * 8);
   size_t off = serve_b;
   std::vector<size_t> utab_off, pw_off;
+  std::vector<int> tops;
   std::vector<double> col;
   for (auto& ch : chunks) {
     const int64_t cc = ch.c1 - ch.c0;
     const int64_t nb = ceil_div(cc, CB);
     double* utab = reinterpret_cast<double*>(hs + off);
     utab_off.push_back(off);
-    off += align_up((size_t)std::max(r, 1) * KEY_SLOTS * 8, 256);
+    off += align_up((size_t)std::max(r, 1) * KEY_STRIDE * 8, 256);
+    int mmax = 0;
     uint32_t* pw = reinterpret_cast<uint32_t*>(hs + off);
     pw_off.push_back(off);
     off += align_up((size_t)nb * CB_WORDS * rmax * 4, 256);
@@ -796,7 +1011,8 @@ static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d
       std::sort(col.begin(), col.end());
       col.erase(std::unique(col.begin(), col.end()), col.end());
       const double qnan = std::numeric_limits<double>::quiet_NaN();
-      for (int k = 0; k < KEY_SLOTS; ++k) utab[j * KEY_SLOTS + k] = k < (int)col.size() ? col[k] : qnan;
+      for (int k = 0; k < KEY_STRIDE; ++k) utab[j * KEY_STRIDE + k] = k < (int)col.size() ? col[k] : qnan;
+      mmax = std::max(mmax, (int)col.size());
       for (int64_t c = ch.c0; c < ch.c1; ++c) {
         const double v = h_th[c * r + j];
         uint8_t code = 0x7F;
@@ -810,6 +1026,9 @@ static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d
         bytes[q] = code;
       }
     }
+    int top = 1;
+    while (2 * top - 1 < mmax) top *= 2;
+    tops.push_back(top);
   }
   EE_CUDA(cudaMemcpyAsync(dtab, hs, host_need, cudaMemcpyHostToDevice, st));
   EE_CUDA(cudaEventRecord(ws->staged, st));
@@ -828,13 +1047,14 @@ static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d
       const int threads = 256;
       const int64_t total = n * rp;
       const int64_t blocks = imin64(ceil_div(total, threads), (int64_t)sm_count() * 8);
-      const size_t smem = (size_t)std::max(r, 1) * KEY_SLOTS * 8;
+      const size_t smem = (size_t)std::max(r, 1) * KEY_STRIDE * 8;
       if (smem > 48 * 1024)
         EE_CUDA(cudaFuncSetAttribute(k_keys, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
       {
         ProfScope ps(ws, st, "k_keys");
-        k_keys<<<(unsigned)blocks, threads, smem, st>>>(d_scores, n, r, rp, d_utab, keys);
+        k_keys<<<(unsigned)blocks, threads, smem, st>>>(d_scores, n, r, rp, tops[ci], d_utab,
+                                                        keys);
       }
       EE_LAUNCH_CHECK();
     }
@@ -861,7 +1081,10 @@ int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t*
   if (n < 0 || r < 0 || c < 0) return fail(EE_ERR_ARG, "negative shape");
   if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
   if (c == 0) return EE_OK;
-  if (!d_acc || !d_sav || !h_serve) return fail(EE_ERR_ARG, "null pointer");
+  if (!h_serve) return fail(EE_ERR_ARG, "null serve table");
+  if (!d_acc != !d_sav) return fail(EE_ERR_ARG, "acc and sav must both be given or both be null");
+  if (!d_acc && (mode != EE_MODE_HIST || !d_hist || !d_ok))
+    return fail(EE_ERR_ARG, "counts-only evaluation needs HIST mode and d_hist/d_ok");
   if (n > 0 && (!d_scores && r > 0)) return fail(EE_ERR_ARG, "null scores");
   if (n > 0 && !d_bits) return fail(EE_ERR_ARG, "null correctness bits");
   if (r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
@@ -910,6 +1133,13 @@ int ee_finalize_hist(ee_workspace* ws, const int64_t* d_hist, const int64_t* d_o
         static_cast<const double*>(ws->d_buf), vanilla, nullptr, nullptr, d_acc, d_sav);
   }
   EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_workspace_set_special(ee_workspace* ws, int32_t on) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  ws->allow_special = on != 0;
   return EE_OK;
 }
 

@@ -63,13 +63,22 @@ class ShardedSweep:
 
     def counts(self, thresholds: np.ndarray):
         """Global (hist [C, R+1], ok [C]) as int64 device tensors."""
-        torch = self.local._torch
         th = np.ascontiguousarray(thresholds, dtype=np.float64)
-        _, _, ok, hist = self.local._eval_device(th, want_hist=True, mode_code=nat.MODE_HIST)
+        _, _, ok, hist = self.local._eval_device(th, want_hist=True, mode_code=nat.MODE_HIST,
+                                                 counts_only=True)
         return reduce_counts(hist, ok, self.group)
+
+    def _single(self) -> bool:
+        import torch.distributed as dist
+
+        return not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(self.group) == 1
 
     def evaluate_many(self, thresholds: np.ndarray, *, to_host: bool = True):
         torch = self.local._torch
+        if self._single():  # nothing to exchange: one fused evaluation
+            th = np.ascontiguousarray(thresholds, dtype=np.float64)
+            acc, sav, _, _ = self.local._eval_device(th, mode_code=nat.MODE_HIST)
+            return (acc.cpu().numpy(), sav.cpu().numpy()) if to_host else (acc, sav)
         hist, ok = self.counts(thresholds)
         c = hist.shape[0]
         acc = torch.empty(c, dtype=torch.float64, device="cuda")
@@ -108,8 +117,7 @@ def eval_thresholds_host_sharded(scores, correct_ext, serve, vanilla, thresholds
     st = nat.stream_handle(torch)
     nat.check(lib.ee_eval_thresholds(nat.workspace(), nat.ptr(d_s), nat.ptr(bits), n, r,
                                      serve.ctypes.data, float(vanilla), th.ctypes.data, c,
-                                     nat.MODE_HIST, hist.data_ptr(), ok.data_ptr(),
-                                     acc.data_ptr(), sav.data_ptr(), st))
+                                     nat.MODE_HIST, hist.data_ptr(), ok.data_ptr(), None, None, st))
     hist, ok = reduce_counts(hist, ok, group)
     nat.check(lib.ee_finalize_hist(nat.workspace(), hist.data_ptr(), ok.data_ptr(), c, r, n_total,
                                    serve.ctypes.data, float(vanilla), acc.data_ptr(),

@@ -218,19 +218,20 @@ class WindowEvaluator:
     def correct_ext(self) -> np.ndarray:
         return self._arrays.correct_ext()
 
-    def _eval_device(self, th: np.ndarray, want_hist: bool = False, mode_code: int | None = None):
+    def _eval_device(self, th: np.ndarray, want_hist: bool = False, mode_code: int | None = None,
+                     counts_only: bool = False):
         torch = self._torch
         lib = nat.load_library()
         c = th.shape[0]
-        acc = torch.empty(c, dtype=torch.float64, device="cuda")
-        sav = torch.empty(c, dtype=torch.float64, device="cuda")
+        acc = None if counts_only else torch.empty(c, dtype=torch.float64, device="cuda")
+        sav = None if counts_only else torch.empty(c, dtype=torch.float64, device="cuda")
         ok = torch.empty(c, dtype=torch.int64, device="cuda")
         hist = torch.empty((c, self.r + 1), dtype=torch.int64, device="cuda") if want_hist else None
         nat.check(lib.ee_eval_thresholds(
             nat.workspace(), nat.ptr(self.d_scores), self.d_bits.data_ptr(), self.n, self.r,
             self.serve.ctypes.data, float(self.vanilla_ms), th.ctypes.data if th.size else None,
             c, self._mode_code if mode_code is None else mode_code, nat.ptr(hist), ok.data_ptr(),
-            acc.data_ptr(), sav.data_ptr(), nat.stream_handle(torch)))
+            nat.ptr(acc), nat.ptr(sav), nat.stream_handle(torch)))
         return acc, sav, ok, hist
 
     def evaluate_many(self, thresholds: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
