@@ -104,6 +104,22 @@ int ee_eval_lattice(ee_workspace* ws, const double* d_scores, const uint32_t* d_
                     int32_t r, const double* h_serve, double vanilla, const double* h_vals,
                     int32_t n_vals, double* d_acc, double* d_sav, void* stream);
 
+/* Device-resident Algorithm 1: the whole threshold hill climb of
+ * tuner.tune (pkg/src/eesim/tuner.py:97-171) in one single-CTA launch over a
+ * device window (d_scores f64 [n, r], d_bits u32 [n]). Every round's tentative
+ * increments are scored in EXACT mode and selected with the reference's key
+ * (same IEEE operations), so thresholds, savings, accuracy, rounds, evals and
+ * the step trace are bit-identical to the compiled reference.
+ * Synchronous. Outputs: h_out f64 [r + 2] = thresholds, savings, accuracy;
+ * h_info i32 [4] = rounds, evals, trace rows, status (0 ok, 1 accuracy
+ * postcondition violated, 2 exceeded max_rounds); h_trace f64 [trace_cap, r]
+ * (step vectors, first row = initial steps). n <= EE_TUNE_N_MAX. */
+#define EE_TUNE_N_MAX 65536
+int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n, int32_t r,
+            const double* h_serve, double vanilla, double acc_loss_budget, double init_step,
+            double min_step, int32_t max_rounds, double* h_out, int32_t* h_info, double* h_trace,
+            int32_t trace_cap, void* stream);
+
 /* Finalises externally reduced histograms (e.g. after an all-reduce across
  * ranks of per-shard d_hist/d_ok from ee_eval_thresholds in HIST mode):
  * d_hist i64 [c, r+1], d_ok i64 [c], n = total samples -> d_acc, d_sav with

@@ -27,6 +27,7 @@ MODE_EXACT = 1
 MODE_HIST = 2
 MODES = {"auto": MODE_AUTO, "exact": MODE_EXACT, "hist": MODE_HIST}
 EXACT_N_MAX = 4096
+TUNE_N_MAX = 65536
 MAX_RAMPS = 31
 
 _c_i64 = ctypes.c_int64
@@ -60,6 +61,11 @@ SIGNATURES = {
     "ee_profile_enable": (ctypes.c_int, [_vp, _c_i32]),
     "ee_workspace_set_special": (ctypes.c_int, [_vp, _c_i32]),
     "ee_profile_read": (ctypes.c_int, [_vp, ctypes.c_char_p, _c_i64]),
+    "ee_tune": (
+        ctypes.c_int,
+        [_vp, _vp, _vp, _c_i64, _c_i32, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+         ctypes.c_double, _c_i32, _vp, _vp, _vp, _c_i32, _vp],
+    ),
     "ee_eval_lattice": (
         ctypes.c_int,
         [_vp, _vp, _vp, _c_i64, _c_i32, _vp, ctypes.c_double, _vp, _c_i32, _vp, _vp, _vp],

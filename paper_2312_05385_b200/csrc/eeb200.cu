@@ -464,6 +464,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 
 }  // namespace
 #include "sweep_diag.cuh"
+#include "tune_device.cuh"
 namespace {
 
 __global__ void k_fill_nan(double* a, double* b, int64_t C) {
@@ -1184,6 +1185,59 @@ int ee_profile_read(ee_workspace* ws, char* buf, int64_t cap) {
   js += "}";
   if ((int64_t)js.size() + 1 > cap) return fail(EE_ERR_ARG, "profile buffer too small");
   std::memcpy(buf, js.c_str(), js.size() + 1);
+  return EE_OK;
+}
+
+int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n, int32_t r,
+            const double* h_serve, double vanilla, double acc_loss_budget, double init_step,
+            double min_step, int32_t max_rounds, double* h_out, int32_t* h_info, double* h_trace,
+            int32_t trace_cap, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (n < 1 || r < 1) return fail(EE_ERR_ARG, "tune needs a nonempty window and ramps");
+  if (r > tunedev::MAXR) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (n > EE_TUNE_N_MAX) return fail(EE_ERR_ARG, "window larger than EE_TUNE_N_MAX");
+  if (!d_scores || !d_bits || !h_serve || !h_out || !h_info) return fail(EE_ERR_ARG, "null pointer");
+  if (trace_cap < 0 || (trace_cap > 0 && !h_trace)) return fail(EE_ERR_ARG, "bad trace buffer");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  const size_t serve_b = align_up((size_t)(r + 1) * 8, 256);
+  const size_t out_b = align_up((size_t)(r + 2) * 8 + 4 * 4, 256);
+  const size_t trace_b = align_up((size_t)std::max(trace_cap, 1) * r * 8, 256);
+  const size_t sites_b = align_up((size_t)(r + 1) * ((n + 7) & ~7), 256);
+  int rc = ws_reserve(ws, serve_b + out_b + trace_b + sites_b, serve_b);
+  if (rc) return rc;
+  auto* d0 = static_cast<unsigned char*>(ws->d_buf);
+  std::memcpy(ws->h_stage, h_serve, (size_t)(r + 1) * 8);
+  EE_CUDA(cudaMemcpyAsync(d0, ws->h_stage, serve_b, cudaMemcpyHostToDevice, st));
+  EE_CUDA(cudaEventRecord(ws->staged, st));
+  double* d_out = reinterpret_cast<double*>(d0 + serve_b);
+  int* d_info = reinterpret_cast<int*>(d0 + serve_b + (size_t)(r + 2) * 8);
+  double* d_trace = reinterpret_cast<double*>(d0 + serve_b + out_b);
+  unsigned char* d_sites = d0 + serve_b + out_b + trace_b;
+  tunedev::Params p{acc_loss_budget, init_step, min_step, max_rounds, trace_cap};
+  const size_t n8 = (size_t)((n + 7) & ~7);
+  const size_t rows_b = n8 * 4 + (size_t)(r + 1) * n8;
+  const size_t win_b = (size_t)n * r * 8;
+  const int rows_in = rows_b <= 120 * 1024;
+  const int in_smem = rows_in && rows_b + win_b <= 200 * 1024;
+  const size_t smem = rows_in ? rows_b + (in_smem ? win_b : 0) : 0;
+  if (smem)
+    EE_CUDA(cudaFuncSetAttribute(tunedev::k_tune, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  {
+    ProfScope ps(ws, st, "k_tune");
+    tunedev::k_tune<<<1, tunedev::THREADS, smem, st>>>(d_scores, d_bits, (int)n, r,
+                                                        reinterpret_cast<const double*>(d0),
+                                                        vanilla, p, d_sites, d_out, d_info,
+                                                        d_trace, in_smem, rows_in);
+  }
+  EE_LAUNCH_CHECK();
+  EE_CUDA(cudaMemcpyAsync(h_out, d_out, (size_t)(r + 2) * 8, cudaMemcpyDeviceToHost, st));
+  EE_CUDA(cudaMemcpyAsync(h_info, d_info, 4 * 4, cudaMemcpyDeviceToHost, st));
+  EE_CUDA(cudaStreamSynchronize(st));
+  const int rows = std::min(h_info[2], trace_cap);
+  if (rows > 0)
+    EE_CUDA(cudaMemcpy(h_trace, d_trace, (size_t)rows * r * 8, cudaMemcpyDeviceToHost));
   return EE_OK;
 }
 

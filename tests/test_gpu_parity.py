@@ -160,10 +160,11 @@ def _tune_case(entry):
     return chain8, [s8[1], s8[3], s8[5]], list(w.records)
 
 
-def test_tune_matches_reference_bitwise(cuda, golden):
+@pytest.mark.parametrize("device_loop", [True, False])
+def test_tune_matches_reference_bitwise(cuda, golden, device_loop):
     for entry in golden["tunes"]:
         prof, ramps, recs = _tune_case(entry)
-        res = tune(recs, ramps, TunerParams(), prof)
+        res = tune(recs, ramps, TunerParams(), prof, device_loop=device_loop)
         want = entry["tune"]
         assert dict(res.thresholds) == want["thresholds"]
         assert res.savings_ms.hex() == want["savings"]
@@ -171,7 +172,8 @@ def test_tune_matches_reference_bitwise(cuda, golden):
         assert (res.rounds, res.evals) == (want["rounds"], want["evals"])
         assert [list(t) for t in res.step_trace] == want["trace"]
         for k in (2, 3):
-            rk = tune(recs, ramps, TunerParams(acc_loss_budget=0.05), prof, k=k)
+            rk = tune(recs, ramps, TunerParams(acc_loss_budget=0.05), prof, k=k,
+                      device_loop=device_loop)
             assert dict(rk.thresholds) == entry[f"tune_k{k}_b0.05"]["thresholds"]
             assert rk.savings_ms.hex() == entry[f"tune_k{k}_b0.05"]["savings"]
 
@@ -189,12 +191,13 @@ def test_grid_oracle_matches_reference_bitwise(cuda, golden):
             assert res.accuracy == want["accuracy"] and res.n_points == want["n_points"]
 
 
-def test_tune_config1_window(cuda, golden):
+@pytest.mark.parametrize("device_loop", [True, False])
+def test_tune_config1_window(cuda, golden, device_loop):
     chain13 = config4_profile()
     s13 = find_feasible_sites(chain13)
     w = synthesize_workload(chain13, 1000, 0.7, config4_curve(s13), seed=42, miscalibration=0.1)
     ramps = [s13[0], s13[2], s13[4], s13[6], s13[8], s13[10]]
-    res = tune(list(w.records), ramps, TunerParams(), chain13)
+    res = tune(list(w.records), ramps, TunerParams(), chain13, device_loop=device_loop)
     want = golden["tune_1k"]
     assert dict(res.thresholds) == want["thresholds"]
     assert res.savings_ms.hex() == want["savings"]
