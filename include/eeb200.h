@@ -120,6 +120,42 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
             double min_step, int32_t max_rounds, double* h_out, int32_t* h_info, double* h_trace,
             int32_t trace_cap, void* stream);
 
+/* ---- Ramp heads / exit controller / compaction ----
+ * One ramp over a batch of b rows, fused in one launch: global-average pool of
+ * the ramp input (d_feat: NCHW [b, c, hw] when nhwc == 0, NHWC [b, hw, c]
+ * when nhwc == 1; hw == 1 for pre-pooled inputs such as a token-0 hidden
+ * state; fp32 or bf16 when feat_bf16), ramp FC (d_w [k, c] fp32/bf16, d_bias
+ * [k] fp32 nullable, k <= 256), softmax confidence (conf 0: err = 1 - max p;
+ * conf 1: err = H(p)/ln k), argmax label, and the reference exit rule
+ * (double)err < threshold (strict, engine.py:207) for rows whose d_alive byte
+ * is 1 (d_alive NULL = all alive). Outputs per row: d_err f32, d_label i32,
+ * d_exit u8, optional d_logits f32 [b, k]. Then, in the same launch, the
+ * surviving (alive, non-exiting) rows are compacted in ascending row order
+ * into d_keep with their count in *d_nkeep, and each exiting row's (label,
+ * err, site) is scattered to its request slot d_slot[row] (NULL = row index)
+ * in d_slot_label / d_slot_err / d_slot_site (all NULL = no scatter). */
+int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, int64_t b,
+                       int32_t c, int32_t hw, int32_t nhwc, const void* d_w, int32_t w_bf16,
+                       const float* d_bias, int32_t k, int32_t conf, double threshold,
+                       const uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
+                       int32_t* d_label, uint8_t* d_exit, float* d_logits, int32_t* d_keep,
+                       int32_t* d_nkeep, int32_t* d_slot_label, float* d_slot_err,
+                       int32_t* d_slot_site, void* stream);
+
+/* Same epilogue from precomputed fp32 logits [b, k] (large heads whose FC runs
+ * as a tensor-core GEMM). */
+int ee_exit_from_logits(ee_workspace* ws, const float* d_logits, int64_t b, int32_t k,
+                        int32_t conf, double threshold, const uint8_t* d_alive,
+                        const int32_t* d_slot, int32_t site, float* d_err, int32_t* d_label,
+                        uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
+                        float* d_slot_err, int32_t* d_slot_site, void* stream);
+
+/* Gathers rows d_keep[0 .. *d_nkeep) of d_src (row_bytes each, multiple of
+ * 16) into the dense d_dst (capacity max_rows rows): downstream blocks then
+ * run only on the non-exited samples (compaction mode). */
+int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
+                    const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream);
+
 /* Finalises externally reduced histograms (e.g. after an all-reduce across
  * ranks of per-shard d_hist/d_ok from ee_eval_thresholds in HIST mode):
  * d_hist i64 [c, r+1], d_ok i64 [c], n = total samples -> d_acc, d_sav with

@@ -465,6 +465,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 }  // namespace
 #include "sweep_diag.cuh"
 #include "tune_device.cuh"
+#include "exit_controller.cuh"
 namespace {
 
 __global__ void k_fill_nan(double* a, double* b, int64_t C) {
@@ -1238,6 +1239,105 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
   const int rows = std::min(h_info[2], trace_cap);
   if (rows > 0)
     EE_CUDA(cudaMemcpy(h_trace, d_trace, (size_t)rows * r * 8, cudaMemcpyDeviceToHost));
+  return EE_OK;
+}
+
+static int exit_out(ee_workspace* ws, cudaStream_t st, int64_t b, const int32_t* d_slot,
+                    int32_t site, float* d_err, int32_t* d_label, uint8_t* d_exit,
+                    float* d_logits, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
+                    float* d_slot_err, int32_t* d_slot_site, exitc::Out* o) {
+  if (!d_err || !d_label || !d_exit || !d_keep || !d_nkeep)
+    return fail(EE_ERR_ARG, "null output pointer");
+  if ((d_slot_label != nullptr) != (d_slot_err != nullptr) ||
+      (d_slot_label != nullptr) != (d_slot_site != nullptr))
+    return fail(EE_ERR_ARG, "slot scatter targets must be all given or all null");
+  int rc = ws_reserve(ws, 256, 0);
+  if (rc) return rc;
+  EE_CUDA(cudaMemsetAsync(ws->d_buf, 0, 4, st));
+  *o = exitc::Out{d_err, d_label, d_exit, d_logits, d_keep, d_nkeep, d_slot, d_slot_label,
+                  d_slot_err, d_slot_site, site, static_cast<unsigned*>(ws->d_buf)};
+  (void)b;
+  return EE_OK;
+}
+
+int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, int64_t b,
+                       int32_t c, int32_t hw, int32_t nhwc, const void* d_w, int32_t w_bf16,
+                       const float* d_bias, int32_t k, int32_t conf, double threshold,
+                       const uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
+                       int32_t* d_label, uint8_t* d_exit, float* d_logits, int32_t* d_keep,
+                       int32_t* d_nkeep, int32_t* d_slot_label, float* d_slot_err,
+                       int32_t* d_slot_site, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (b < 1 || c < 1 || hw < 1 || k < 1) return fail(EE_ERR_ARG, "bad shape");
+  if (k > exitc::MAXK_FUSED) return fail(EE_ERR_ARG, "K too large for the fused head (use the GEMM + ee_exit_from_logits)");
+  if (conf != 0 && conf != 1) return fail(EE_ERR_ARG, "conf must be 0 (max-prob) or 1 (entropy)");
+  if (!d_feat || !d_w) return fail(EE_ERR_ARG, "null input pointer");
+  if (b > 0x7fffffff) return fail(EE_ERR_ARG, "batch too large");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  exitc::Out o;
+  int rc = exit_out(ws, st, b, d_slot, site, d_err, d_label, d_exit, d_logits, d_keep, d_nkeep,
+                    d_slot_label, d_slot_err, d_slot_site, &o);
+  if (rc) return rc;
+  const size_t smem = (size_t)(c + k) * 4;
+  if (smem > 200 * 1024) return fail(EE_ERR_ARG, "too many channels for the fused head");
+  ProfScope ps(ws, st, "k_exit_fused");
+#define EE_EXITK(TF, TW)                                                                       \
+  do {                                                                                         \
+    auto kern = exitc::k_exit_fused<TF, TW>;                                                   \
+    if (smem > 48 * 1024)                                                                      \
+      EE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    kern<<<(unsigned)b, exitc::THREADS, smem, st>>>(static_cast<const TF*>(d_feat), b, c, hw,   \
+                                                     nhwc, static_cast<const TW*>(d_w), d_bias, k, \
+                                                     conf, threshold, d_alive, o);             \
+  } while (0)
+  if (feat_bf16 && w_bf16)
+    EE_EXITK(uint16_t, uint16_t);
+  else if (feat_bf16)
+    EE_EXITK(uint16_t, float);
+  else if (w_bf16)
+    EE_EXITK(float, uint16_t);
+  else
+    EE_EXITK(float, float);
+#undef EE_EXITK
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, int32_t k,
+                        int32_t conf, double threshold, const uint8_t* d_alive,
+                        const int32_t* d_slot, int32_t site, float* d_err, int32_t* d_label,
+                        uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
+                        float* d_slot_err, int32_t* d_slot_site, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (b < 1 || k < 1) return fail(EE_ERR_ARG, "bad shape");
+  if (conf != 0 && conf != 1) return fail(EE_ERR_ARG, "conf must be 0 (max-prob) or 1 (entropy)");
+  if (!d_logits_in) return fail(EE_ERR_ARG, "null logits");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  exitc::Out o;
+  int rc = exit_out(ws, st, b, d_slot, site, d_err, d_label, d_exit, nullptr, d_keep, d_nkeep,
+                    d_slot_label, d_slot_err, d_slot_site, &o);
+  if (rc) return rc;
+  ProfScope ps(ws, st, "k_exit_logits");
+  const int rows_per = exitc::THREADS / 32;
+  exitc::k_exit_logits<<<(unsigned)ceil_div(b, rows_per), exitc::THREADS, 0, st>>>(
+      d_logits_in, b, k, conf, threshold, d_alive, o);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
+                    const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream) {
+  if (row_bytes <= 0 || row_bytes % 16) return fail(EE_ERR_ARG, "row_bytes must be a positive multiple of 16");
+  if (!d_src || !d_keep || !d_nkeep || !d_dst) return fail(EE_ERR_ARG, "null pointer");
+  if (max_rows < 1) return EE_OK;
+  auto st = (cudaStream_t)stream;
+  const int64_t blocks = std::min<int64_t>(max_rows, (int64_t)sm_count() * 8);
+  exitc::k_compact_rows<<<(unsigned)blocks, 256, 0, st>>>(
+      static_cast<const uint8_t*>(d_src), row_bytes, d_keep, d_nkeep,
+      static_cast<uint8_t*>(d_dst));
+  EE_LAUNCH_CHECK();
   return EE_OK;
 }
 

@@ -1,0 +1,238 @@
+// exit_controller.cuh — fused ramp head + exit controller + batch compactor
+// (north star (2)). Included by eeb200.cu.
+//
+// For one ramp over a batch of B rows:
+//   pool   global average over HW of the ramp input (NCHW [B, C, HW] or
+//          NHWC [B, HW, C]; HW = 1 means already pooled, e.g. a BERT token-0
+//          hidden state)                                   fp32 accumulate
+//   logits W[K, C] @ pooled + bias                          fp32
+//   err    1 - max softmax  (conf = 0)                      fp32
+//          or H(p) / ln K   (conf = 1, the paper's entropy rule)
+//   label  argmax (first maximum, like torch.argmax)
+//   exit   (double)err < threshold  — the reference exit rule, strict
+//          (engine.py:207), applied only to rows still alive
+// then one CTA (the last to finish) compacts the batch: surviving rows are
+// listed in ascending row order (stable), and every exiting row's
+// (label, err, site) is scattered to its request slot.
+//
+// One CTA per row; the weights stay in L2 across CTAs. For large K (ImageNet
+// heads) the logits come from the tensor-core GEMM and ee_exit_from_logits
+// runs the same epilogue.
+#pragma once
+
+namespace exitc {
+
+constexpr int THREADS = 256;
+constexpr int MAXK_FUSED = 256;
+
+struct Out {
+  float* err;        // [B] per row (all rows)
+  int32_t* label;    // [B]
+  uint8_t* exits;    // [B] 1 = exits here
+  float* logits;     // [B, K] optional
+  int32_t* keep;     // [B] compacted surviving rows (ascending)
+  int32_t* n_keep;   // [1]
+  const int32_t* slot;  // [B] request slot of each row (nullable = identity)
+  int32_t* slot_label;  // [slots] scatter targets (nullable)
+  float* slot_err;
+  int32_t* slot_site;
+  int32_t site;
+  unsigned* done;    // grid completion counter (zeroed by the host)
+};
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) {
+  return __uint_as_float(((uint32_t)h) << 16);
+}
+
+template <typename T>
+__device__ __forceinline__ float ld_f32(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float ld_f32<float>(const float* p, int64_t i) {
+  return __ldg(p + i);
+}
+template <>
+__device__ __forceinline__ float ld_f32<uint16_t>(const uint16_t* p, int64_t i) {
+  return bf16_to_f32(__ldg(p + i));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// softmax confidence over logits l[0..K) in shared memory (one warp)
+__device__ __forceinline__ void confidence(const float* l, int K, int conf, float* err_out,
+                                           int* label_out) {
+  const int lane = threadIdx.x & 31;
+  float mx = -INFINITY;
+  int arg = 0x7fffffff;
+  for (int k = lane; k < K; k += 32) {
+    const float v = l[k];
+    if (v > mx || (v == mx && k < arg)) {
+      mx = v;
+      arg = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const int a2 = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (m2 > mx || (m2 == mx && a2 < arg)) {
+      mx = m2;
+      arg = a2;
+    }
+  }
+  float se = 0.f, sle = 0.f;
+  for (int k = lane; k < K; k += 32) {
+    const float d = l[k] - mx;
+    const float e = expf(d);
+    se += e;
+    sle += d * e;
+  }
+  se = warp_sum(se);
+  sle = warp_sum(sle);
+  float err;
+  if (conf == 0) {
+    err = 1.f - 1.f / se;  // max p = exp(0) / sum
+  } else {
+    // H = log(sum) - sum_k d_k e_k / sum ; normalised by ln K
+    const float H = logf(se) - sle / se;
+    err = K > 1 ? H / logf((float)K) : 0.f;
+  }
+  err = fminf(fmaxf(err, 0.f), 1.f);  // err in [0, 1] (trace.py:93)
+  *err_out = err;
+  *label_out = arg;
+}
+
+// last CTA: stable compaction of the survivors + scatter of exiting rows
+__device__ void compact_and_scatter(int64_t B, const uint8_t* alive_in, const Out& o) {
+  __shared__ int warp_tot[THREADS / 32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t r0 = 0; r0 < B; r0 += THREADS) {
+    const int64_t row = r0 + threadIdx.x;
+    const bool valid = row < B;
+    const uint8_t ex = valid ? __ldcg(o.exits + row) : 0;
+    const bool alive = valid && (alive_in ? alive_in[row] != 0 : true);
+    const bool keep = alive && !ex;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_tot[wid] = __popc(m);
+    __syncthreads();
+    int off = base;
+    for (int w = 0; w < wid; ++w) off += warp_tot[w];
+    if (keep) o.keep[off + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
+    if (valid && ex && o.slot_label) {
+      const int32_t s = o.slot ? o.slot[row] : (int32_t)row;
+      o.slot_label[s] = __ldcg(o.label + row);
+      o.slot_err[s] = __ldcg(o.err + row);
+      o.slot_site[s] = o.site;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < THREADS / 32; ++w) base += warp_tot[w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *o.n_keep = base;
+}
+
+__device__ __forceinline__ bool last_cta(unsigned* done) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// pool + FC + confidence + compare for one row per CTA, K <= MAXK_FUSED
+template <typename TF, typename TW>
+__global__ void __launch_bounds__(THREADS)
+    k_exit_fused(const TF* __restrict__ feat, int64_t B, int C, int HW, int nhwc,
+                 const TW* __restrict__ W, const float* __restrict__ bias, int K, int conf,
+                 double threshold, const uint8_t* __restrict__ alive_in, Out o) {
+  extern __shared__ float sh[];  // pooled[C], logits[K]
+  float* pooled = sh;
+  float* logits = sh + C;
+  const int64_t row = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const float inv = 1.f / (float)HW;
+  if (nhwc || HW == 1) {
+    // channels contiguous: threads over channels, loop over positions
+    const TF* base = feat + row * (int64_t)HW * C;
+    for (int c = threadIdx.x; c < C; c += THREADS) {
+      float acc = 0.f;
+      for (int p = 0; p < HW; ++p) acc += ld_f32(base, (int64_t)p * C + c);
+      pooled[c] = acc * inv;
+    }
+  } else {
+    // NCHW: one warp per channel, lanes over the contiguous HW plane
+    const TF* base = feat + row * (int64_t)C * HW;
+    for (int c = wid; c < C; c += THREADS / 32) {
+      float acc = 0.f;
+      for (int p = lane; p < HW; p += 32) acc += ld_f32(base, (int64_t)c * HW + p);
+      acc = warp_sum(acc);
+      if (lane == 0) pooled[c] = acc * inv;
+    }
+  }
+  __syncthreads();
+  // logits: one warp per output class, lanes over channels
+  for (int k = wid; k < K; k += THREADS / 32) {
+    float acc = 0.f;
+    for (int c = lane; c < C; c += 32) acc += ld_f32(W, (int64_t)k * C + c) * pooled[c];
+    acc = warp_sum(acc);
+    if (lane == 0) logits[k] = acc + (bias ? bias[k] : 0.f);
+  }
+  __syncthreads();
+  if (o.logits)
+    for (int k = threadIdx.x; k < K; k += THREADS) o.logits[row * K + k] = logits[k];
+  if (wid == 0) {
+    float err;
+    int label;
+    confidence(logits, K, conf, &err, &label);
+    if (lane == 0) {
+      const bool alive = alive_in ? alive_in[row] != 0 : true;
+      o.err[row] = err;
+      o.label[row] = label;
+      o.exits[row] = (alive && (double)err < threshold) ? 1 : 0;
+    }
+  }
+  if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
+}
+
+// confidence + compare + compaction from precomputed logits [B, K] (fp32)
+__global__ void __launch_bounds__(THREADS)
+    k_exit_logits(const float* __restrict__ logits_in, int64_t B, int K, int conf,
+                  double threshold, const uint8_t* __restrict__ alive_in, Out o) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * (THREADS / 32) + wid;  // one warp per row
+  if (row < B) {
+    float err;
+    int label;
+    confidence(logits_in + row * K, K, conf, &err, &label);
+    if (lane == 0) {
+      const bool alive = alive_in ? alive_in[row] != 0 : true;
+      o.err[row] = err;
+      o.label[row] = label;
+      o.exits[row] = (alive && (double)err < threshold) ? 1 : 0;
+    }
+  }
+  if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
+}
+
+// gather surviving rows into a dense buffer (downstream blocks skip exited rows)
+__global__ void k_compact_rows(const uint8_t* __restrict__ src, int64_t row_bytes,
+                               const int32_t* __restrict__ keep, const int32_t* __restrict__ n_keep,
+                               uint8_t* __restrict__ dst) {
+  const int64_t nk = *n_keep;
+  for (int64_t r = blockIdx.x; r < nk; r += gridDim.x) {
+    const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)keep[r] * row_bytes);
+    uint4* d = reinterpret_cast<uint4*>(dst + r * row_bytes);
+    for (int64_t q = threadIdx.x; q < row_bytes / 16; q += blockDim.x) d[q] = __ldg(s + q);
+  }
+}
+
+}  // namespace exitc

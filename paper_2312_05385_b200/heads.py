@@ -1,0 +1,157 @@
+"""Ramp heads and the fused exit controller.
+
+There is no reference code for these rows: eesim abstracts a ramp to an
+(err, label) signal per input. The paper defines a ramp as
+"a final fc layer, prepended with a lightweight pooling" and
+an input exits at the first active ramp whose error score is strictly below
+that ramp's threshold (engine.py:189-220). Here one launch does the pooling,
+the FC, the softmax confidence (1 - max p, or normalised entropy), the
+threshold compare, a stable compaction of the surviving rows and the scatter
+of exiting rows' results to their request slots (ee_exit_controller). Large
+heads (e.g. 1000 ImageNet classes) take their logits from a GEMM and run the
+same epilogue (ee_exit_from_logits).
+
+The parity oracle is a plain torch fp32 restatement (oracle/heads_ref.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from paper_2312_05385_b200 import _native as nat
+from paper_2312_05385_b200.errors import ParameterError
+
+CONF = {"maxprob": 0, "entropy": 1}
+
+
+@dataclass
+class ExitResult:
+    err: "object"     # f32 [B]
+    label: "object"   # i32 [B]
+    exits: "object"   # u8  [B]
+    keep: "object"    # i32 [B], first n_keep entries are the surviving rows (ascending)
+    n_keep: "object"  # i32 [1] (device)
+    logits: "object" = None
+
+    def survivors(self):
+        return self.keep[: int(self.n_keep.item())]
+
+
+@dataclass
+class SlotTable:
+    """Per-request results of exited rows, filled by the scatter."""
+
+    label: "object"  # i32 [slots]
+    err: "object"    # f32 [slots]
+    site: "object"   # i32 [slots]; -1 = not released yet
+
+    @classmethod
+    def empty(cls, slots: int):
+        torch = nat.torch_cuda()
+        return cls(torch.full((slots,), -1, dtype=torch.int32, device="cuda"),
+                   torch.full((slots,), float("nan"), dtype=torch.float32, device="cuda"),
+                   torch.full((slots,), -1, dtype=torch.int32, device="cuda"))
+
+
+def _outputs(torch, b, k, want_logits):
+    dev = "cuda"
+    return (torch.empty(b, dtype=torch.float32, device=dev),
+            torch.empty(b, dtype=torch.int32, device=dev),
+            torch.empty(b, dtype=torch.uint8, device=dev),
+            torch.empty((b, k), dtype=torch.float32, device=dev) if want_logits else None,
+            torch.empty(b, dtype=torch.int32, device=dev),
+            torch.empty(1, dtype=torch.int32, device=dev))
+
+
+def _check_aux(torch, b, alive, slot):
+    if alive is not None and (alive.dtype != torch.uint8 or alive.numel() != b or not alive.is_cuda):
+        raise ParameterError("alive must be a CUDA uint8 tensor with one byte per row")
+    if slot is not None and (slot.dtype != torch.int32 or slot.numel() != b or not slot.is_cuda):
+        raise ParameterError("slot must be a CUDA int32 tensor with one entry per row")
+
+
+class ExitController:
+    """One ramp: fused pool -> FC -> confidence -> compare -> compact -> scatter."""
+
+    def __init__(self, weight, bias=None, *, conf: str = "maxprob", site: int = 0):
+        torch = nat.torch_cuda()
+        if conf not in CONF:
+            raise ParameterError(f"conf must be one of {sorted(CONF)}")
+        if weight.dim() != 2:
+            raise ParameterError("weight must be [K, C]")
+        if weight.dtype not in (torch.float32, torch.bfloat16):
+            raise ParameterError("weight must be fp32 or bf16")
+        self.weight = weight.detach().contiguous().cuda()
+        self.bias = None if bias is None else bias.detach().float().contiguous().cuda()
+        self.k, self.c = self.weight.shape
+        self.conf = conf
+        self.site = site
+
+    def __call__(self, feat, threshold: float, *, alive=None, slot=None,
+                 slots: SlotTable | None = None, want_logits: bool = False) -> ExitResult:
+        """feat: [B, C, H, W] / [B, C] (NCHW) or channels-last memory format; fp32 or bf16."""
+        torch = nat.torch_cuda()
+        if feat.dtype not in (torch.float32, torch.bfloat16) or not feat.is_cuda:
+            raise ParameterError("feat must be a CUDA fp32 or bf16 tensor")
+        b = feat.shape[0]
+        if feat.dim() == 2:
+            c, hw, nhwc = feat.shape[1], 1, 0
+            feat = feat.contiguous()
+        elif feat.dim() == 4:
+            c, hw = feat.shape[1], feat.shape[2] * feat.shape[3]
+            if feat.is_contiguous(memory_format=torch.channels_last) and not feat.is_contiguous():
+                nhwc = 1
+            else:
+                feat, nhwc = feat.contiguous(), 0
+        else:
+            raise ParameterError("feat must be [B, C] or [B, C, H, W]")
+        if c != self.c:
+            raise ParameterError(f"feat has {c} channels, head expects {self.c}")
+        _check_aux(torch, b, alive, slot)
+        err, label, exits, logits, keep, n_keep = _outputs(torch, b, self.k, want_logits)
+        nat.check(nat.load_library().ee_exit_controller(
+            nat.workspace(), feat.data_ptr(), int(feat.dtype == torch.bfloat16), b, c, hw, nhwc,
+            self.weight.data_ptr(), int(self.weight.dtype == torch.bfloat16), nat.ptr(self.bias),
+            self.k, CONF[self.conf], float(threshold), nat.ptr(alive), nat.ptr(slot), self.site,
+            err.data_ptr(), label.data_ptr(), exits.data_ptr(), nat.ptr(logits),
+            keep.data_ptr(), n_keep.data_ptr(),
+            nat.ptr(slots.label if slots else None), nat.ptr(slots.err if slots else None),
+            nat.ptr(slots.site if slots else None), nat.stream_handle(torch)))
+        return ExitResult(err, label, exits, keep, n_keep, logits)
+
+
+def exit_from_logits(logits, threshold: float, *, conf: str = "maxprob", site: int = 0,
+                     alive=None, slot=None, slots: SlotTable | None = None) -> ExitResult:
+    """Confidence + compare + compaction + scatter over precomputed fp32 logits [B, K]."""
+    torch = nat.torch_cuda()
+    if logits.dtype != torch.float32 or logits.dim() != 2 or not logits.is_cuda:
+        raise ParameterError("logits must be a CUDA fp32 [B, K] tensor")
+    logits = logits.contiguous()
+    b, k = logits.shape
+    _check_aux(torch, b, alive, slot)
+    err, label, exits, _, keep, n_keep = _outputs(torch, b, k, False)
+    nat.check(nat.load_library().ee_exit_from_logits(
+        nat.workspace(), logits.data_ptr(), b, k, CONF[conf], float(threshold), nat.ptr(alive),
+        nat.ptr(slot), site, err.data_ptr(), label.data_ptr(), exits.data_ptr(),
+        keep.data_ptr(), n_keep.data_ptr(),
+        nat.ptr(slots.label if slots else None), nat.ptr(slots.err if slots else None),
+        nat.ptr(slots.site if slots else None), nat.stream_handle(torch)))
+    return ExitResult(err, label, exits, keep, n_keep, None)
+
+
+def compact_rows(src, keep, n_keep, out=None):
+    """Gather the surviving rows of `src` ([B, ...], contiguous) into a dense
+    buffer (compaction mode: downstream blocks run only on these rows).
+    Returns the full-capacity output; its first n_keep rows are valid."""
+    torch = nat.torch_cuda()
+    src = src.contiguous()
+    b = src.shape[0]
+    row_bytes = src.numel() // max(b, 1) * src.element_size()
+    if row_bytes % 16:
+        raise ParameterError("row size must be a multiple of 16 bytes")
+    if out is None:
+        out = torch.empty_like(src)
+    nat.check(nat.load_library().ee_compact_rows(
+        src.data_ptr(), row_bytes, keep.data_ptr(), n_keep.data_ptr(), b, out.data_ptr(),
+        nat.stream_handle(torch)))
+    return out

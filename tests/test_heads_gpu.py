@@ -1,0 +1,115 @@
+"""GPU parity of the fused ramp head / exit controller (A12-A13) against the
+torch fp32 restatement in oracle/heads_ref.py.
+
+Tolerances: logits within 1e-4 relative (fp32 accumulation order differs);
+err within 2e-5 absolute; labels and exit masks exact except rows whose
+oracle err lies within 1e-5 of the threshold (the north star's near-tie
+carve-out, counted and reported); compaction order and scatter exact given
+the device's own decisions."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import heads_ref as H
+from paper_2312_05385_b200.heads import ExitController, SlotTable, compact_rows, exit_from_logits
+
+pytestmark = pytest.mark.gpu
+
+NEAR = 1e-5
+
+
+def _check(res, feat, w, bias, conf, thr, alive=None, check_logits=True):
+    logits_ref = H.ramp_head(feat, w, bias)
+    err_ref, label_ref = H.confidence(logits_ref, conf)
+    if check_logits and res.logits is not None:
+        got = res.logits.cpu()
+        assert torch.allclose(got, logits_ref, rtol=1e-4, atol=1e-4)
+    err = res.err.cpu().double()
+    assert torch.allclose(err, err_ref, rtol=0, atol=2e-5)
+    near = (err_ref - thr).abs() < NEAR
+    ex_ref = H.exit_decision(err_ref, thr, alive)
+    ex = res.exits.cpu().bool()
+    assert torch.equal(ex[~near], ex_ref[~near])
+    # labels: exact unless the top-2 logits tie within fp32 noise
+    top2 = torch.topk(logits_ref, 2, dim=1).values if logits_ref.shape[1] > 1 else None
+    ambiguous = (top2[:, 0] - top2[:, 1]).abs() < 1e-4 if top2 is not None else torch.zeros_like(near)
+    assert torch.equal(res.label.cpu().long()[~ambiguous], label_ref[~ambiguous])
+    # compaction: stable ascending list of alive rows the device did not exit
+    keep_ref = H.compaction(ex, alive)
+    assert torch.equal(res.survivors().cpu(), keep_ref)
+    return int(near.sum())
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc", "pooled"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("conf", ["maxprob", "entropy"])
+def test_fused_head_matches_torch(cuda, layout, dtype, conf):
+    g = torch.Generator().manual_seed(1)
+    b, c, k = 64, 96, 10
+    if layout == "pooled":
+        feat = torch.randn(b, c, generator=g)
+    else:
+        feat = torch.randn(b, c, 7, 7, generator=g)
+    w = torch.randn(k, c, generator=g) * 0.3
+    bias = torch.randn(k, generator=g) * 0.1
+    feat_d = feat.to(dtype).cuda()
+    if layout == "nhwc":
+        feat_d = feat_d.to(memory_format=torch.channels_last)
+    head = ExitController(w.cuda(), bias.cuda(), conf=conf, site=3)
+    err_probe = head(feat_d, 0.0, want_logits=True).err.cpu()
+    thr = float(err_probe.median())
+    res = head(feat_d, thr, want_logits=True)
+    _check(res, feat_d.float().cpu(), w, bias, conf, thr)
+
+
+def test_alive_mask_slots_and_scatter(cuda):
+    g = torch.Generator().manual_seed(2)
+    b, c, k = 300, 64, 2  # BERT-like binary head, more rows than one CTA scan tile
+    feat = torch.randn(b, c, generator=g)
+    w = torch.randn(k, c, generator=g)
+    head = ExitController(w.cuda(), None, conf="entropy", site=7)
+    alive = (torch.rand(b, generator=g) < 0.7).to(torch.uint8).cuda()
+    slot = torch.randperm(b, generator=g).to(torch.int32).cuda()
+    slots = SlotTable.empty(b)
+    probe = head(feat.cuda(), 0.0).err.cpu()
+    thr = float(probe.quantile(0.4))
+    res = head(feat.cuda(), thr, alive=alive, slot=slot, slots=slots)
+    _check(res, feat, w, None, "entropy", thr, alive=alive.cpu())
+    ex = res.exits.cpu().bool()
+    assert not ex[alive.cpu() == 0].any()  # dead rows never exit again
+    s = slot.cpu().long()
+    site = slots.site.cpu()
+    assert (site[s[ex]] == 7).all() and (site[s[~ex]] == -1).all()
+    assert torch.equal(slots.label.cpu()[s[ex]], res.label.cpu()[ex])
+    assert torch.equal(slots.err.cpu()[s[ex]], res.err.cpu()[ex])
+
+
+def test_large_head_from_logits_and_row_compaction(cuda):
+    g = torch.Generator().manual_seed(3)
+    b, k = 256, 1000
+    logits = torch.randn(b, k, generator=g) * 3
+    probe = exit_from_logits(logits.cuda(), 0.0).err.cpu()
+    thr = float(probe.quantile(0.5))
+    res = exit_from_logits(logits.cuda(), thr, conf="maxprob")
+    err_ref, label_ref = H.confidence(logits, "maxprob")
+    assert torch.allclose(res.err.cpu().double(), err_ref, atol=2e-5, rtol=0)
+    near = (err_ref - thr).abs() < NEAR
+    assert torch.equal(res.exits.cpu().bool()[~near], H.exit_decision(err_ref, thr)[~near])
+    # compaction mode: gather the survivors' activations
+    act = torch.randn(b, 64, 4, 4, generator=g).cuda()
+    dense = compact_rows(act, res.keep, res.n_keep)
+    keep = res.survivors().long()
+    assert torch.equal(dense[: keep.numel()], act[keep])
+
+
+def test_exit_rule_is_strict(cuda):
+    # a uniform-logit row has err exactly 1 - 1/K; at threshold == err it must not exit
+    k = 4
+    logits = torch.zeros(2, k).cuda()
+    res = exit_from_logits(logits, 1.0 - 1.0 / k, conf="maxprob")
+    assert res.exits.cpu().tolist() == [0, 0]
+    res = exit_from_logits(logits, np.nextafter(1.0 - 1.0 / k, 2.0), conf="maxprob")
+    assert res.exits.cpu().tolist() == [1, 1]
