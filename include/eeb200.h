@@ -150,6 +150,18 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits, int64_t b, int3
                         uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
                         float* d_slot_err, int32_t* d_slot_site, void* stream);
 
+/* Tensor-core ramp-head GEMM (tcgen05.mma, TMEM accumulators):
+ * d_c f32 [m, n] = d_a bf16 [m, k] (row-major) x d_b bf16 [n, k]^T (row-major,
+ * i.e. nn.Linear weight layout) + d_bias f32 [n] (nullable). k % 8 == 0.
+ * splits <= 0 picks a split-K that fills the SMs; split partials are summed
+ * in a fixed order (deterministic). */
+int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
+                    float* d_c, int64_t m, int64_t n, int64_t k, int32_t splits, void* stream);
+
+/* Global average pool NCHW f32 [b, c, hw] -> bf16 [b, c] (round to nearest
+ * even): the A operand of a large ramp head. */
+int ee_pool_bf16(const float* d_x, int64_t b, int32_t c, int32_t hw, void* d_out, void* stream);
+
 /* Gathers rows d_keep[0 .. *d_nkeep) of d_src (row_bytes each, multiple of
  * 16) into the dense d_dst (capacity max_rows rows): downstream blocks then
  * run only on the non-exited samples (compaction mode). */

@@ -466,6 +466,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 #include "sweep_diag.cuh"
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
+#include "gemm_tc.cuh"
 namespace {
 
 __global__ void k_fill_nan(double* a, double* b, int64_t C) {
@@ -1323,6 +1324,70 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
   const int rows_per = exitc::THREADS / 32;
   exitc::k_exit_logits<<<(unsigned)ceil_div(b, rows_per), exitc::THREADS, 0, st>>>(
       d_logits_in, b, k, conf, threshold, d_alive, o);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
+                    float* d_c, int64_t m, int64_t n, int64_t k, int32_t splits, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
+    return fail(EE_ERR_ARG, "bad GEMM shape");
+  if (k % 8) return fail(EE_ERR_ARG, "K must be a multiple of 8 (16-byte rows)");
+  if (!d_a || !d_b || !d_c) return fail(EE_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_b)) & 15)
+    return fail(EE_ERR_ARG, "A and B must be 16-byte aligned");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  const int BN = n >= 128 ? 128 : 64;
+  const int64_t mt = ceil_div(m, gemmtc::BM), nt = ceil_div(n, BN);
+  const int kt_total = (int)ceil_div(k, gemmtc::BK);
+  int sp = splits;
+  if (sp <= 0) sp = (int)std::max<int64_t>(1, std::min<int64_t>(kt_total, sm_count() / std::max<int64_t>(1, mt * nt)));
+  sp = std::min(sp, kt_total);
+  const int per = (kt_total + sp - 1) / sp;
+  sp = (kt_total + per - 1) / per;  // no empty splits
+  float* partials = nullptr;
+  if (sp > 1) {
+    int rc = ws_reserve(ws, (size_t)sp * m * n * 4, 0);
+    if (rc) return rc;
+    partials = static_cast<float*>(ws->d_buf);
+  }
+  const size_t smem = 2 * ((size_t)gemmtc::BM * gemmtc::BK * 2 + (size_t)BN * gemmtc::BK * 2);
+  dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)sp);
+  {
+    ProfScope ps(ws, st, "k_gemm_bf16");
+    if (BN == 128) {
+      EE_CUDA(cudaFuncSetAttribute(gemmtc::k_gemm_bf16<128>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      gemmtc::k_gemm_bf16<128><<<grid, gemmtc::THREADS, smem, st>>>(
+          static_cast<const uint16_t*>(d_a), static_cast<const uint16_t*>(d_b), d_bias, d_c,
+          (int)m, (int)n, (int)k, per, partials);
+    } else {
+      EE_CUDA(cudaFuncSetAttribute(gemmtc::k_gemm_bf16<64>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      gemmtc::k_gemm_bf16<64><<<grid, gemmtc::THREADS, smem, st>>>(
+          static_cast<const uint16_t*>(d_a), static_cast<const uint16_t*>(d_b), d_bias, d_c,
+          (int)m, (int)n, (int)k, per, partials);
+    }
+  }
+  EE_LAUNCH_CHECK();
+  if (sp > 1) {
+    ProfScope ps(ws, st, "k_splitk_sum");
+    const int64_t mn = m * n;
+    gemmtc::k_splitk_sum<<<(unsigned)std::min<int64_t>(ceil_div(mn, 256), sm_count() * 8), 256, 0,
+                           st>>>(partials, sp, mn, (int)n, d_bias, d_c);
+    EE_LAUNCH_CHECK();
+  }
+  return EE_OK;
+}
+
+int ee_pool_bf16(const float* d_x, int64_t b, int32_t c, int32_t hw, void* d_out, void* stream) {
+  if (b < 1 || c < 1 || hw < 1) return fail(EE_ERR_ARG, "bad shape");
+  if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
+  const int64_t bc = b * c;
+  gemmtc::k_pool_bf16<<<(unsigned)std::min<int64_t>(ceil_div(bc, 8), sm_count() * 16), 256, 0,
+                        (cudaStream_t)stream>>>(d_x, bc, hw, static_cast<uint16_t*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

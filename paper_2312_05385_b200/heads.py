@@ -155,3 +155,58 @@ def compact_rows(src, keep, n_keep, out=None):
         src.data_ptr(), row_bytes, keep.data_ptr(), n_keep.data_ptr(), b, out.data_ptr(),
         nat.stream_handle(torch)))
     return out
+
+
+def linear_tc(x, weight, bias=None, *, splits: int = 0):
+    """fp32 [M, N] = x bf16 [M, K] @ weight bf16 [N, K]^T + bias, on the 5th-gen
+    tensor cores (tcgen05.mma with TMEM accumulators; ee_gemm_bf16_tn)."""
+    torch = nat.torch_cuda()
+    if x.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise ParameterError("linear_tc takes bf16 operands")
+    x, weight = x.contiguous(), weight.contiguous()
+    m, k = x.shape
+    n = weight.shape[0]
+    if weight.shape[1] != k:
+        raise ParameterError("inner dimensions differ")
+    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    b = None if bias is None else bias.float().contiguous()
+    nat.check(nat.load_library().ee_gemm_bf16_tn(
+        nat.workspace(), x.data_ptr(), weight.data_ptr(), nat.ptr(b), out.data_ptr(), m, n, k,
+        splits, nat.stream_handle(torch)))
+    return out
+
+
+def pool_bf16(x):
+    """Global average pool of an NCHW fp32 map to a bf16 [B, C] GEMM operand."""
+    torch = nat.torch_cuda()
+    if x.dtype != torch.float32 or x.dim() != 4:
+        raise ParameterError("pool_bf16 takes an fp32 [B, C, H, W] tensor")
+    x = x.contiguous()
+    b, c, h, w = x.shape
+    out = torch.empty((b, c), dtype=torch.bfloat16, device="cuda")
+    nat.check(nat.load_library().ee_pool_bf16(x.data_ptr(), b, c, h * w, out.data_ptr(),
+                                              nat.stream_handle(torch)))
+    return out
+
+
+class LargeRampHead:
+    """Ramp with a wide classifier (e.g. 1000 ImageNet classes): pool -> bf16
+    tensor-core GEMM -> fused confidence / compare / compaction / scatter."""
+
+    def __init__(self, weight, bias=None, *, conf: str = "maxprob", site: int = 0):
+        torch = nat.torch_cuda()
+        self.weight = weight.detach().to(torch.bfloat16).contiguous().cuda()
+        self.bias = None if bias is None else bias.detach().float().contiguous().cuda()
+        self.conf = conf
+        self.site = site
+
+    def __call__(self, feat, threshold: float, *, alive=None, slot=None,
+                 slots: SlotTable | None = None, want_logits: bool = False) -> ExitResult:
+        torch = nat.torch_cuda()
+        x = pool_bf16(feat) if feat.dim() == 4 else feat.to(torch.bfloat16)
+        logits = linear_tc(x, self.weight, self.bias)
+        res = exit_from_logits(logits, threshold, conf=self.conf, site=self.site, alive=alive,
+                               slot=slot, slots=slots)
+        if want_logits:
+            res.logits = logits
+        return res
