@@ -128,7 +128,8 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
  * [k] fp32 nullable, k <= 256), softmax confidence (conf 0: err = 1 - max p;
  * conf 1: err = H(p)/ln k), argmax label, and the reference exit rule
  * (double)err < threshold (strict, engine.py:207) for rows whose d_alive byte
- * is 1 (d_alive NULL = all alive). Outputs per row: d_err f32, d_label i32,
+ * is 1 (d_alive NULL = all alive); d_alive is updated in place (exiting rows
+ * are cleared), so chaining ramps needs no extra launch. Outputs per row: d_err f32, d_label i32,
  * d_exit u8, optional d_logits f32 [b, k]. Then, in the same launch, the
  * surviving (alive, non-exiting) rows are compacted in ascending row order
  * into d_keep with their count in *d_nkeep, and each exiting row's (label,
@@ -137,7 +138,7 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
 int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, int64_t b,
                        int32_t c, int32_t hw, int32_t nhwc, const void* d_w, int32_t w_bf16,
                        const float* d_bias, int32_t k, int32_t conf, double threshold,
-                       const uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
+                       uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
                        int32_t* d_label, uint8_t* d_exit, float* d_logits, int32_t* d_keep,
                        int32_t* d_nkeep, int32_t* d_slot_label, float* d_slot_err,
                        int32_t* d_slot_site, void* stream);
@@ -145,7 +146,7 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
 /* Same epilogue from precomputed fp32 logits [b, k] (large heads whose FC runs
  * as a tensor-core GEMM). */
 int ee_exit_from_logits(ee_workspace* ws, const float* d_logits, int64_t b, int32_t k,
-                        int32_t conf, double threshold, const uint8_t* d_alive,
+                        int32_t conf, double threshold, uint8_t* d_alive,
                         const int32_t* d_slot, int32_t site, float* d_err, int32_t* d_label,
                         uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
                         float* d_slot_err, int32_t* d_slot_site, void* stream);
@@ -158,9 +159,10 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits, int64_t b, int3
 int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
                     float* d_c, int64_t m, int64_t n, int64_t k, int32_t splits, void* stream);
 
-/* Global average pool NCHW f32 [b, c, hw] -> bf16 [b, c] (round to nearest
- * even): the A operand of a large ramp head. */
-int ee_pool_bf16(const float* d_x, int64_t b, int32_t c, int32_t hw, void* d_out, void* stream);
+/* Global average pool NCHW [b, c, hw] (f32, or bf16 when x_bf16) -> bf16
+ * [b, c] (round to nearest even): the A operand of a large ramp head. */
+int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t hw, void* d_out,
+                 void* stream);
 
 /* Gathers rows d_keep[0 .. *d_nkeep) of d_src (row_bytes each, multiple of
  * 16) into the dense d_dst (capacity max_rows rows): downstream blocks then

@@ -1264,7 +1264,7 @@ static int exit_out(ee_workspace* ws, cudaStream_t st, int64_t b, const int32_t*
 int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, int64_t b,
                        int32_t c, int32_t hw, int32_t nhwc, const void* d_w, int32_t w_bf16,
                        const float* d_bias, int32_t k, int32_t conf, double threshold,
-                       const uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
+                       uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
                        int32_t* d_label, uint8_t* d_exit, float* d_logits, int32_t* d_keep,
                        int32_t* d_nkeep, int32_t* d_slot_label, float* d_slot_err,
                        int32_t* d_slot_site, void* stream) {
@@ -1306,7 +1306,7 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
 }
 
 int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, int32_t k,
-                        int32_t conf, double threshold, const uint8_t* d_alive,
+                        int32_t conf, double threshold, uint8_t* d_alive,
                         const int32_t* d_slot, int32_t site, float* d_err, int32_t* d_label,
                         uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
                         float* d_slot_err, int32_t* d_slot_site, void* stream) {
@@ -1382,12 +1382,18 @@ int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const fl
   return EE_OK;
 }
 
-int ee_pool_bf16(const float* d_x, int64_t b, int32_t c, int32_t hw, void* d_out, void* stream) {
+int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t hw, void* d_out,
+                 void* stream) {
   if (b < 1 || c < 1 || hw < 1) return fail(EE_ERR_ARG, "bad shape");
   if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
   const int64_t bc = b * c;
-  gemmtc::k_pool_bf16<<<(unsigned)std::min<int64_t>(ceil_div(bc, 8), sm_count() * 16), 256, 0,
-                        (cudaStream_t)stream>>>(d_x, bc, hw, static_cast<uint16_t*>(d_out));
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(bc, 8), sm_count() * 16);
+  if (x_bf16)
+    gemmtc::k_pool_bf16<uint16_t><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const uint16_t*>(d_x), bc, hw, static_cast<uint16_t*>(d_out));
+  else
+    gemmtc::k_pool_bf16<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const float*>(d_x), bc, hw, static_cast<uint16_t*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

@@ -107,6 +107,7 @@ __device__ __forceinline__ void confidence(const float* l, int K, int conf, floa
 
 // last CTA: stable compaction of the survivors + scatter of exiting rows
 __device__ void compact_and_scatter(int64_t B, const uint8_t* alive_in, const Out& o) {
+  // alive_in already has this launch's exits cleared (keep = alive after the ramp)
   __shared__ int warp_tot[THREADS / 32];
   __shared__ int base;
   if (threadIdx.x == 0) base = 0;
@@ -116,7 +117,7 @@ __device__ void compact_and_scatter(int64_t B, const uint8_t* alive_in, const Ou
     const int64_t row = r0 + threadIdx.x;
     const bool valid = row < B;
     const uint8_t ex = valid ? __ldcg(o.exits + row) : 0;
-    const bool alive = valid && (alive_in ? alive_in[row] != 0 : true);
+    const bool alive = valid && (alive_in ? __ldcg(alive_in + row) != 0 : true);
     const bool keep = alive && !ex;
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) warp_tot[wid] = __popc(m);
@@ -153,7 +154,7 @@ template <typename TF, typename TW>
 __global__ void __launch_bounds__(THREADS)
     k_exit_fused(const TF* __restrict__ feat, int64_t B, int C, int HW, int nhwc,
                  const TW* __restrict__ W, const float* __restrict__ bias, int K, int conf,
-                 double threshold, const uint8_t* __restrict__ alive_in, Out o) {
+                 double threshold, uint8_t* __restrict__ alive_in, Out o) {
   extern __shared__ float sh[];  // pooled[C], logits[K]
   float* pooled = sh;
   float* logits = sh + C;
@@ -195,9 +196,11 @@ __global__ void __launch_bounds__(THREADS)
     confidence(logits, K, conf, &err, &label);
     if (lane == 0) {
       const bool alive = alive_in ? alive_in[row] != 0 : true;
+      const bool ex = alive && (double)err < threshold;
       o.err[row] = err;
       o.label[row] = label;
-      o.exits[row] = (alive && (double)err < threshold) ? 1 : 0;
+      o.exits[row] = ex ? 1 : 0;
+      if (ex && alive_in) alive_in[row] = 0;  // exited rows stop being alive
     }
   }
   if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(THREADS)
 // confidence + compare + compaction from precomputed logits [B, K] (fp32)
 __global__ void __launch_bounds__(THREADS)
     k_exit_logits(const float* __restrict__ logits_in, int64_t B, int K, int conf,
-                  double threshold, const uint8_t* __restrict__ alive_in, Out o) {
+                  double threshold, uint8_t* __restrict__ alive_in, Out o) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * (THREADS / 32) + wid;  // one warp per row
   if (row < B) {
@@ -215,9 +218,11 @@ __global__ void __launch_bounds__(THREADS)
     confidence(logits_in + row * K, K, conf, &err, &label);
     if (lane == 0) {
       const bool alive = alive_in ? alive_in[row] != 0 : true;
+      const bool ex = alive && (double)err < threshold;
       o.err[row] = err;
       o.label[row] = label;
-      o.exits[row] = (alive && (double)err < threshold) ? 1 : 0;
+      o.exits[row] = ex ? 1 : 0;
+      if (ex && alive_in) alive_in[row] = 0;
     }
   }
   if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);

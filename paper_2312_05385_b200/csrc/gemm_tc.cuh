@@ -220,14 +220,18 @@ __global__ void k_splitk_sum(const float* __restrict__ partials, int splits, int
   }
 }
 
-// global average pool NCHW [B, C, HW] -> bf16 [B, C] (GEMM A operand)
-__global__ void k_pool_bf16(const float* __restrict__ x, int64_t BC, int HW,
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(uint16_t v) { return __uint_as_float((uint32_t)v << 16); }
+
+// global average pool NCHW [B, C, HW] (fp32 or bf16) -> bf16 [B, C] (GEMM A operand)
+template <typename T>
+__global__ void k_pool_bf16(const T* __restrict__ x, int64_t BC, int HW,
                             uint16_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   for (int64_t bc = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); bc < BC;
        bc += (int64_t)gridDim.x * (blockDim.x / 32)) {
     float acc = 0.f;
-    for (int p = lane; p < HW; p += 32) acc += __ldg(x + bc * HW + p);
+    for (int p = lane; p < HW; p += 32) acc += to_f32(__ldg(x + bc * HW + p));
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {

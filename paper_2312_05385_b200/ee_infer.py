@@ -1,0 +1,258 @@
+"""Early-exit batch inference on the GPU (BASELINE configs 1-3; north star (1)-(2)).
+
+A backbone is split into stages at its ramp sites. After each active site the
+ramp head + exit controller (heads.py) pools, classifies, scores confidence,
+compares against the site's threshold, clears the exiting rows from the alive
+mask in place and scatters their (label, err, site) to their request slots —
+one launch per ramp, no host round trip in feedback mode.
+
+Two modes, SURVEY §7 hard part 6:
+  * "feedback" (default; Apparate semantics): results exit early
+    but every input runs to completion, so every active ramp's (err, label)
+    and the final label are observed for all inputs — exactly the signals
+    the accuracy monitor and the threshold tuner consume (serving.py:277-281).
+  * "compact": surviving rows are gathered into a dense batch after each ramp
+    (stable ascending order), so later stages run only on non-exited rows;
+    later ramps' signals of exited rows are then censored (NaN / -1).
+
+The exit rule is the reference's (engine.py:189-220): first active ramp with
+err strictly below its threshold; otherwise the final model label is
+released. `BatchResult.records()` re-expresses a batch as RequestRecords, the
+form the reference's tuner consumes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from paper_2312_05385_b200 import _native as nat
+from paper_2312_05385_b200.errors import ParameterError
+from paper_2312_05385_b200.heads import ExitController, LargeRampHead, SlotTable, exit_from_logits
+
+
+@dataclass
+class BatchResult:
+    released_label: "object"  # i32 [B]
+    released_site: "object"   # i32 [B]: ramp index, or n_ramps for the final model
+    released_err: "object"    # f32 [B]
+    ramp_err: "object"        # f32 [R, B] every active ramp's error score (NaN if censored)
+    ramp_label: "object"      # i32 [R, B]
+    final_label: "object"     # i32 [B] (-1 if censored in compaction mode)
+    release_ms: np.ndarray | None = None  # per request, from batch start (host, if timed)
+    batch_ms: float | None = None
+
+    def records(self, site_names: Sequence[str], first_id: int = 0, arrival_ms: float = 0.0):
+        """The batch as reference RequestRecords (err/label per site, final label)."""
+        from paper_2312_05385_b200.trace import RampSignal, RequestRecord
+
+        err = self.ramp_err.double().cpu().numpy()
+        lab = self.ramp_label.cpu().numpy()
+        fin = self.final_label.cpu().numpy()
+        out = []
+        for i in range(err.shape[1]):
+            sig = {name: RampSignal(float(err[j, i]), int(lab[j, i])) for j, name in enumerate(site_names)}
+            out.append(RequestRecord(first_id + i, arrival_ms, sig, int(fin[i])))
+        return out
+
+
+@dataclass
+class EEPipeline:
+    """stages[j] maps the previous activation to site j's activation; the last
+    stage produces final logits. ramps maps a stage index to its ramp head."""
+
+    stages: list
+    ramps: dict
+    site_names: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self.ramp_order = sorted(self.ramps)
+        if any(j >= len(self.stages) - 1 for j in self.ramp_order):
+            raise ParameterError("ramps must sit before the final stage")
+        if not self.site_names:
+            self.site_names = [f"s{j}" for j in self.ramp_order]
+
+    @property
+    def n_ramps(self) -> int:
+        return len(self.ramp_order)
+
+    def run(self, x, thresholds: Sequence[float], *, mode: str = "feedback",
+            timed: bool = False) -> BatchResult:
+        torch = nat.torch_cuda()
+        if len(thresholds) != self.n_ramps:
+            raise ParameterError(f"{self.n_ramps} thresholds expected")
+        if mode not in ("feedback", "compact"):
+            raise ParameterError("mode must be 'feedback' or 'compact'")
+        b = x.shape[0]
+        R = self.n_ramps
+        dev = "cuda"
+        slots = SlotTable.empty(b)
+        alive = torch.ones(b, dtype=torch.uint8, device=dev)
+        rows = torch.arange(b, dtype=torch.int32, device=dev)  # request slot of each live row
+        ramp_err = torch.full((R, b), float("nan"), dtype=torch.float32, device=dev)
+        ramp_label = torch.full((R, b), -1, dtype=torch.int32, device=dev)
+        final_label = torch.full((b,), -1, dtype=torch.int32, device=dev)
+        marks = []
+        if timed:
+            start = torch.cuda.Event(enable_timing=True)
+            start.record()
+        h = x
+        r = 0
+        with torch.no_grad():
+            for j, stage in enumerate(self.stages[:-1]):
+                if h.shape[0] == 0:
+                    break
+                h = stage(h)
+                head = self.ramps.get(j)
+                if head is None:
+                    continue
+                res = head(h, float(thresholds[r]), alive=alive, slot=rows, slots=slots)
+                ramp_err[r].index_copy_(0, rows.long(), res.err)
+                ramp_label[r].index_copy_(0, rows.long(), res.label)
+                if timed:
+                    ev = torch.cuda.Event(enable_timing=True)
+                    ev.record()
+                    marks.append(ev)
+                if mode == "compact":
+                    keep = res.survivors().long()  # host sync: the next stage's batch size
+                    h = h.index_select(0, keep)
+                    rows = rows.index_select(0, keep)
+                    alive = torch.ones(keep.numel(), dtype=torch.uint8, device=dev)
+                r += 1
+            if h.shape[0]:
+                logits = self.stages[-1](h).float()
+                final_label.index_copy_(0, rows.long(), torch.argmax(logits, dim=1).to(torch.int32))
+                # every still-alive row is released with the final model's label
+                exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=R, alive=alive,
+                                 slot=rows, slots=slots)
+        out = BatchResult(slots.label, slots.site, slots.err, ramp_err, ramp_label, final_label)
+        if timed:
+            end = torch.cuda.Event(enable_timing=True)
+            end.record()
+            end.synchronize()
+            t = [start.elapsed_time(m) for m in marks] + [start.elapsed_time(end)]
+            site = slots.site.cpu().numpy()
+            out.release_ms = np.asarray(t)[np.clip(site, 0, R)]
+            out.batch_ms = t[-1]
+        return out
+
+
+# ---------------------------------------------------------------- model builders
+def _calibrate_bn(model, shape, batches: int = 4, seed: int = 0):
+    """Seeded train-mode passes so random-init BatchNorm statistics are sane."""
+    torch = nat.torch_cuda()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    model.train()
+    with torch.no_grad():
+        for _ in range(batches):
+            model(torch.randn(*shape, generator=g, device="cuda"))
+    model.eval()
+
+
+def resnet18_cifar(num_classes: int = 10, ramp_sites=(0, 2, 3, 5, 6, 8), seed: int = 0,
+                   conf: str = "maxprob"):
+    """BASELINE config 1: ResNet-18, CIFAR shape (3x32x32), 6 ramps.
+
+    Sites: 0 stem, 1 layer1.0, 2 layer1.1, 3 layer2.0, 4 layer2.1, 5 layer3.0,
+    6 layer3.1, 7 layer4.0, 8 layer4.1 (SURVEY §8d picks stem, layer1.1,
+    layer2.0, layer3.0, layer3.1, layer4.1)."""
+    torch = nat.torch_cuda()
+    import torchvision
+
+    torch.manual_seed(seed)
+    m = torchvision.models.resnet18(num_classes=num_classes)
+    m.conv1 = torch.nn.Conv2d(3, 64, 3, 1, 1, bias=False)
+    m.maxpool = torch.nn.Identity()
+    m = m.cuda()
+    _calibrate_bn(m, (64, 3, 32, 32), seed=seed)
+    stem = torch.nn.Sequential(m.conv1, m.bn1, m.relu)
+    blocks = [stem, m.layer1[0], m.layer1[1], m.layer2[0], m.layer2[1], m.layer3[0], m.layer3[1],
+              m.layer4[0], m.layer4[1]]
+    chans = [64, 64, 64, 128, 128, 256, 256, 512, 512]
+    final = torch.nn.Sequential(m.avgpool, torch.nn.Flatten(), m.fc)
+    g = torch.Generator().manual_seed(seed + 1)
+    ramps = {}
+    for s in ramp_sites:
+        w = torch.randn(num_classes, chans[s], generator=g) / chans[s] ** 0.5
+        ramps[s] = ExitController(w.cuda(), torch.zeros(num_classes).cuda(), conf=conf, site=len(ramps))
+    names = ["stem", "layer1.0", "layer1.1", "layer2.0", "layer2.1", "layer3.0", "layer3.1",
+             "layer4.0", "layer4.1"]
+    return EEPipeline(blocks + [final], ramps, [names[s] for s in sorted(ramps)]), m
+
+
+def resnet50_imagenet(seed: int = 0, conf: str = "maxprob", dtype=None):
+    """BASELINE config 3: ResNet-50, 224x224, a ramp after each of the 16
+    bottlenecks, 1000-class heads on the tensor-core GEMM path."""
+    torch = nat.torch_cuda()
+    import torchvision
+
+    torch.manual_seed(seed)
+    m = torchvision.models.resnet50().cuda()
+    _calibrate_bn(m, (32, 3, 224, 224), seed=seed)
+    stem = torch.nn.Sequential(m.conv1, m.bn1, m.relu, m.maxpool)
+    blocks = []
+    chans = []
+    for layer, c in ((m.layer1, 256), (m.layer2, 512), (m.layer3, 1024), (m.layer4, 2048)):
+        for blk in layer:
+            blocks.append(blk)
+            chans.append(c)
+    stages = [torch.nn.Sequential(stem, blocks[0])] + blocks[1:]
+    final = torch.nn.Sequential(m.avgpool, torch.nn.Flatten(), m.fc)
+    g = torch.Generator().manual_seed(seed + 1)
+    ramps = {}
+    for s, c in enumerate(chans):
+        w = torch.randn(1000, c, generator=g) / c ** 0.5
+        ramps[s] = LargeRampHead(w.cuda(), None, conf=conf, site=s)
+    names = [f"bottleneck{s}" for s in range(len(chans))]
+    return EEPipeline(stages + [final], ramps, names), m
+
+
+def bert_base(seq: int = 128, seed: int = 0, conf: str = "entropy"):
+    """BASELINE config 2: BERT-base-shape encoder (random init), a ramp after
+    every layer on the token-0 hidden state (768 -> 2), entropy confidence."""
+    torch = nat.torch_cuda()
+    from transformers import BertConfig, BertModel
+
+    torch.manual_seed(seed)
+    cfg = BertConfig(attn_implementation="sdpa")
+    bert = BertModel(cfg, add_pooling_layer=False).cuda().eval()
+
+    class Embed(torch.nn.Module):
+        def forward(self, ids):
+            return bert.embeddings(input_ids=ids)
+
+    class Layer(torch.nn.Module):
+        def __init__(self, layer):
+            super().__init__()
+            self.layer = layer
+
+        def forward(self, h):
+            out = self.layer(h)
+            return out[0] if isinstance(out, tuple) else out
+
+    g = torch.Generator().manual_seed(seed + 1)
+    layers = [Layer(l) for l in bert.encoder.layer]
+    stages = [torch.nn.Sequential(Embed(), layers[0])] + layers[1:]
+    heads = {}
+    for s in range(len(layers)):
+        w = torch.randn(2, cfg.hidden_size, generator=g) / cfg.hidden_size ** 0.5
+        heads[s] = _Token0Head(ExitController(w.cuda(), torch.zeros(2).cuda(), conf=conf, site=s))
+    final_w = (torch.randn(2, cfg.hidden_size, generator=g) / cfg.hidden_size ** 0.5).cuda()
+
+    class Final(torch.nn.Module):
+        def forward(self, h):
+            return h[:, 0].float() @ final_w.t()
+
+    return EEPipeline(stages + [Final()], heads, [f"layer{s}" for s in range(len(layers))]), bert
+
+
+class _Token0Head:
+    """Ramp on a transformer layer: the head reads the token-0 hidden state."""
+
+    def __init__(self, ctrl: ExitController):
+        self.ctrl = ctrl
+
+    def __call__(self, h, threshold, **kw):
+        return self.ctrl(h[:, 0].contiguous(), threshold, **kw)

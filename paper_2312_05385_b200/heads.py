@@ -177,15 +177,15 @@ def linear_tc(x, weight, bias=None, *, splits: int = 0):
 
 
 def pool_bf16(x):
-    """Global average pool of an NCHW fp32 map to a bf16 [B, C] GEMM operand."""
+    """Global average pool of an NCHW fp32/bf16 map to a bf16 [B, C] GEMM operand."""
     torch = nat.torch_cuda()
-    if x.dtype != torch.float32 or x.dim() != 4:
-        raise ParameterError("pool_bf16 takes an fp32 [B, C, H, W] tensor")
+    if x.dtype not in (torch.float32, torch.bfloat16) or x.dim() != 4:
+        raise ParameterError("pool_bf16 takes an fp32 or bf16 [B, C, H, W] tensor")
     x = x.contiguous()
     b, c, h, w = x.shape
     out = torch.empty((b, c), dtype=torch.bfloat16, device="cuda")
-    nat.check(nat.load_library().ee_pool_bf16(x.data_ptr(), b, c, h * w, out.data_ptr(),
-                                              nat.stream_handle(torch)))
+    nat.check(nat.load_library().ee_pool_bf16(x.data_ptr(), int(x.dtype == torch.bfloat16), b, c,
+                                              h * w, out.data_ptr(), nat.stream_handle(torch)))
     return out
 
 

@@ -76,10 +76,13 @@ def test_alive_mask_slots_and_scatter(cuda):
     slots = SlotTable.empty(b)
     probe = head(feat.cuda(), 0.0).err.cpu()
     thr = float(probe.quantile(0.4))
+    alive_before = alive.cpu().clone()
     res = head(feat.cuda(), thr, alive=alive, slot=slot, slots=slots)
-    _check(res, feat, w, None, "entropy", thr, alive=alive.cpu())
+    _check(res, feat, w, None, "entropy", thr, alive=alive_before)
     ex = res.exits.cpu().bool()
-    assert not ex[alive.cpu() == 0].any()  # dead rows never exit again
+    assert not ex[alive_before == 0].any()  # dead rows never exit again
+    # the alive mask is updated in place: exactly the exiting rows were cleared
+    assert torch.equal(alive.cpu().bool(), alive_before.bool() & ~ex)
     s = slot.cpu().long()
     site = slots.site.cpu()
     assert (site[s[ex]] == 7).all() and (site[s[~ex]] == -1).all()
