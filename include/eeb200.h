@@ -128,7 +128,9 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
  * [k] fp32 nullable, k <= 256), softmax confidence (conf 0: err = 1 - max p;
  * conf 1: err = H(p)/ln k), argmax label, and the reference exit rule
  * (double)err < threshold (strict, engine.py:207) for rows whose d_alive byte
- * is 1 (d_alive NULL = all alive); d_alive is updated in place (exiting rows
+ * is 1 (d_alive NULL = all alive). A non-NULL d_threshold (one device f64)
+ * overrides `threshold`, so a captured CUDA graph picks up retuned
+ * thresholds without re-capture. d_alive is updated in place (exiting rows
  * are cleared), so chaining ramps needs no extra launch. Outputs per row: d_err f32, d_label i32,
  * d_exit u8, optional d_logits f32 [b, k]. Then, in the same launch, the
  * surviving (alive, non-exiting) rows are compacted in ascending row order
@@ -138,7 +140,8 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
 int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, int64_t b,
                        int32_t c, int32_t hw, int32_t nhwc, const void* d_w, int32_t w_bf16,
                        const float* d_bias, int32_t k, int32_t conf, double threshold,
-                       uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
+                       const double* d_threshold, uint8_t* d_alive, const int32_t* d_slot,
+                       int32_t site, float* d_err,
                        int32_t* d_label, uint8_t* d_exit, float* d_logits, int32_t* d_keep,
                        int32_t* d_nkeep, int32_t* d_slot_label, float* d_slot_err,
                        int32_t* d_slot_site, void* stream);
@@ -146,7 +149,8 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
 /* Same epilogue from precomputed fp32 logits [b, k] (large heads whose FC runs
  * as a tensor-core GEMM). */
 int ee_exit_from_logits(ee_workspace* ws, const float* d_logits, int64_t b, int32_t k,
-                        int32_t conf, double threshold, uint8_t* d_alive,
+                        int32_t conf, double threshold, const double* d_threshold,
+                        uint8_t* d_alive,
                         const int32_t* d_slot, int32_t site, float* d_err, int32_t* d_label,
                         uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
                         float* d_slot_err, int32_t* d_slot_site, void* stream);

@@ -69,11 +69,11 @@ SIGNATURES = {
     "ee_exit_controller": (
         ctypes.c_int,
         [_vp, _vp, _c_i32, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _c_i32, _vp, _c_i32, _c_i32,
-         ctypes.c_double, _vp, _vp, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+         ctypes.c_double, _vp, _vp, _vp, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     ),
     "ee_exit_from_logits": (
         ctypes.c_int,
-        [_vp, _vp, _c_i64, _c_i32, _c_i32, ctypes.c_double, _vp, _vp, _c_i32, _vp, _vp, _vp,
+        [_vp, _vp, _c_i64, _c_i32, _c_i32, ctypes.c_double, _vp, _vp, _vp, _c_i32, _vp, _vp, _vp,
          _vp, _vp, _vp, _vp, _vp, _vp],
     ),
     "ee_compact_rows": (ctypes.c_int, [_vp, _c_i64, _vp, _vp, _c_i64, _vp, _vp]),

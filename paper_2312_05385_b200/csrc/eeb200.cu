@@ -534,6 +534,7 @@ int ws_reserve(ee_workspace* ws, size_t dev_bytes, size_t host_bytes) {
     EE_CUDA(cudaMalloc(&ws->d_buf, cap));
     ws->d_cap = cap;
   }
+  if (host_bytes == 0) return EE_OK;  // device scratch only: no host sync (capture-safe)
   if (ws->staged) EE_CUDA(cudaEventSynchronize(ws->staged));
   if (host_bytes > ws->h_cap) {
     if (ws->h_stage) EE_CUDA(cudaFreeHost(ws->h_stage));
@@ -1264,7 +1265,8 @@ static int exit_out(ee_workspace* ws, cudaStream_t st, int64_t b, const int32_t*
 int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, int64_t b,
                        int32_t c, int32_t hw, int32_t nhwc, const void* d_w, int32_t w_bf16,
                        const float* d_bias, int32_t k, int32_t conf, double threshold,
-                       uint8_t* d_alive, const int32_t* d_slot, int32_t site, float* d_err,
+                       const double* d_threshold, uint8_t* d_alive, const int32_t* d_slot,
+                       int32_t site, float* d_err,
                        int32_t* d_label, uint8_t* d_exit, float* d_logits, int32_t* d_keep,
                        int32_t* d_nkeep, int32_t* d_slot_label, float* d_slot_err,
                        int32_t* d_slot_site, void* stream) {
@@ -1290,7 +1292,7 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
       EE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     kern<<<(unsigned)b, exitc::THREADS, smem, st>>>(static_cast<const TF*>(d_feat), b, c, hw,   \
                                                      nhwc, static_cast<const TW*>(d_w), d_bias, k, \
-                                                     conf, threshold, d_alive, o);             \
+                                                     conf, threshold, d_threshold, d_alive, o); \
   } while (0)
   if (feat_bf16 && w_bf16)
     EE_EXITK(uint16_t, uint16_t);
@@ -1306,7 +1308,8 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
 }
 
 int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, int32_t k,
-                        int32_t conf, double threshold, uint8_t* d_alive,
+                        int32_t conf, double threshold, const double* d_threshold,
+                        uint8_t* d_alive,
                         const int32_t* d_slot, int32_t site, float* d_err, int32_t* d_label,
                         uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
                         float* d_slot_err, int32_t* d_slot_site, void* stream) {
@@ -1323,7 +1326,7 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
   ProfScope ps(ws, st, "k_exit_logits");
   const int rows_per = exitc::THREADS / 32;
   exitc::k_exit_logits<<<(unsigned)ceil_div(b, rows_per), exitc::THREADS, 0, st>>>(
-      d_logits_in, b, k, conf, threshold, d_alive, o);
+      d_logits_in, b, k, conf, threshold, d_threshold, d_alive, o);
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

@@ -154,7 +154,9 @@ template <typename TF, typename TW>
 __global__ void __launch_bounds__(THREADS)
     k_exit_fused(const TF* __restrict__ feat, int64_t B, int C, int HW, int nhwc,
                  const TW* __restrict__ W, const float* __restrict__ bias, int K, int conf,
-                 double threshold, uint8_t* __restrict__ alive_in, Out o) {
+                 double threshold, const double* __restrict__ d_threshold,
+                 uint8_t* __restrict__ alive_in, Out o) {
+  if (d_threshold) threshold = *d_threshold;
   extern __shared__ float sh[];  // pooled[C], logits[K]
   float* pooled = sh;
   float* logits = sh + C;
@@ -209,7 +211,9 @@ __global__ void __launch_bounds__(THREADS)
 // confidence + compare + compaction from precomputed logits [B, K] (fp32)
 __global__ void __launch_bounds__(THREADS)
     k_exit_logits(const float* __restrict__ logits_in, int64_t B, int K, int conf,
-                  double threshold, uint8_t* __restrict__ alive_in, Out o) {
+                  double threshold, const double* __restrict__ d_threshold,
+                  uint8_t* __restrict__ alive_in, Out o) {
+  if (d_threshold) threshold = *d_threshold;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * (THREADS / 32) + wid;  // one warp per row
   if (row < B) {

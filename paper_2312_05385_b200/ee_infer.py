@@ -78,7 +78,12 @@ class EEPipeline:
     def n_ramps(self) -> int:
         return len(self.ramp_order)
 
-    def run(self, x, thresholds: Sequence[float], *, mode: str = "feedback",
+    def capture(self, example, thresholds) -> "GraphRunner":
+        """Capture one feedback-mode batch into a CUDA graph (static shapes; the
+        thresholds live in device memory, so retuning needs no re-capture)."""
+        return GraphRunner(self, example, thresholds)
+
+    def run(self, x, thresholds, *, mode: str = "feedback",
             timed: bool = False) -> BatchResult:
         torch = nat.torch_cuda()
         if len(thresholds) != self.n_ramps:
@@ -88,6 +93,10 @@ class EEPipeline:
         b = x.shape[0]
         R = self.n_ramps
         dev = "cuda"
+        # thresholds: host floats, or a CUDA f64 [R] tensor read by the kernels at run time
+        dev_th = hasattr(thresholds, "data_ptr")
+        if dev_th:
+            thresholds = [thresholds[r : r + 1] for r in range(R)]
         slots = SlotTable.empty(b)
         alive = torch.ones(b, dtype=torch.uint8, device=dev)
         rows = torch.arange(b, dtype=torch.int32, device=dev)  # request slot of each live row
@@ -108,9 +117,14 @@ class EEPipeline:
                 head = self.ramps.get(j)
                 if head is None:
                     continue
-                res = head(h, float(thresholds[r]), alive=alive, slot=rows, slots=slots)
-                ramp_err[r].index_copy_(0, rows.long(), res.err)
-                ramp_label[r].index_copy_(0, rows.long(), res.label)
+                th = thresholds[r] if dev_th else float(thresholds[r])
+                if mode == "feedback":  # rows are the identity: write signals in place
+                    res = head(h, th, alive=alive, slot=rows, slots=slots,
+                               out_err=ramp_err[r], out_label=ramp_label[r])
+                else:
+                    res = head(h, th, alive=alive, slot=rows, slots=slots)
+                    ramp_err[r].index_copy_(0, rows.long(), res.err)
+                    ramp_label[r].index_copy_(0, rows.long(), res.label)
                 if timed:
                     ev = torch.cuda.Event(enable_timing=True)
                     ev.record()
@@ -137,6 +151,36 @@ class EEPipeline:
             out.release_ms = np.asarray(t)[np.clip(site, 0, R)]
             out.batch_ms = t[-1]
         return out
+
+
+class GraphRunner:
+    """A feedback-mode EEPipeline batch replayed as one CUDA graph: the whole
+    backbone + every ramp head / exit controller + scatter in one launch from
+    the host (the per-ramp Python and launch overhead disappears)."""
+
+    def __init__(self, pipe: EEPipeline, example, thresholds):
+        torch = nat.torch_cuda()
+        self.pipe = pipe
+        self.x = example.clone()
+        self.th = torch.tensor([float(t) for t in thresholds], dtype=torch.float64, device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):  # warm-up: grow workspaces, pick cuDNN algorithms
+                pipe.run(self.x, self.th)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = pipe.run(self.x, self.th)
+
+    def set_thresholds(self, thresholds):
+        self.th.copy_(self.th.new_tensor([float(t) for t in thresholds]))
+
+    def run(self, x=None) -> BatchResult:
+        if x is not None:
+            self.x.copy_(x)
+        self.graph.replay()
+        return self.out
 
 
 # ---------------------------------------------------------------- model builders
@@ -256,3 +300,15 @@ class _Token0Head:
 
     def __call__(self, h, threshold, **kw):
         return self.ctrl(h[:, 0].contiguous(), threshold, **kw)
+
+    @property
+    def weight(self):
+        return self.ctrl.weight
+
+    @property
+    def bias(self):
+        return self.ctrl.bias
+
+    @property
+    def conf(self):
+        return self.ctrl.conf

@@ -53,10 +53,10 @@ class SlotTable:
                    torch.full((slots,), -1, dtype=torch.int32, device="cuda"))
 
 
-def _outputs(torch, b, k, want_logits):
+def _outputs(torch, b, k, want_logits, out_err=None, out_label=None):
     dev = "cuda"
-    return (torch.empty(b, dtype=torch.float32, device=dev),
-            torch.empty(b, dtype=torch.int32, device=dev),
+    return (out_err if out_err is not None else torch.empty(b, dtype=torch.float32, device=dev),
+            out_label if out_label is not None else torch.empty(b, dtype=torch.int32, device=dev),
             torch.empty(b, dtype=torch.uint8, device=dev),
             torch.empty((b, k), dtype=torch.float32, device=dev) if want_logits else None,
             torch.empty(b, dtype=torch.int32, device=dev),
@@ -87,9 +87,12 @@ class ExitController:
         self.conf = conf
         self.site = site
 
-    def __call__(self, feat, threshold: float, *, alive=None, slot=None,
-                 slots: SlotTable | None = None, want_logits: bool = False) -> ExitResult:
-        """feat: [B, C, H, W] / [B, C] (NCHW) or channels-last memory format; fp32 or bf16."""
+    def __call__(self, feat, threshold, *, alive=None, slot=None,
+                 slots: SlotTable | None = None, want_logits: bool = False,
+                 out_err=None, out_label=None) -> ExitResult:
+        """feat: [B, C, H, W] / [B, C] (NCHW) or channels-last memory format; fp32 or bf16.
+        `threshold` is a float or a one-element CUDA f64 tensor (graph-capture friendly);
+        out_err / out_label let the caller supply the per-row output buffers."""
         torch = nat.torch_cuda()
         if feat.dtype not in (torch.float32, torch.bfloat16) or not feat.is_cuda:
             raise ParameterError("feat must be a CUDA fp32 or bf16 tensor")
@@ -108,11 +111,13 @@ class ExitController:
         if c != self.c:
             raise ParameterError(f"feat has {c} channels, head expects {self.c}")
         _check_aux(torch, b, alive, slot)
-        err, label, exits, logits, keep, n_keep = _outputs(torch, b, self.k, want_logits)
+        err, label, exits, logits, keep, n_keep = _outputs(torch, b, self.k, want_logits,
+                                                           out_err, out_label)
+        th_val, th_ptr = _threshold_args(torch, threshold)
         nat.check(nat.load_library().ee_exit_controller(
             nat.workspace(), feat.data_ptr(), int(feat.dtype == torch.bfloat16), b, c, hw, nhwc,
             self.weight.data_ptr(), int(self.weight.dtype == torch.bfloat16), nat.ptr(self.bias),
-            self.k, CONF[self.conf], float(threshold), nat.ptr(alive), nat.ptr(slot), self.site,
+            self.k, CONF[self.conf], th_val, th_ptr, nat.ptr(alive), nat.ptr(slot), self.site,
             err.data_ptr(), label.data_ptr(), exits.data_ptr(), nat.ptr(logits),
             keep.data_ptr(), n_keep.data_ptr(),
             nat.ptr(slots.label if slots else None), nat.ptr(slots.err if slots else None),
@@ -120,8 +125,18 @@ class ExitController:
         return ExitResult(err, label, exits, keep, n_keep, logits)
 
 
-def exit_from_logits(logits, threshold: float, *, conf: str = "maxprob", site: int = 0,
-                     alive=None, slot=None, slots: SlotTable | None = None) -> ExitResult:
+def _threshold_args(torch, threshold):
+    """(scalar, device pointer): a CUDA f64 tensor is read by the kernel at run time."""
+    if hasattr(threshold, "data_ptr"):
+        if threshold.dtype != torch.float64 or not threshold.is_cuda or threshold.numel() != 1:
+            raise ParameterError("device threshold must be a one-element CUDA float64 tensor")
+        return 0.0, threshold.data_ptr()
+    return float(threshold), None
+
+
+def exit_from_logits(logits, threshold, *, conf: str = "maxprob", site: int = 0,
+                     alive=None, slot=None, slots: SlotTable | None = None,
+                     out_err=None, out_label=None) -> ExitResult:
     """Confidence + compare + compaction + scatter over precomputed fp32 logits [B, K]."""
     torch = nat.torch_cuda()
     if logits.dtype != torch.float32 or logits.dim() != 2 or not logits.is_cuda:
@@ -129,9 +144,10 @@ def exit_from_logits(logits, threshold: float, *, conf: str = "maxprob", site: i
     logits = logits.contiguous()
     b, k = logits.shape
     _check_aux(torch, b, alive, slot)
-    err, label, exits, _, keep, n_keep = _outputs(torch, b, k, False)
+    err, label, exits, _, keep, n_keep = _outputs(torch, b, k, False, out_err, out_label)
+    th_val, th_ptr = _threshold_args(torch, threshold)
     nat.check(nat.load_library().ee_exit_from_logits(
-        nat.workspace(), logits.data_ptr(), b, k, CONF[conf], float(threshold), nat.ptr(alive),
+        nat.workspace(), logits.data_ptr(), b, k, CONF[conf], th_val, th_ptr, nat.ptr(alive),
         nat.ptr(slot), site, err.data_ptr(), label.data_ptr(), exits.data_ptr(),
         keep.data_ptr(), n_keep.data_ptr(),
         nat.ptr(slots.label if slots else None), nat.ptr(slots.err if slots else None),
@@ -200,13 +216,14 @@ class LargeRampHead:
         self.conf = conf
         self.site = site
 
-    def __call__(self, feat, threshold: float, *, alive=None, slot=None,
-                 slots: SlotTable | None = None, want_logits: bool = False) -> ExitResult:
+    def __call__(self, feat, threshold, *, alive=None, slot=None,
+                 slots: SlotTable | None = None, want_logits: bool = False,
+                 out_err=None, out_label=None) -> ExitResult:
         torch = nat.torch_cuda()
         x = pool_bf16(feat) if feat.dim() == 4 else feat.to(torch.bfloat16)
         logits = linear_tc(x, self.weight, self.bias)
         res = exit_from_logits(logits, threshold, conf=self.conf, site=self.site, alive=alive,
-                               slot=slot, slots=slots)
+                               slot=slot, slots=slots, out_err=out_err, out_label=out_label)
         if want_logits:
             res.logits = logits
         return res

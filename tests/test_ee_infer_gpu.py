@@ -95,3 +95,26 @@ def test_resnet50_config3_tensor_core_heads(cuda):
     th = _thresholds(pipe, torch.randn(32, 3, 224, 224, generator=g, device="cuda"))
     res = pipe.run(x, th)
     _check_rule(pipe, res, th)
+
+
+def test_cuda_graph_replay_matches_eager_and_retunes(cuda):
+    pipe, _ = ee_infer.resnet18_cifar()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(32, 3, 32, 32, generator=g, device="cuda")
+    th = _thresholds(pipe, torch.randn(256, 3, 32, 32, generator=g, device="cuda"))
+    runner = pipe.capture(x, th)
+    out = runner.run()
+    ref = pipe.run(x, th)
+    assert torch.equal(out.released_site, ref.released_site)
+    assert torch.equal(out.released_label, ref.released_label)
+    assert torch.equal(out.ramp_err, ref.ramp_err)
+    # retune without re-capture: thresholds are read from device memory
+    th2 = [t * 0.5 for t in th]
+    runner.set_thresholds(th2)
+    out2 = runner.run()
+    ref2 = pipe.run(x, th2)
+    assert torch.equal(out2.released_site, ref2.released_site)
+    x2 = torch.randn(32, 3, 32, 32, generator=g, device="cuda")
+    out3 = runner.run(x2)
+    ref3 = pipe.run(x2, th2)
+    assert torch.equal(out3.released_label, ref3.released_label)

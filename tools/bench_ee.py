@@ -1,0 +1,107 @@
+"""EE batch inference throughput and latency (BASELINE configs 1-3).
+
+For each config: thresholds from per-ramp err quantiles of a calibration
+batch, then timed batches (CUDA events) in feedback mode (Apparate:
+every input runs to completion, results released early) and compaction mode.
+Reports samples/s, p50 batch latency, p50 per-request release latency, exit
+rate, and the same model without ramps (vanilla) for context. bf16 autocast
+for the backbone; ramp heads take bf16 activations."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2312_05385_b200 import ee_infer
+
+
+def quantile_thresholds(pipe, x, q=(0.05, 0.10, 0.15, 0.20, 0.25, 0.30)):
+    probe = pipe.run(x, [0.0] * pipe.n_ramps)
+    err = probe.ramp_err.float().cpu().numpy()
+    qs = list(q) + [q[-1]] * max(0, pipe.n_ramps - len(q))
+    return [float(np.nanquantile(err[j], qs[j])) for j in range(pipe.n_ramps)]
+
+
+def bench(name, pipe, make_input, batch, iters, warmup=5):
+    th = quantile_thresholds(pipe, make_input(max(batch, 64)))
+    out = {"config": name, "batch": batch, "ramps": pipe.n_ramps}
+    for mode in ("feedback", "compact"):
+        x = make_input(batch)
+        for _ in range(warmup):
+            pipe.run(x, th, mode=mode)
+        lat, rel, exits = [], [], []
+        for _ in range(iters):
+            res = pipe.run(x, th, mode=mode, timed=True)
+            lat.append(res.batch_ms)
+            rel.extend(res.release_ms.tolist())
+            exits.append(float((res.released_site.cpu().numpy() < pipe.n_ramps).mean()))
+        out[mode] = {"samples_per_s": batch / (np.mean(lat) / 1e3),
+                     "p50_batch_ms": float(np.percentile(lat, 50)),
+                     "p50_request_release_ms": float(np.percentile(rel, 50)),
+                     "exit_rate": float(np.mean(exits))}
+    # feedback mode captured as one CUDA graph (thresholds in device memory)
+    x = make_input(batch)
+    runner = pipe.capture(x, th)
+    for _ in range(warmup):
+        runner.run()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(iters):
+        ev0.record()
+        runner.run()
+        ev1.record()
+        ev1.synchronize()
+        ts.append(ev0.elapsed_time(ev1))
+    ref = pipe.run(x, th)
+    same = bool(torch.equal(runner.out.released_site, ref.released_site)
+                and torch.equal(runner.out.released_label, ref.released_label))
+    out["feedback_graph"] = {"samples_per_s": batch / (np.mean(ts) / 1e3),
+                             "p50_batch_ms": float(np.percentile(ts, 50)),
+                             "matches_eager": same}
+    # vanilla: the same stages, no ramps
+    x = make_input(batch)
+    with torch.no_grad():
+        for _ in range(warmup):
+            h = x
+            for s in pipe.stages:
+                h = s(h)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(iters):
+            ev0.record()
+            h = x
+            for s in pipe.stages:
+                h = s(h)
+            ev1.record()
+            ev1.synchronize()
+            ts.append(ev0.elapsed_time(ev1))
+    out["vanilla"] = {"samples_per_s": batch / (np.mean(ts) / 1e3), "p50_batch_ms": float(np.percentile(ts, 50))}
+    return out
+
+
+def main():
+    torch.backends.cudnn.benchmark = True
+    which = sys.argv[1:] or ["1", "2", "3"]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    res = []
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        if "1" in which:
+            pipe, _ = ee_infer.resnet18_cifar()
+            res.append(bench("resnet18_cifar_6ramps", pipe,
+                             lambda b: torch.randn(b, 3, 32, 32, generator=g, device="cuda"), 32, 50))
+        if "2" in which:
+            pipe, _ = ee_infer.bert_base()
+            res.append(bench("bert_base_12ramps_seq128_entropy", pipe,
+                             lambda b: torch.randint(0, 30522, (b, 128), generator=g, device="cuda"), 64, 20))
+        if "3" in which:
+            pipe, _ = ee_infer.resnet50_imagenet()
+            res.append(bench("resnet50_imagenet_16ramps", pipe,
+                             lambda b: torch.randn(b, 3, 224, 224, generator=g, device="cuda"), 256, 10))
+    for r in res:
+        print(json.dumps(r))
+
+
+if __name__ == "__main__":
+    main()
