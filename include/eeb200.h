@@ -188,6 +188,26 @@ int ee_finalize_hist(ee_workspace* ws, const int64_t* d_hist, const int64_t* d_o
  * scan. Results are identical; 0 forces the generic path (tests, A/B). */
 int ee_workspace_set_special(ee_workspace* ws, int32_t on);
 
+/* Which diagonal-family kernel runs (default 2): 2 = k_diag2 (coalesced,
+ * conflict-free bin table, predicated updates, one launch) wherever it
+ * applies (even r <= 16, <= 127 distinct thresholds, 16-byte aligned scores),
+ * else k_diag; 1 = k_diag only. Results are identical (A/B, tests). Calls on
+ * one workspace must be stream-ordered: k_diag2 keeps a global accumulator in
+ * the workspace that every launch leaves zeroed for the next. */
+int ee_workspace_set_diag_version(ee_workspace* ws, int32_t version);
+
+/* Benchmark aid: overwrites d_buf (bytes, > L2 size to evict it) with a
+ * streaming-store kernel that uses the same max-shared carveout as the sweep
+ * kernels, so an L2 flush between timed sweeps does not also reconfigure the
+ * SMs' L1/shared split. */
+int ee_l2_flush(void* d_buf, int64_t bytes, void* stream);
+
+/* Profiling aid: while d_trace (device u64 [grid * 6], zeroed by the caller)
+ * is set, every k_diag2 CTA records %globaltimer stamps (start, prologue done,
+ * last warp out of the sweep loop, merged into the accumulator, and, for the
+ * last CTA, finalised). NULL turns it off. */
+int ee_diag_trace(ee_workspace* ws, uint64_t* d_trace);
+
 /* Per-launch timing: while enabled, every kernel launched through `ws` is
  * bracketed by CUDA events on its stream. ee_profile_read synchronises, writes
  * {"kernel": {"launches": L, "ms": T}, ...} (JSON) into buf and resets. */

@@ -60,6 +60,9 @@ SIGNATURES = {
     ),
     "ee_profile_enable": (ctypes.c_int, [_vp, _c_i32]),
     "ee_workspace_set_special": (ctypes.c_int, [_vp, _c_i32]),
+    "ee_workspace_set_diag_version": (ctypes.c_int, [_vp, _c_i32]),
+    "ee_diag_trace": (ctypes.c_int, [_vp, _vp]),
+    "ee_l2_flush": (ctypes.c_int, [_vp, _c_i64, _vp]),
     "ee_profile_read": (ctypes.c_int, [_vp, ctypes.c_char_p, _c_i64]),
     "ee_tune": (
         ctypes.c_int,
@@ -154,6 +157,11 @@ def workspace() -> ctypes.c_void_p:
     return ws.handle
 
 
+def set_diag_version(version: int = 2) -> None:
+    """2 = k_diag2 where it applies (default), 1 = the first diagonal kernel only."""
+    check(load_library().ee_workspace_set_diag_version(workspace(), int(version)))
+
+
 def set_special(on: bool = True) -> None:
     """Enable/disable family-specialised sweeps on this thread's workspace."""
     check(load_library().ee_workspace_set_special(workspace(), int(on)))
@@ -170,6 +178,14 @@ def profile_read() -> dict:
     buf = ctypes.create_string_buffer(1 << 16)
     check(load_library().ee_profile_read(workspace(), buf, len(buf)))
     return json.loads(buf.value.decode())
+
+
+def l2_flush(buf) -> None:
+    """Evict L2 by streaming over `buf` (a CUDA tensor larger than L2), same carveout as the sweeps."""
+    import torch
+
+    check(load_library().ee_l2_flush(buf.data_ptr(), buf.numel() * buf.element_size(),
+                                     stream_handle(torch)))
 
 
 def stream_handle(torch) -> int:

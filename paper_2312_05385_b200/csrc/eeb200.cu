@@ -24,6 +24,7 @@
 #include <limits>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <unordered_set>
 #include <vector>
 
@@ -464,10 +465,21 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 
 }  // namespace
 #include "sweep_diag.cuh"
+#include "sweep_diag2.cuh"
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
 #include "gemm_tc.cuh"
 namespace {
+
+// L2 eviction for benchmarks: streams a buffer larger than L2 with the same
+// max-shared carveout as the sweep kernels, so flushing between timed sweeps
+// does not also force an L1/shared reconfiguration of every SM.
+__global__ void __launch_bounds__(1024) k_l2_flush(uint4* buf, int64_t n16) {
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x)
+    __stcs(buf + i, z);
+}
 
 __global__ void k_fill_nan(double* a, double* b, int64_t C) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -493,6 +505,12 @@ struct ee_workspace {
   // this workspace launches, on the launching stream
   bool profiling = false;
   bool allow_special = true;  // family-specialised sweeps (diagonal); off = generic SWAR path
+  int diag_version = 2;       // 2 = k_diag2 where it applies, 1 = k_diag only (A/B, tests)
+  // k_diag2 global accumulator: zero between launches (each launch leaves it
+  // zeroed), so calls on one workspace must be stream-ordered
+  long long* d_diag_acc = nullptr;
+  bool diag_acc_dirty = true;
+  unsigned long long* d_diag_trace = nullptr;  // set by ee_diag_trace (profiling)
   struct Mark {
     const char* name;
     cudaEvent_t a, b;
@@ -664,6 +682,7 @@ int ee_workspace_destroy(ee_workspace* ws) {
   if (!ws) return EE_OK;
   if (ws->staged) cudaEventSynchronize(ws->staged);
   if (ws->d_buf) cudaFree(ws->d_buf);
+  if (ws->d_diag_acc) cudaFree(ws->d_diag_acc);
   if (ws->h_stage) cudaFreeHost(ws->h_stage);
   if (ws->staged) cudaEventDestroy(ws->staged);
   delete ws;
@@ -946,15 +965,142 @@ static int eval_diag(ee_workspace* ws, const double* d_scores, const uint32_t* d
   return EE_OK;
 }
 
+// k_diag2 (sweep_diag2.cuh). Returns 1 when the inputs fall outside its
+// envelope (odd or > 16 ramps, misaligned scores, > 127 distinct thresholds,
+// no single-threshold bin grid) so the caller runs k_diag instead.
+}  // extern "C"
+template <int R>
+static cudaError_t launch_diag2(const diag2::Params& p, int64_t n, int upd, cudaStream_t st,
+                                ee_workspace* ws) {
+  auto k = upd == 1 ? diag2::k_diag2<R, 1> : diag2::k_diag2<R, 0>;
+  constexpr int smem = diag2::smem_bytes<R>();
+  static bool attr_set[2] = {false, false};  // once per instantiation (a driver call)
+  if (!attr_set[upd]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[upd] = true;
+  }
+  const int64_t nchunks = ceil_div(n, 32);
+  const unsigned grid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), ceil_div(nchunks, diag2::WARPS)));
+  ProfScope ps(ws, st, "k_diag2");  // events bracket the launch itself
+  k<<<grid, diag2::THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+extern "C" {
+
+static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                      int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
+                      const std::vector<double>& u, int64_t* d_hist, int64_t* d_ok, double* d_acc,
+                      double* d_sav, cudaStream_t st) {
+  const int m = (int)u.size();
+  if (ws->diag_version < 2 || r < 2 || r > diag2::RMAX || (r & 1) || m < 1 || m > diag2::MAX_M)
+    return 1;
+  if ((reinterpret_cast<uintptr_t>(d_scores) & 15) != 0) return 1;
+  if (u.back() == std::numeric_limits<double>::infinity()) return 1;  // bin 255 stays threshold-free
+  // grid over the finite thresholds: smallest -> bin 2, largest -> bin 253
+  double f0 = 0.0, f1 = 0.0;
+  bool any = false;
+  for (double x : u)
+    if (std::isfinite(x)) {
+      if (!any) f0 = x;
+      f1 = x;
+      any = true;
+    }
+  diag2::Params p{};
+  double a = 1e-300;
+  if (any && f1 > f0) a = 251.0 / (f1 - f0);
+  const double c0 = any ? 2.0 - a * f0 : 2.0;
+  if (!std::isfinite(a) || !(a > 0.0) || !std::isfinite(c0)) return 1;
+  p.a = a;
+  p.c0 = c0;
+  std::vector<unsigned> bu((size_t)m);
+  for (int i = 0; i < m; ++i) {  // one threshold per bin, none in bin 255
+    bu[i] = diag2::bin_of(u[i], p.a, p.c0);
+    if (bu[i] == 255u) return 1;
+    if (i > 0 && bu[i] <= bu[i - 1]) return 1;
+  }
+  // bin table: lo = #{thresholds in lower bins} (all < x), and the byte offset
+  // of the bin's own threshold in u[] (or of the NaN sentinel SENT)
+  for (int k = 0, lo = 0; k < diag2::NB; ++k) {
+    while (lo < m && bu[lo] < (unsigned)k) ++lo;
+    const int cmp = (lo < m && bu[lo] == (unsigned)k) ? lo : diag2::SENT;
+    p.tab[k] = (uint32_t)lo | ((uint32_t)(cmp * 8) << 16);
+  }
+  if (!ws->d_diag_acc) {
+    EE_CUDA(cudaMalloc(&ws->d_diag_acc, (size_t)diag2::ACC_WORDS * 8));
+    ws->diag_acc_dirty = true;
+  }
+  if (ws->diag_acc_dirty) {
+    EE_CUDA(cudaMemsetAsync(ws->d_diag_acc, 0, (size_t)diag2::ACC_WORDS * 8, st));
+    ws->diag_acc_dirty = false;
+  }
+  p.s = d_scores;
+  p.bits = d_bits;
+  p.n = n;
+  p.gD = ws->d_diag_acc;
+  p.done = reinterpret_cast<unsigned*>(ws->d_diag_acc + diag2::CORR_IDX + 1);
+  p.hist = d_hist;
+  p.ok = d_ok;
+  p.acc = d_acc;
+  p.sav = d_sav;
+  p.C = C;
+  p.m = m;
+  p.trace = ws->d_diag_trace;
+  p.vanilla = vanilla;
+  for (int j = 0; j <= r; ++j) p.serve[j] = h_serve[j];
+  for (int i = 0; i < m; ++i) p.u[i] = u[i];
+  std::vector<unsigned char> pos((size_t)C);
+  for (int64_t c = 0; c < C; ++c) {
+    const double v = h_th[c * r];
+    pos[c] = v == v ? (unsigned char)(std::lower_bound(u.begin(), u.end(), canon(v)) - u.begin())
+                    : (unsigned char)255;
+  }
+  if (C <= diag2::MAX_POS) {
+    std::memcpy(p.pos, pos.data(), (size_t)C);
+  } else {
+    const size_t need = align_up((size_t)C, 256);
+    int rc = ws_reserve(ws, need, need);
+    if (rc) return rc;
+    std::memcpy(ws->h_stage, pos.data(), (size_t)C);
+    EE_CUDA(cudaMemcpyAsync(ws->d_buf, ws->h_stage, need, cudaMemcpyHostToDevice, st));
+    EE_CUDA(cudaEventRecord(ws->staged, st));
+    p.pos_dev = static_cast<const unsigned char*>(ws->d_buf);
+  }
+  cudaError_t e;
+  const int upd = ws->diag_version == 3 ? 0 : 1;
+  {
+    switch (r) {
+      case 2: e = launch_diag2<2>(p, n, upd, st, ws); break;
+      case 4: e = launch_diag2<4>(p, n, upd, st, ws); break;
+      case 6: e = launch_diag2<6>(p, n, upd, st, ws); break;
+      case 8: e = launch_diag2<8>(p, n, upd, st, ws); break;
+      case 10: e = launch_diag2<10>(p, n, upd, st, ws); break;
+      case 12: e = launch_diag2<12>(p, n, upd, st, ws); break;
+      case 14: e = launch_diag2<14>(p, n, upd, st, ws); break;
+      default: e = launch_diag2<16>(p, n, upd, st, ws); break;
+    }
+  }
+  if (e != cudaSuccess) {
+    ws->diag_acc_dirty = true;
+    return fail(EE_ERR_CUDA, std::string("k_diag2: ") + cudaGetErrorString(e));
+  }
+  return EE_OK;
+}
+
 static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
                      int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
                      int64_t* d_hist, int64_t* d_ok, double* d_acc, double* d_sav,
                      cudaStream_t st) {
   {
     std::vector<double> u;
-    if (ws->allow_special && diagonal_rows(h_th, C, r, u))
+    if (ws->allow_special && diagonal_rows(h_th, C, r, u)) {
+      const int rc = eval_diag2(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, C, u, d_hist,
+                                d_ok, d_acc, d_sav, st);
+      if (rc != 1) return rc;
       return eval_diag(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, C, u, d_hist, d_ok,
                        d_acc, d_sav, st);
+    }
   }
   const int rw = std::max(1, (r + 3) / 4);
   const int rp = 4 * rw;
@@ -1144,6 +1290,35 @@ int ee_workspace_set_special(ee_workspace* ws, int32_t on) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
   std::lock_guard<std::mutex> lock(ws->mu);
   ws->allow_special = on != 0;
+  return EE_OK;
+}
+
+int ee_workspace_set_diag_version(ee_workspace* ws, int32_t version) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (version < 1 || version > 3) return fail(EE_ERR_ARG, "diagonal kernel version must be 1, 2 or 3");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  ws->diag_version = version;
+  return EE_OK;
+}
+
+int ee_l2_flush(void* d_buf, int64_t bytes, void* stream) {
+  if (!d_buf || bytes < 16) return fail(EE_ERR_ARG, "bad flush buffer");
+  static bool attr = false;
+  if (!attr) {
+    EE_CUDA(cudaFuncSetAttribute(k_l2_flush, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    attr = true;
+  }
+  k_l2_flush<<<(unsigned)sm_count() * 2, 1024, 0, (cudaStream_t)stream>>>(
+      static_cast<uint4*>(d_buf), bytes / 16);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_diag_trace(ee_workspace* ws, uint64_t* d_trace) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  ws->d_diag_trace = reinterpret_cast<unsigned long long*>(d_trace);
   return EE_OK;
 }
 

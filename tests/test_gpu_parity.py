@@ -301,3 +301,44 @@ def test_diagonal_family_path_matches_generic(cuda, r, clustered):
     assert np.array_equal(acc_d, acc_g) and np.array_equal(sav_d, sav_g)
     hist_o, ok_o = O.eval_hist(scores, cext, th)
     assert np.array_equal(hist_d, hist_o) and np.array_equal(ok_d, ok_o)
+
+
+@pytest.mark.parametrize("r,n,m,c_rep", [(2, 1, 5, 1), (4, 31, 17, 1), (6, 33, 64, 1),
+                                         (10, 4099, 127, 1), (12, 70001, 64, 1), (12, 2500, 40, 20),
+                                         (14, 9000, 100, 1), (16, 12345, 126, 2)])
+def test_diag2_matches_diag1_and_oracle(cuda, r, n, m, c_rep):
+    """k_diag2 (coalesced, replicated bin table, predicated updates, one launch)
+    against k_diag and the C oracle: ragged tails (n % 32 != 0), up to 127
+    distinct thresholds incl. +-inf and +-0, NaN rows and NaN scores, rows whose
+    no-exit bit is 0, and more than 512 candidates (device position map)."""
+    from paper_2312_05385_b200 import _native
+
+    rng = np.random.default_rng(9100 + r + n)
+    scores, cext, serve, vanilla, _ = random_window(rng, n, r, 1, nan_frac=0.01)
+    scores[rng.random((n, r)) < 0.01] = np.inf
+    scores[rng.random((n, r)) < 0.01] = -0.0
+    cext[:, r] = (rng.random(n) < 0.8).astype(np.float64)  # some samples with bit r = 0
+    extra = np.array([0.0, np.inf, -np.inf, 1.0])
+    vals = np.unique(np.concatenate([np.round(rng.random(4 * m) * 997) / 997, extra]))[:m]
+    rows = np.concatenate([vals, [np.nan]])
+    rows = np.repeat(rows, c_rep)
+    rng.shuffle(rows)
+    th = np.repeat(rows[:, None], r, axis=1)
+    arrays = WindowArrays(scores, cext.astype(np.uint8))
+    prof = make_chain(r + 1)
+    ev = WindowEvaluator.from_arrays(arrays, find_feasible_sites(prof)[:r], prof, mode="hist")
+    hist2, ok2 = ev.histograms(th)
+    acc2, sav2 = ev.evaluate_many(th)
+    _native.set_diag_version(1)
+    try:
+        hist1, ok1 = ev.histograms(th)
+        acc1, sav1 = ev.evaluate_many(th)
+    finally:
+        _native.set_diag_version(2)
+    assert np.array_equal(hist2, hist1) and np.array_equal(ok2, ok1)
+    assert np.array_equal(acc2, acc1) and np.array_equal(sav2, sav1)
+    hist_o, ok_o = O.eval_hist(scores, cext, th)
+    assert np.array_equal(hist2, hist_o) and np.array_equal(ok2, ok_o)
+    # repeated calls on the same workspace: the accumulator is left zeroed
+    hist3, ok3 = ev.histograms(th)
+    assert np.array_equal(hist3, hist2) and np.array_equal(ok3, ok2)

@@ -22,6 +22,9 @@ elif family == "axis":
 else:
     th = (np.arange(64) / 63.0)[np.random.default_rng(1).integers(0, 64, size=(64, r))]
 sw = ShardedSweep(arrays, sites, prof)
+if os.environ.get("DIAG_VERSION"):
+    from paper_2312_05385_b200 import _native
+    _native.set_diag_version(int(os.environ["DIAG_VERSION"]))
 for _ in range(reps):
     sw.evaluate_many(th, to_host=False)
 torch.cuda.synchronize()
