@@ -372,12 +372,16 @@ def e2e_run(args, arrays, prof, sites, th, rank, world):
         import torch.distributed as dist
 
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    h2d = scores.nbytes + cext.nbytes + th.nbytes + serve.nbytes
-    d2h = 16 * th.shape[0] + 4
+    # bytes that cross PCIe: the f64 scores, correct_ext packed on the host to one
+    # u32 per sample (ee_eval_thresholds_host), thresholds/serve (launch parameters)
+    h2d = scores.nbytes + 4 * scores.shape[0] + th.nbytes + serve.nbytes
+    d2h = 16 * th.shape[0]
     return {"value": th.shape[0] / float(t.item()), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": float(t.item()) * 1e3,
-            "path": "paper_2312_05385_b200.kernels.eval_thresholds(pinned numpy) mode=hist"}
+            "path": "paper_2312_05385_b200.kernels.eval_thresholds(pinned numpy) mode=hist -> "
+                    "ee_eval_thresholds_host: correct_ext packed on all host cores while the "
+                    "scores stream over PCIe"}
 
 
 def cpu_baseline(args, arrays, prof, sites, th, acc_gpu, sav_gpu):

@@ -96,6 +96,24 @@ int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t*
                        const double* h_th, int64_t c, int32_t mode, int64_t* d_hist,
                        int64_t* d_ok, double* d_acc, double* d_sav, void* stream);
 
+/* The same evaluation from HOST buffers (the reference's own calling
+ * convention: numpy arrays in, numpy arrays out, engine.py:165-170):
+ * h_scores f64 [n, r], h_correct_ext f64 [n, r+1] (0.0/1.0, else
+ * EE_ERR_NOT_BINARY), h_serve f64 [r+1], h_th f64 [c, r] -> h_acc, h_sav f64
+ * [c]. correct_ext is packed to 4-byte bit rows on n_threads host threads
+ * (<= 0: all cores) while the scores stream to the device, so 8r + 4 bytes
+ * per sample cross PCIe instead of 16r + 8. Synchronous. */
+int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
+                            int64_t n, int32_t r, const double* h_serve, double vanilla,
+                            const double* h_th, int64_t c, int32_t mode, double* h_acc,
+                            double* h_sav, int32_t n_threads, void* stream);
+
+/* Host-side packing of correct_ext f64 [n, r1] into u32 bit rows (bit j =
+ * column j) on n_threads threads (<= 0: all cores); EE_ERR_NOT_BINARY if any
+ * entry is not exactly 0.0 or 1.0. */
+int ee_pack_correct_host(const double* h_correct_ext, int64_t n, int32_t r1, uint32_t* h_bits,
+                         int32_t n_threads);
+
 /* Scores the full lattice vals^r in lexicographic (meshgrid 'ij') row order
  * without materialising it — the candidate set of tuner.grid_oracle
  * (pkg/src/eesim/tuner.py:213-223) — and returns acc/sav per lattice point

@@ -24,6 +24,7 @@
 #include <limits>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <unordered_set>
 #include <vector>
@@ -508,6 +509,12 @@ struct ee_workspace {
   int diag_version = 2;       // 2 = k_diag2 where it applies, 1 = k_diag only (A/B, tests)
   // k_diag2 global accumulator: zero between launches (each launch leaves it
   // zeroed), so calls on one workspace must be stream-ordered
+  // inputs staged by ee_eval_thresholds_host: device scores/bits/outputs and
+  // the pinned host bit rows packed on the CPU
+  void* d_in = nullptr;
+  size_t d_in_cap = 0;
+  uint32_t* h_bits = nullptr;
+  size_t h_bits_cap = 0;
   long long* d_diag_acc = nullptr;
   bool diag_acc_dirty = true;
   unsigned long long* d_diag_trace = nullptr;  // set by ee_diag_trace (profiling)
@@ -683,6 +690,8 @@ int ee_workspace_destroy(ee_workspace* ws) {
   if (ws->staged) cudaEventSynchronize(ws->staged);
   if (ws->d_buf) cudaFree(ws->d_buf);
   if (ws->d_diag_acc) cudaFree(ws->d_diag_acc);
+  if (ws->d_in) cudaFree(ws->d_in);
+  if (ws->h_bits) cudaFreeHost(ws->h_bits);
   if (ws->h_stage) cudaFreeHost(ws->h_stage);
   if (ws->staged) cudaEventDestroy(ws->staged);
   delete ws;
@@ -1223,23 +1232,11 @@ static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d
   return EE_OK;
 }
 
-int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits,
-                       int64_t n, int32_t r, const double* h_serve, double vanilla,
-                       const double* h_th, int64_t c, int32_t mode, int64_t* d_hist,
-                       int64_t* d_ok, double* d_acc, double* d_sav, void* stream) {
-  if (!ws) return fail(EE_ERR_ARG, "null workspace");
-  if (n < 0 || r < 0 || c < 0) return fail(EE_ERR_ARG, "negative shape");
-  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
-  if (c == 0) return EE_OK;
-  if (!h_serve) return fail(EE_ERR_ARG, "null serve table");
-  if (!d_acc != !d_sav) return fail(EE_ERR_ARG, "acc and sav must both be given or both be null");
-  if (!d_acc && (mode != EE_MODE_HIST || !d_hist || !d_ok))
-    return fail(EE_ERR_ARG, "counts-only evaluation needs HIST mode and d_hist/d_ok");
-  if (n > 0 && (!d_scores && r > 0)) return fail(EE_ERR_ARG, "null scores");
-  if (n > 0 && !d_bits) return fail(EE_ERR_ARG, "null correctness bits");
-  if (r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
-  std::lock_guard<std::mutex> lock(ws->mu);
-  auto st = (cudaStream_t)stream;
+// Mode dispatch (caller holds ws->mu and has validated the arguments).
+static int eval_dispatch(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                         int32_t r, const double* h_serve, double vanilla, const double* h_th,
+                         int64_t c, int32_t mode, int64_t* d_hist, int64_t* d_ok, double* d_acc,
+                         double* d_sav, cudaStream_t st) {
   if (n == 0) {
     k_fill_nan<<<(unsigned)ceil_div(c, 256), 256, 0, st>>>(d_acc, d_sav, c);
     EE_LAUNCH_CHECK();
@@ -1257,6 +1254,153 @@ int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t*
     return eval_hist(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, d_hist, d_ok, d_acc,
                      d_sav, st);
   return fail(EE_ERR_ARG, "unknown mode");
+}
+
+int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits,
+                       int64_t n, int32_t r, const double* h_serve, double vanilla,
+                       const double* h_th, int64_t c, int32_t mode, int64_t* d_hist,
+                       int64_t* d_ok, double* d_acc, double* d_sav, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (n < 0 || r < 0 || c < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (c == 0) return EE_OK;
+  if (!h_serve) return fail(EE_ERR_ARG, "null serve table");
+  if (!d_acc != !d_sav) return fail(EE_ERR_ARG, "acc and sav must both be given or both be null");
+  if (!d_acc && (mode != EE_MODE_HIST || !d_hist || !d_ok))
+    return fail(EE_ERR_ARG, "counts-only evaluation needs HIST mode and d_hist/d_ok");
+  if (n > 0 && (!d_scores && r > 0)) return fail(EE_ERR_ARG, "null scores");
+  if (n > 0 && !d_bits) return fail(EE_ERR_ARG, "null correctness bits");
+  if (r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  return eval_dispatch(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, mode, d_hist, d_ok,
+                       d_acc, d_sav, (cudaStream_t)stream);
+}
+
+// correct_ext f64 [n, r1] -> bit rows on the host, rows [i0, i1); *bad |= any
+// non-0/1 entry. Works on the IEEE bit patterns (1.0 = 0x3ff0..., +-0.0 has no
+// bits but the sign), fully unrolled per column count so the compiler keeps a
+// row in registers: ~3 integer ops per entry.
+}  // extern "C"
+template <int R1>
+static void pack_rows_fixed(const double* c, int64_t i0, int64_t i1, uint32_t* bits, int* bad) {
+  const uint64_t* u = reinterpret_cast<const uint64_t*>(c);
+  uint64_t b = 0;
+  for (int64_t i = i0; i < i1; ++i) {
+    const uint64_t* row = u + i * R1;
+    uint32_t w = 0;
+#pragma GCC unroll 32
+    for (int j = 0; j < R1; ++j) {
+      const uint64_t x = row[j];
+      const uint64_t one = x == 0x3ff0000000000000ull;
+      w |= (uint32_t)one << j;
+      b |= (x << 1) & (one - 1);  // nonzero unless the entry is +-0.0 or 1.0
+    }
+    bits[i] = w;
+  }
+  if (b) *bad = 1;
+}
+extern "C" {
+
+static void pack_rows_host(const double* c, int64_t i0, int64_t i1, int r1, uint32_t* bits,
+                           int* bad) {
+  switch (r1) {
+#define EE_PACK_CASE(K) \
+  case K:               \
+    return pack_rows_fixed<K>(c, i0, i1, bits, bad);
+    EE_PACK_CASE(1) EE_PACK_CASE(2) EE_PACK_CASE(3) EE_PACK_CASE(4) EE_PACK_CASE(5)
+    EE_PACK_CASE(6) EE_PACK_CASE(7) EE_PACK_CASE(8) EE_PACK_CASE(9) EE_PACK_CASE(10)
+    EE_PACK_CASE(11) EE_PACK_CASE(12) EE_PACK_CASE(13) EE_PACK_CASE(14) EE_PACK_CASE(15)
+    EE_PACK_CASE(16) EE_PACK_CASE(17) EE_PACK_CASE(18) EE_PACK_CASE(19) EE_PACK_CASE(20)
+    EE_PACK_CASE(21) EE_PACK_CASE(22) EE_PACK_CASE(23) EE_PACK_CASE(24) EE_PACK_CASE(25)
+    EE_PACK_CASE(26) EE_PACK_CASE(27) EE_PACK_CASE(28) EE_PACK_CASE(29) EE_PACK_CASE(30)
+    EE_PACK_CASE(31) EE_PACK_CASE(32)
+#undef EE_PACK_CASE
+    default:
+      *bad = 1;
+  }
+}
+
+int ee_pack_correct_host(const double* h_correct_ext, int64_t n, int32_t r1, uint32_t* h_bits,
+                         int32_t n_threads) {
+  if (n < 0 || r1 < 1) return fail(EE_ERR_ARG, "bad shape");
+  if (r1 > EE_MAX_RAMPS + 1) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (n == 0) return EE_OK;
+  if (!h_correct_ext || !h_bits) return fail(EE_ERR_ARG, "null pointer");
+  int t = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  t = (int)std::min<int64_t>(t, std::max<int64_t>(1, n / 4096));
+  std::vector<int> bad((size_t)t, 0);
+  std::vector<std::thread> pool;
+  for (int k = 1; k < t; ++k)
+    pool.emplace_back(pack_rows_host, h_correct_ext, n * k / t, n * (k + 1) / t, (int)r1, h_bits,
+                      &bad[k]);
+  pack_rows_host(h_correct_ext, 0, n / t, r1, h_bits, &bad[0]);
+  for (auto& th : pool) th.join();
+  for (int b : bad)
+    if (b) return fail(EE_ERR_NOT_BINARY, "correct_ext must contain only 0.0 and 1.0");
+  return EE_OK;
+}
+
+int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
+                            int64_t n, int32_t r, const double* h_serve, double vanilla,
+                            const double* h_th, int64_t c, int32_t mode, double* h_acc,
+                            double* h_sav, int32_t n_threads, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (n < 0 || r < 0 || c < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (c == 0) return EE_OK;
+  if (!h_serve || !h_acc || !h_sav) return fail(EE_ERR_ARG, "null pointer");
+  if (n > 0 && ((!h_scores && r > 0) || !h_correct_ext)) return fail(EE_ERR_ARG, "null inputs");
+  if (r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  const size_t s_b = align_up((size_t)n * r * 8, 256), b_b = align_up((size_t)n * 4, 256);
+  const size_t o_b = align_up((size_t)c * 8, 256);
+  const size_t need = s_b + b_b + 2 * o_b;
+  if (need > ws->d_in_cap) {
+    if (ws->d_in) EE_CUDA(cudaFree(ws->d_in));
+    ws->d_in = nullptr;
+    EE_CUDA(cudaMalloc(&ws->d_in, need));
+    ws->d_in_cap = need;
+  }
+  if ((size_t)n > ws->h_bits_cap) {
+    if (ws->h_bits) EE_CUDA(cudaFreeHost(ws->h_bits));
+    ws->h_bits = nullptr;
+    EE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ws->h_bits), std::max<size_t>(n, 1) * 4,
+                          cudaHostAllocDefault));
+    ws->h_bits_cap = (size_t)n;
+  }
+  auto* base = static_cast<unsigned char*>(ws->d_in);
+  double* d_scores = reinterpret_cast<double*>(base);
+  uint32_t* d_bits = reinterpret_cast<uint32_t*>(base + s_b);
+  double* d_acc = reinterpret_cast<double*>(base + s_b + b_b);
+  double* d_sav = reinterpret_cast<double*>(base + s_b + b_b + o_b);
+  // the CPU packs correct_ext into 4-byte bit rows (25x fewer bytes over PCIe)
+  // on worker threads while the scores stream to the device
+  int prc = EE_OK;
+  std::string perr;
+  std::thread packer([&] {
+    prc = ee_pack_correct_host(h_correct_ext, n, r + 1, ws->h_bits, n_threads);
+    if (prc) perr = g_err;  // thread-local
+  });
+  cudaError_t ce = cudaSuccess;
+  if (n > 0 && r > 0) ce = cudaMemcpyAsync(d_scores, h_scores, (size_t)n * r * 8, cudaMemcpyHostToDevice, st);
+  packer.join();
+  if (prc) {
+    cudaStreamSynchronize(st);  // the caller's buffers stay in use until the copy is done
+    return fail(prc, perr);
+  }
+  if (ce != cudaSuccess) return fail(EE_ERR_CUDA, std::string("scores H2D: ") + cudaGetErrorString(ce));
+  if (n > 0) EE_CUDA(cudaMemcpyAsync(d_bits, ws->h_bits, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+  int rc = eval_dispatch(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, mode, nullptr,
+                         nullptr, d_acc, d_sav, st);
+  if (rc) {
+    cudaStreamSynchronize(st);
+    return rc;
+  }
+  EE_CUDA(cudaMemcpyAsync(h_acc, d_acc, (size_t)c * 8, cudaMemcpyDeviceToHost, st));
+  EE_CUDA(cudaMemcpyAsync(h_sav, d_sav, (size_t)c * 8, cudaMemcpyDeviceToHost, st));
+  EE_CUDA(cudaStreamSynchronize(st));
+  return EE_OK;
 }
 
 int ee_finalize_hist(ee_workspace* ws, const int64_t* d_hist, const int64_t* d_ok, int64_t c,

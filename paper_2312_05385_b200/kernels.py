@@ -92,6 +92,18 @@ def _to_device(torch, x):
     return t.to("cuda", non_blocking=t.is_pinned())
 
 
+def pack_correct_host(correct_ext, n_threads: int = 0) -> np.ndarray:
+    """correct_ext f64 (N, R+1) -> u32 bit rows, packed on the host CPU cores
+    (ValueError if an entry is not exactly 0.0 or 1.0)."""
+    correct_ext = _check_view(correct_ext, 2, "correct_ext")
+    n, r1 = correct_ext.shape
+    bits = np.empty(n, dtype=np.uint32)
+    nat.check(nat.load_library().ee_pack_correct_host(
+        correct_ext.ctypes.data if n else None, n, r1, bits.ctypes.data if n else None,
+        int(n_threads)))
+    return bits
+
+
 def pack_correct(correct_ext, torch=None):
     """correct_ext f64 (N, R+1) -> (u32 bit rows on device, device flag)."""
     torch = torch or nat.torch_cuda()
@@ -157,6 +169,17 @@ def eval_thresholds(scores, correct_ext, serve, vanilla, thresholds, *, mode: st
     code = _mode_code(mode)
     torch = nat.torch_cuda()
     lib = nat.load_library()
+    if not _is_cuda_tensor(scores) and not _is_cuda_tensor(correct_ext):
+        # host buffers (the reference's calling convention): one native call packs
+        # correct_ext on the CPU cores while the scores stream to the device
+        acc = np.empty(c)
+        sav = np.empty(c)
+        nat.check(lib.ee_eval_thresholds_host(
+            nat.workspace(), scores.ctypes.data if scores.size else None,
+            correct_ext.ctypes.data if correct_ext.size else None, n, r, serve.ctypes.data,
+            float(vanilla), thresholds.ctypes.data if thresholds.size else None, c, code,
+            acc.ctypes.data, sav.ctypes.data, 0, nat.stream_handle(torch)))
+        return acc, sav
     d_s = _to_device(torch, scores)
     bits, flag = pack_correct(correct_ext, torch)
     acc = torch.empty(c, dtype=torch.float64, device="cuda")

@@ -7,6 +7,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 from paper_2312_05385_b200 import _native, kernels
@@ -102,3 +103,25 @@ def test_no_gpu_means_loud_failure(monkeypatch):
         pytest.skip("a GPU is present")
     with pytest.raises(Exception, match="CUDA device"):
         kernels.exit_sites(np.zeros((3, 2)), np.zeros(2))
+
+
+def test_host_pack_correct_matches_numpy_and_rejects_non_binary():
+    """ee_pack_correct_host (the CPU half of ee_eval_thresholds_host) is plain
+    host code: bit j of row i = correct_ext[i, j], multi-threaded, exact."""
+    from paper_2312_05385_b200 import kernels
+
+    rng = np.random.default_rng(5)
+    for n, r1 in [(0, 3), (1, 1), (37, 13), (100_003, 13), (5000, 32)]:
+        cext = rng.integers(0, 2, size=(n, r1)).astype(np.float64)
+        want = (cext.astype(np.uint64) << np.arange(r1, dtype=np.uint64)).sum(axis=1).astype(np.uint32) \
+            if n else np.empty(0, dtype=np.uint32)
+        for threads in (1, 3, 0):
+            got = kernels.pack_correct_host(cext, n_threads=threads)
+            assert np.array_equal(got, want)
+    bad = np.zeros((9000, 4))
+    bad[7777, 2] = 0.5
+    with pytest.raises(ValueError):
+        kernels.pack_correct_host(bad)
+    bad[7777, 2] = np.nan
+    with pytest.raises(ValueError):
+        kernels.pack_correct_host(bad)
