@@ -1,0 +1,398 @@
+"""Token-level early exit for generative decoding on the GPU (BASELINE config 5,
+SURVEY §8a row A15; north star: "GPT-2-medium-shape decoder token-level early
+exit with KV-cache fill for skipped layers, batch 32 decode, time-per-token").
+
+The reference models this as a latency timeline (pkg/src/eesim/generative.py,
+_SequenceSim at 170-273). Here the same schedule runs for real on a
+GPT-2-medium-shape decoder (random init, bf16):
+
+  * every decode step runs the prefix layers [0, L) for all B sequences, then
+    the ramp: the model's own final LayerNorm + LM head on the layer-L hidden
+    state ("GPT-2: final LN + LM head") as a 5th-gen
+    tensor-core GEMM (ee_gemm_bf16_tn) followed by the fused confidence +
+    strict-compare epilogue (ee_exit_from_logits; engine.py:207's rule);
+  * a token that exits releases the ramp's argmax at once; its suffix layers
+    [L, N) are deferred: its layer-L hidden state is parked per sequence
+    (generative.py:217-218);
+  * the next token of that sequence that does not exit carries every deferred
+    suffix with it (generative.py:230-259): one suffix pass over the chunk
+    [deferred..., current] fills the KV cache of the skipped layers for the
+    deferred positions and computes the current token's output;
+  * a sequence that parks flush_cap suffixes flushes them at once ("cap",
+    generative.py:219-220), and the end of decoding flushes the rest ("end").
+
+So the KV cache of every layer ends up exactly as full decoding would leave it
+(inputs always run to completion), and every token — exited or
+not — also gets the original model's output, which is the feedback the
+reference's tuner consumes (token_feedback, generative.py:284-306).
+
+Both passes run at fixed shapes (B x 1 prefix tokens, B x (flush_cap + 1)
+suffix chunk slots with masks) and are captured as CUDA graphs; decode at
+batch 32 is weight-bandwidth bound, so the padded suffix slots cost little.
+Per-token release latency (time-per-token) is measured with CUDA events:
+ramp release for exits, suffix + head for the rest.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2312_05385_b200 import _native as nat
+from paper_2312_05385_b200.errors import ParameterError
+from paper_2312_05385_b200.heads import exit_from_logits, linear_tc
+
+
+@dataclass(frozen=True)
+class GPT2Spec:
+    n_layer: int = 24   # GPT-2-medium
+    d_model: int = 1024
+    n_head: int = 16
+    vocab: int = 50257
+    n_pos: int = 1024
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_head
+
+
+class GPT2Decoder:
+    """GPT-2-shape decoder weights (random init, GPT-2 init scheme) and a static
+    KV cache [layer][B, H, T + 1, Dh] (slot T is a write sink for padding)."""
+
+    def __init__(self, spec: GPT2Spec = GPT2Spec(), *, batch: int, max_tokens: int, seed: int = 0):
+        torch = nat.torch_cuda()
+        self.torch = torch
+        self.spec = spec
+        self.B = batch
+        self.T = max_tokens
+        if max_tokens > spec.n_pos:
+            raise ParameterError(f"max_tokens {max_tokens} exceeds n_pos {spec.n_pos}")
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        d, bf = spec.d_model, torch.bfloat16
+
+        def normal(*shape, std=0.02):
+            return (torch.randn(*shape, generator=g, device="cuda") * std).to(bf)
+
+        self.wte = normal(spec.vocab, d)
+        self.wpe = normal(spec.n_pos, d, std=0.01)
+        proj_std = 0.02 / math.sqrt(2 * spec.n_layer)
+        self.layers = []
+        for _ in range(spec.n_layer):
+            self.layers.append({
+                "ln1_w": torch.ones(d, device="cuda", dtype=bf), "ln1_b": torch.zeros(d, device="cuda", dtype=bf),
+                "qkv_w": normal(3 * d, d), "qkv_b": torch.zeros(3 * d, device="cuda", dtype=bf),
+                "o_w": normal(d, d, std=proj_std), "o_b": torch.zeros(d, device="cuda", dtype=bf),
+                "ln2_w": torch.ones(d, device="cuda", dtype=bf), "ln2_b": torch.zeros(d, device="cuda", dtype=bf),
+                "fc_w": normal(4 * d, d), "fc_b": torch.zeros(4 * d, device="cuda", dtype=bf),
+                "pr_w": normal(d, 4 * d, std=proj_std), "pr_b": torch.zeros(d, device="cuda", dtype=bf),
+            })
+        self.lnf_w = torch.ones(d, device="cuda", dtype=bf)
+        self.lnf_b = torch.zeros(d, device="cuda", dtype=bf)
+        H, Dh = spec.n_head, spec.head_dim
+        self.k_cache = [torch.zeros(batch, H, max_tokens + 1, Dh, device="cuda", dtype=bf)
+                        for _ in range(spec.n_layer)]
+        self.v_cache = [torch.zeros_like(k) for k in self.k_cache]
+        self.rows = torch.arange(batch, device="cuda")
+        self.key_idx = torch.arange(max_tokens + 1, device="cuda")
+
+    # ---- one pass over layers [l0, l1) for a [B, q, d] chunk at absolute positions
+    def layers_forward(self, h, pos, l0: int, l1: int):
+        """h bf16 [B, q, d]; pos i64 [B, q] (-1 = padding: no KV write, output unused).
+        Appends K/V at `pos` in layers [l0, l1) and attends causally over the cache."""
+        torch = self.torch
+        F = torch.nn.functional
+        B, q, d = h.shape
+        H, Dh, T = self.spec.n_head, self.spec.head_dim, self.T
+        valid = pos >= 0
+        wpos = torch.where(valid, pos, torch.full_like(pos, T))  # padding -> sink slot T
+        rows = self.rows[:, None].expand(B, q)
+        # key j visible to query (b, i) iff j <= pos[b, i]; padding queries see key 0 only
+        qpos = torch.where(valid, pos, torch.zeros_like(pos))
+        mask = (self.key_idx[None, None, :] <= qpos[:, :, None]) & (self.key_idx[None, None, :] < T)
+        mask = mask[:, None, :, :]
+        for l in range(l0, l1):
+            w = self.layers[l]
+            x = F.layer_norm(h, (d,), w["ln1_w"], w["ln1_b"], eps=1e-5)
+            qkv = F.linear(x, w["qkv_w"], w["qkv_b"]).view(B, q, 3, H, Dh)
+            qh = qkv[:, :, 0].transpose(1, 2)
+            self.k_cache[l][rows, :, wpos] = qkv[:, :, 1]
+            self.v_cache[l][rows, :, wpos] = qkv[:, :, 2]
+            att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l], attn_mask=mask)
+            h = h + F.linear(att.transpose(1, 2).reshape(B, q, d), w["o_w"], w["o_b"])
+            x = F.layer_norm(h, (d,), w["ln2_w"], w["ln2_b"], eps=1e-5)
+            h = h + F.linear(F.gelu(F.linear(x, w["fc_w"], w["fc_b"]), approximate="tanh"),
+                             w["pr_w"], w["pr_b"])
+        return h
+
+    def embed(self, tokens, pos):
+        return self.wte[tokens] + self.wpe[pos.clamp(min=0)]
+
+    def head_logits(self, h2d):
+        """Final LN + tied LM head on [M, d] -> fp32 [M, V] (tcgen05 GEMM)."""
+        F = self.torch.nn.functional
+        x = F.layer_norm(h2d, (self.spec.d_model,), self.lnf_w, self.lnf_b, eps=1e-5)
+        return linear_tc(x.to(self.torch.bfloat16).contiguous(), self.wte)
+
+    def reset(self):
+        for k, v in zip(self.k_cache, self.v_cache):
+            k.zero_()
+            v.zero_()
+
+    def full_forward(self, tokens):
+        """Teacher-forced causal forward of [B, T'] tokens through every layer
+        (fresh cache, one chunk): the reference for KV-fill correctness."""
+        torch = self.torch
+        B, Tn = tokens.shape
+        pos = torch.arange(Tn, device="cuda")[None, :].expand(B, Tn).contiguous()
+        self.reset()
+        h = self.layers_forward(self.embed(tokens, pos), pos, 0, self.spec.n_layer)
+        F = torch.nn.functional
+        return F.layer_norm(h, (self.spec.d_model,), self.lnf_w, self.lnf_b, eps=1e-5)
+
+
+@dataclass
+class TokenLog:
+    """One generated token of one sequence (host)."""
+    seq: int
+    index: int        # 0 = first generated token
+    err: float        # ramp error score
+    ramp_label: int   # ramp argmax
+    exited: bool
+    released: int     # the token emitted (ramp label if exited, else the model's)
+    final: int = -1   # the original model's token (filled when its suffix runs)
+    tpt_ms: float = float("nan")
+
+
+@dataclass
+class DecodeReport:
+    tokens: list[TokenLog]
+    flushes: list[tuple[int, int, int, str]]  # (seq, step, count, kind)
+    step_ms: list[float]
+    final_hidden: dict = field(default_factory=dict)  # (seq, position) -> fp32 [d] (optional)
+
+
+class TokenEEDecoder:
+    """Batch decoding with one ramp after layer `ramp_layer` (max_ramps = 1,
+    generative.py:78) and the reference's deferral schedule."""
+
+    def __init__(self, model: GPT2Decoder, ramp_layer: int, threshold: float, *,
+                 flush_cap: int = 4, conf: str = "maxprob", use_graphs: bool = True):
+        if not 1 <= ramp_layer < model.spec.n_layer:
+            raise ParameterError("ramp_layer must be inside the decoder")
+        if flush_cap < 1:
+            raise ParameterError("flush_cap must be >= 1")
+        self.m = model
+        self.L = ramp_layer
+        self.cap = flush_cap
+        self.conf = conf
+        self.use_graphs = use_graphs
+        torch = model.torch
+        B, d, C = model.B, model.spec.d_model, flush_cap + 1
+        self.threshold = torch.full((1,), float(threshold), dtype=torch.float64, device="cuda")
+        # static buffers (CUDA-graph inputs / outputs)
+        self.cur = torch.zeros(B, dtype=torch.long, device="cuda")
+        self.ppos = torch.zeros(B, 1, dtype=torch.long, device="cuda")
+        self.h_ramp = torch.zeros(B, d, dtype=torch.bfloat16, device="cuda")
+        self.err = torch.zeros(B, dtype=torch.float32, device="cuda")
+        self.label = torch.zeros(B, dtype=torch.int32, device="cuda")
+        self.exits = torch.zeros(B, dtype=torch.uint8, device="cuda")
+        self.chunk = torch.zeros(B, C, d, dtype=torch.bfloat16, device="cuda")
+        self.spos = torch.full((B, C), -1, dtype=torch.long, device="cuda")
+        self.final_label = torch.zeros(B * C, dtype=torch.int32, device="cuda")
+        self.final_err = torch.zeros(B * C, dtype=torch.float32, device="cuda")
+        self.final_h = torch.zeros(B, C, d, dtype=torch.float32, device="cuda")
+        self.never = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")  # argmax only
+        self._g_prefix = self._g_suffix = None
+
+    # ---- the two fixed-shape passes
+    def _prefix(self):
+        m = self.m
+        h = m.layers_forward(m.embed(self.cur[:, None], self.ppos), self.ppos, 0, self.L)
+        self.h_ramp.copy_(h[:, 0])
+        logits = m.head_logits(self.h_ramp)
+        exit_from_logits(logits, self.threshold, conf=self.conf, site=0,
+                         out_err=self.err, out_label=self.label, out_exits=self.exits)
+
+    def _suffix(self):
+        m = self.m
+        B, C, d = self.chunk.shape
+        h = m.layers_forward(self.chunk, self.spos, self.L, m.spec.n_layer)
+        F = m.torch.nn.functional
+        self.final_h.copy_(F.layer_norm(h, (d,), m.lnf_w, m.lnf_b, eps=1e-5).float())
+        logits = linear_tc(self.final_h.view(B * C, d).to(m.torch.bfloat16).contiguous(), m.wte)
+        exit_from_logits(logits, self.never, conf=self.conf, site=1,
+                         out_err=self.final_err, out_label=self.final_label)
+
+    def _capture(self):
+        torch = self.m.torch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):  # warm-up allocations outside the capture
+                self._prefix()
+                self._suffix()
+        torch.cuda.current_stream().wait_stream(s)
+        self._g_prefix = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._g_prefix):
+            self._prefix()
+        self._g_suffix = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._g_suffix):
+            self._suffix()
+
+    def run_prefix(self):
+        (self._g_prefix.replay() if self._g_prefix else self._prefix())
+
+    def run_suffix(self):
+        (self._g_suffix.replay() if self._g_suffix else self._suffix())
+
+    # ---- decoding
+    def prefill(self, prompt):
+        """Full forward over the prompt [B, P] (no early exit); returns the first
+        generated token per sequence."""
+        torch = self.m.torch
+        m = self.m
+        B, P = prompt.shape
+        pos = torch.arange(P, device="cuda")[None, :].expand(B, P).contiguous()
+        m.reset()
+        h = m.layers_forward(m.embed(prompt, pos), pos, 0, m.spec.n_layer)
+        logits = m.head_logits(h[:, -1].contiguous())
+        res = exit_from_logits(logits, self.never, conf=self.conf)
+        return res.label.long(), P
+
+    def generate(self, prompt, n_new: int, *, keep_hidden: bool = False, timed: bool = True,
+                 fixed_exits=None) -> DecodeReport:
+        """Decode n_new tokens per sequence after `prompt` [B, P]. fixed_exits (bool
+        [n_new, B], optional) forces the exit decisions (tests)."""
+        torch = self.m.torch
+        m = self.m
+        B, C = m.B, self.cap + 1
+        if prompt.shape[0] != B:
+            raise ParameterError("prompt batch must equal the decoder batch")
+        if self.use_graphs and self._g_prefix is None:
+            self.ppos.fill_(-1)  # capture with every write aimed at the sink slot
+            self.spos.fill_(-1)
+            self._capture()
+        first, P = self.prefill(prompt)
+        if P + n_new > m.T:
+            raise ParameterError("prompt + new tokens exceed the KV cache")
+        self.cur.copy_(first)
+        p = np.full(B, P, dtype=np.int64)       # next position in the prefix layers
+        q = np.full(B, P, dtype=np.int64)       # next position in the suffix layers
+        deferred: list[list[TokenLog]] = [[] for _ in range(B)]
+        logs: list[TokenLog] = []
+        flushes: list[tuple[int, int, int, str]] = []
+        step_ms: list[float] = []
+        hidden: dict = {}
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+        rows_t = torch.arange(B, device="cuda")
+
+        def run_chunk(members: dict[int, list[TokenLog]], kinds: dict[int, str], step: int):
+            """Suffix pass for {seq: [tokens...]} (deferred first, current last)."""
+            sp = np.full((B, C), -1, dtype=np.int64)
+            for s, toks in members.items():
+                sp[s, :len(toks)] = np.arange(q[s], q[s] + len(toks))
+            self.spos.copy_(torch.from_numpy(sp))
+            self.run_suffix()
+            fl = self.final_label.view(B, C).cpu().numpy()
+            for s, toks in members.items():
+                for i, t in enumerate(toks):
+                    t.final = int(fl[s, i])
+                    if keep_hidden:
+                        hidden[(s, int(q[s]) + i)] = self.final_h[s, i].clone()
+                q[s] += len(toks)
+                if kinds.get(s):
+                    flushes.append((s, step, sum(1 for t in toks if t.exited), kinds[s]))
+
+        for step in range(n_new):
+            self.ppos.copy_(torch.from_numpy(p[:, None]))
+            ev[0].record()
+            self.run_prefix()
+            ev[1].record()
+            exits = self.exits.cpu().numpy().astype(bool)
+            if fixed_exits is not None:
+                exits = np.asarray(fixed_exits[step], dtype=bool)
+            err = self.err.cpu().numpy()
+            lab = self.label.cpu().numpy()
+            # park this step's layer-L hidden states behind each sequence's deferred ones
+            slot = np.array([len(deferred[s]) for s in range(B)], dtype=np.int64)
+            self.chunk[rows_t, torch.from_numpy(slot).cuda()] = self.h_ramp
+            members, kinds = {}, {}
+            for s in range(B):
+                t = TokenLog(s, step, float(err[s]), int(lab[s]), bool(exits[s]), int(lab[s]))
+                logs.append(t)
+                deferred[s].append(t)
+                if not exits[s]:  # carries every parked suffix with it
+                    members[s] = deferred[s]
+                    if len(deferred[s]) > 1:
+                        kinds[s] = "carry"
+                    deferred[s] = []
+                elif len(deferred[s]) >= self.cap:
+                    members[s] = deferred[s]
+                    kinds[s] = "cap"
+                    deferred[s] = []
+                p[s] += 1
+            if members:
+                run_chunk(members, kinds, step)
+            ev[2].record()
+            ev[2].synchronize()
+            t_ramp = ev[0].elapsed_time(ev[1])
+            t_full = ev[0].elapsed_time(ev[2])
+            step_ms.append(t_full)
+            nxt = np.empty(B, dtype=np.int64)
+            for s in range(B):
+                t = logs[-B + s]
+                t.tpt_ms = t_ramp if t.exited else t_full
+                if not t.exited:
+                    t.released = t.final
+                nxt[s] = t.released
+            self.cur.copy_(torch.from_numpy(nxt))
+        # end of decoding: flush what is still parked
+        members = {s: deferred[s] for s in range(B) if deferred[s]}
+        if members:
+            run_chunk(members, {s: "end" for s in members}, n_new)
+        return DecodeReport(logs, flushes, step_ms, hidden)
+
+
+def vanilla_step_ms(model: GPT2Decoder, prompt, n_new: int) -> list[float]:
+    """Reference decode (no ramp): every token runs all layers + head, batch B,
+    one CUDA graph per step shape. Returns per-step milliseconds."""
+    torch = model.torch
+    B, P = prompt.shape
+    dec = TokenEEDecoder(model, ramp_layer=model.spec.n_layer - 1, threshold=0.0, use_graphs=False)
+    first, _ = dec.prefill(prompt)
+    cur = torch.zeros(B, dtype=torch.long, device="cuda")
+    pos = torch.zeros(B, 1, dtype=torch.long, device="cuda")
+    never = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")
+    lab = torch.zeros(B, dtype=torch.int32, device="cuda")
+    errb = torch.zeros(B, dtype=torch.float32, device="cuda")
+
+    def step():
+        h = model.layers_forward(model.embed(cur[:, None], pos), pos, 0, model.spec.n_layer)
+        logits = model.head_logits(h[:, 0].contiguous())
+        exit_from_logits(logits, never, out_err=errb, out_label=lab)
+
+    cur.copy_(first)
+    pos.fill_(P)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    out = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(n_new):
+        pos.fill_(P + i)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1))
+        cur.copy_(lab.long())
+    return out

@@ -53,11 +53,11 @@ class SlotTable:
                    torch.full((slots,), -1, dtype=torch.int32, device="cuda"))
 
 
-def _outputs(torch, b, k, want_logits, out_err=None, out_label=None):
+def _outputs(torch, b, k, want_logits, out_err=None, out_label=None, out_exits=None):
     dev = "cuda"
     return (out_err if out_err is not None else torch.empty(b, dtype=torch.float32, device=dev),
             out_label if out_label is not None else torch.empty(b, dtype=torch.int32, device=dev),
-            torch.empty(b, dtype=torch.uint8, device=dev),
+            out_exits if out_exits is not None else torch.empty(b, dtype=torch.uint8, device=dev),
             torch.empty((b, k), dtype=torch.float32, device=dev) if want_logits else None,
             torch.empty(b, dtype=torch.int32, device=dev),
             torch.empty(1, dtype=torch.int32, device=dev))
@@ -136,7 +136,7 @@ def _threshold_args(torch, threshold):
 
 def exit_from_logits(logits, threshold, *, conf: str = "maxprob", site: int = 0,
                      alive=None, slot=None, slots: SlotTable | None = None,
-                     out_err=None, out_label=None) -> ExitResult:
+                     out_err=None, out_label=None, out_exits=None) -> ExitResult:
     """Confidence + compare + compaction + scatter over precomputed fp32 logits [B, K]."""
     torch = nat.torch_cuda()
     if logits.dtype != torch.float32 or logits.dim() != 2 or not logits.is_cuda:
@@ -144,7 +144,7 @@ def exit_from_logits(logits, threshold, *, conf: str = "maxprob", site: int = 0,
     logits = logits.contiguous()
     b, k = logits.shape
     _check_aux(torch, b, alive, slot)
-    err, label, exits, _, keep, n_keep = _outputs(torch, b, k, False, out_err, out_label)
+    err, label, exits, _, keep, n_keep = _outputs(torch, b, k, False, out_err, out_label, out_exits)
     th_val, th_ptr = _threshold_args(torch, threshold)
     nat.check(nat.load_library().ee_exit_from_logits(
         nat.workspace(), logits.data_ptr(), b, k, CONF[conf], th_val, th_ptr, nat.ptr(alive),
