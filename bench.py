@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--family", choices=["diagonal", "axis", "random"], default="diagonal")
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extra", action="store_true",
+                   help="skip the other BASELINE configs (1-3 EE inference, 5 token-level decode)")
     return p.parse_args()
 
 
@@ -331,6 +333,8 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, arrays, prof, sites, th, acc, sav)
+    if rank == 0 and world == 1 and not args.no_extra:
+        line.update(other_configs())
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -399,6 +403,29 @@ def cpu_baseline(args, arrays, prof, sites, th, acc_gpu, sav_gpu):
             "sample": f"full workload ({args.n} samples x {th.shape[0]} candidates), one pass, "
                       f"{procs} forked processes over sample shards",
             "agrees_with_gpu": agree}
+
+
+def other_configs():
+    """The other BASELINE configs, each in its own process after the timed region:
+    1-3 EE batch inference (samples/s, p50 batch and per-request release latency;
+    tools/bench_ee.py) and 5 token-level EE decode (time-per-token p50 vs vanilla;
+    tools/bench_gen.py). Reported beside the config-4 metric, not instead of it."""
+    import subprocess
+
+    out = {}
+    for key, cmd, t in (("ee_inference", ["tools/bench_ee.py"], 420),
+                        ("generative", ["tools/bench_gen.py"], 300)):
+        try:
+            r = subprocess.run([sys.executable, os.path.join(ROOT, *cmd[0].split("/"))] + cmd[1:],
+                               capture_output=True, text=True, timeout=t, cwd=ROOT)
+            lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+            if r.returncode != 0 or not lines:
+                out[key] = {"error": (r.stderr or r.stdout)[-400:]}
+            else:
+                out[key] = lines if key == "ee_inference" else lines[-1]
+        except Exception as exc:  # reported, never fatal to the main line
+            out[key] = {"error": repr(exc)[:400]}
+    return out
 
 
 def traffic_from_profiles():

@@ -108,7 +108,9 @@ class GPT2Decoder:
         H, Dh, T = self.spec.n_head, self.spec.head_dim, self.T
         valid = pos >= 0
         wpos = torch.where(valid, pos, torch.full_like(pos, T))  # padding -> sink slot T
-        rows = self.rows[:, None].expand(B, q)
+        # one scatter index per pass, shared by every layer: cache viewed as
+        # [B*H, T+1, Dh], rows b*H + h, slot wpos[b, i]
+        sidx = wpos[:, None, :, None].expand(B, H, q, Dh).reshape(B * H, q, Dh)
         # key j visible to query (b, i) iff j <= pos[b, i]; padding queries see key 0 only
         qpos = torch.where(valid, pos, torch.zeros_like(pos))
         mask = (self.key_idx[None, None, :] <= qpos[:, :, None]) & (self.key_idx[None, None, :] < T)
@@ -116,10 +118,10 @@ class GPT2Decoder:
         for l in range(l0, l1):
             w = self.layers[l]
             x = F.layer_norm(h, (d,), w["ln1_w"], w["ln1_b"], eps=1e-5)
-            qkv = F.linear(x, w["qkv_w"], w["qkv_b"]).view(B, q, 3, H, Dh)
-            qh = qkv[:, :, 0].transpose(1, 2)
-            self.k_cache[l][rows, :, wpos] = qkv[:, :, 1]
-            self.v_cache[l][rows, :, wpos] = qkv[:, :, 2]
+            qkv = F.linear(x, w["qkv_w"], w["qkv_b"]).view(B, q, 3, H, Dh).permute(2, 0, 3, 1, 4)
+            qh = qkv[0]
+            self.k_cache[l].view(B * H, T + 1, Dh).scatter_(1, sidx, qkv[1].reshape(B * H, q, Dh))
+            self.v_cache[l].view(B * H, T + 1, Dh).scatter_(1, sidx, qkv[2].reshape(B * H, q, Dh))
             att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l], attn_mask=mask)
             h = h + F.linear(att.transpose(1, 2).reshape(B, q, d), w["o_w"], w["o_b"])
             x = F.layer_norm(h, (d,), w["ln2_w"], w["ln2_b"], eps=1e-5)
