@@ -181,6 +181,14 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits, int64_t b, int3
 int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
                     float* d_c, int64_t m, int64_t n, int64_t k, int32_t splits, void* stream);
 
+/* General form: d_c is fp32 [m, n], or bf16 [m, n] (round to nearest even)
+ * when out_bf16 != 0 — the backbone layers' output type. Warp-specialized
+ * tcgen05 kernel: TMA (SWIZZLE_128B) 4-stage ring, one MMA-issuing thread,
+ * TMEM accumulators, 4 epilogue warps; split-K partials are summed in order. */
+int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
+                 void* d_c, int32_t out_bf16, int64_t m, int64_t n, int64_t k, int32_t splits,
+                 void* stream);
+
 /* Global average pool NCHW [b, c, hw] (f32, or bf16 when x_bf16) -> bf16
  * [b, c] (round to nearest even): the A operand of a large ramp head. */
 int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t hw, void* d_out,

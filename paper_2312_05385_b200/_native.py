@@ -61,6 +61,7 @@ SIGNATURES = {
     "ee_profile_enable": (ctypes.c_int, [_vp, _c_i32]),
     "ee_workspace_set_special": (ctypes.c_int, [_vp, _c_i32]),
     "ee_workspace_set_diag_version": (ctypes.c_int, [_vp, _c_i32]),
+    "ee_gemm_bf16": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i32, _c_i64, _c_i64, _c_i64, _c_i32, _vp]),
     "ee_eval_thresholds_host": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i32, _vp, ctypes.c_double,
                                                 _vp, _c_i64, _c_i32, _vp, _vp, _c_i32, _vp]),
     "ee_pack_correct_host": (ctypes.c_int, [_vp, _c_i64, _c_i32, _vp, _c_i32]),

@@ -470,6 +470,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
 #include "gemm_tc.cuh"
+#include "gemm_tc2.cuh"
 namespace {
 
 // L2 eviction for benchmarks: streams a buffer larger than L2 with the same
@@ -1288,7 +1289,7 @@ static void pack_rows_fixed(const double* c, int64_t i0, int64_t i1, uint32_t* b
   for (int64_t i = i0; i < i1; ++i) {
     const uint64_t* row = u + i * R1;
     uint32_t w = 0;
-#pragma GCC unroll 32
+
     for (int j = 0; j < R1; ++j) {
       const uint64_t x = row[j];
       const uint64_t one = x == 0x3ff0000000000000ull;
@@ -1650,8 +1651,56 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
   return EE_OK;
 }
 
-int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
-                    float* d_c, int64_t m, int64_t n, int64_t k, int32_t splits, void* stream) {
+}  // extern "C"
+// TMA descriptors: cuTensorMapEncodeTiled through the runtime's driver entry
+// point (no libcuda link). A bf16 [rows, k] K-major operand, 64 x box_rows
+// boxes (128 B rows), SWIZZLE_128B, zero fill out of bounds.
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool make_operand_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t k,
+                             int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+  cuuint32_t box[2] = {(cuuint32_t)gemm2::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool BF>
+static cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const float* bias,
+                                void* c, int m, int n, int k, int per, float* partials, dim3 grid,
+                                cudaStream_t st) {
+  auto kern = gemm2::k_gemm2<BN, BF>;
+  constexpr int smem = gemm2::smem_bytes<BN>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<grid, gemm2::THREADS, smem, st>>>(ta, tb, bias, c, m, n, k, per, partials);
+  return cudaGetLastError();
+}
+extern "C" {
+
+int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
+                 void* d_c, int32_t out_bf16, int64_t m, int64_t n, int64_t k, int32_t splits,
+                 void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
   if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(EE_ERR_ARG, "bad GEMM shape");
@@ -1661,9 +1710,11 @@ int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const fl
     return fail(EE_ERR_ARG, "A and B must be 16-byte aligned");
   std::lock_guard<std::mutex> lock(ws->mu);
   auto st = (cudaStream_t)stream;
-  const int BN = n >= 128 ? 128 : 64;
-  const int64_t mt = ceil_div(m, gemmtc::BM), nt = ceil_div(n, BN);
-  const int kt_total = (int)ceil_div(k, gemmtc::BK);
+  const int64_t mt = ceil_div(m, gemm2::BM);
+  // wide tiles when they alone fill the SMs, else 128 columns (+ split-K)
+  const int BN = mt * ceil_div(n, 256) >= sm_count() ? 256 : 128;
+  const int64_t nt = ceil_div(n, BN);
+  const int kt_total = (int)ceil_div(k, gemm2::BK);
   int sp = splits;
   if (sp <= 0) sp = (int)std::max<int64_t>(1, std::min<int64_t>(kt_total, sm_count() / std::max<int64_t>(1, mt * nt)));
   sp = std::min(sp, kt_total);
@@ -1675,33 +1726,37 @@ int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const fl
     if (rc) return rc;
     partials = static_cast<float*>(ws->d_buf);
   }
-  const size_t smem = 2 * ((size_t)gemmtc::BM * gemmtc::BK * 2 + (size_t)BN * gemmtc::BK * 2);
+  CUtensorMap ta, tb;
+  if (!make_operand_map(&ta, d_a, m, k, gemm2::BM) || !make_operand_map(&tb, d_b, n, k, BN))
+    return fail(EE_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)sp);
+  cudaError_t e;
   {
-    ProfScope ps(ws, st, "k_gemm_bf16");
-    if (BN == 128) {
-      EE_CUDA(cudaFuncSetAttribute(gemmtc::k_gemm_bf16<128>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      gemmtc::k_gemm_bf16<128><<<grid, gemmtc::THREADS, smem, st>>>(
-          static_cast<const uint16_t*>(d_a), static_cast<const uint16_t*>(d_b), d_bias, d_c,
-          (int)m, (int)n, (int)k, per, partials);
-    } else {
-      EE_CUDA(cudaFuncSetAttribute(gemmtc::k_gemm_bf16<64>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      gemmtc::k_gemm_bf16<64><<<grid, gemmtc::THREADS, smem, st>>>(
-          static_cast<const uint16_t*>(d_a), static_cast<const uint16_t*>(d_b), d_bias, d_c,
-          (int)m, (int)n, (int)k, per, partials);
-    }
+    ProfScope ps(ws, st, "k_gemm2");
+    if (BN == 256)
+      e = out_bf16 ? launch_gemm2<256, true>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st)
+                   : launch_gemm2<256, false>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st);
+    else
+      e = out_bf16 ? launch_gemm2<128, true>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st)
+                   : launch_gemm2<128, false>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st);
   }
-  EE_LAUNCH_CHECK();
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_gemm2: ") + cudaGetErrorString(e));
   if (sp > 1) {
     ProfScope ps(ws, st, "k_splitk_sum");
     const int64_t mn = m * n;
-    gemmtc::k_splitk_sum<<<(unsigned)std::min<int64_t>(ceil_div(mn, 256), sm_count() * 8), 256, 0,
-                           st>>>(partials, sp, mn, (int)n, d_bias, d_c);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(mn, 256), sm_count() * 8);
+    if (out_bf16)
+      gemm2::k_splitk_sum2<true><<<g, 256, 0, st>>>(partials, sp, mn, (int)n, d_bias, d_c);
+    else
+      gemm2::k_splitk_sum2<false><<<g, 256, 0, st>>>(partials, sp, mn, (int)n, d_bias, d_c);
     EE_LAUNCH_CHECK();
   }
   return EE_OK;
+}
+
+int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
+                    float* d_c, int64_t m, int64_t n, int64_t k, int32_t splits, void* stream) {
+  return ee_gemm_bf16(ws, d_a, d_b, d_bias, d_c, 0, m, n, k, splits, stream);
 }
 
 int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t hw, void* d_out,

@@ -173,9 +173,10 @@ def compact_rows(src, keep, n_keep, out=None):
     return out
 
 
-def linear_tc(x, weight, bias=None, *, splits: int = 0):
-    """fp32 [M, N] = x bf16 [M, K] @ weight bf16 [N, K]^T + bias, on the 5th-gen
-    tensor cores (tcgen05.mma with TMEM accumulators; ee_gemm_bf16_tn)."""
+def linear_tc(x, weight, bias=None, *, splits: int = 0, out_bf16: bool = False):
+    """[M, N] = x bf16 [M, K] @ weight bf16 [N, K]^T + bias (fp32, or bf16 with
+    out_bf16), on the 5th-gen tensor cores: TMA-fed, warp-specialized
+    tcgen05.mma with TMEM accumulators (ee_gemm_bf16)."""
     torch = nat.torch_cuda()
     if x.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
         raise ParameterError("linear_tc takes bf16 operands")
@@ -184,11 +185,11 @@ def linear_tc(x, weight, bias=None, *, splits: int = 0):
     n = weight.shape[0]
     if weight.shape[1] != k:
         raise ParameterError("inner dimensions differ")
-    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    out = torch.empty((m, n), dtype=torch.bfloat16 if out_bf16 else torch.float32, device="cuda")
     b = None if bias is None else bias.float().contiguous()
-    nat.check(nat.load_library().ee_gemm_bf16_tn(
-        nat.workspace(), x.data_ptr(), weight.data_ptr(), nat.ptr(b), out.data_ptr(), m, n, k,
-        splits, nat.stream_handle(torch)))
+    nat.check(nat.load_library().ee_gemm_bf16(
+        nat.workspace(), x.data_ptr(), weight.data_ptr(), nat.ptr(b), out.data_ptr(), int(out_bf16),
+        m, n, k, splits, nat.stream_handle(torch)))
     return out
 
 

@@ -53,3 +53,25 @@ def test_large_ramp_head_end_to_end(cuda):
     assert torch.allclose(res.logits.cpu(), ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
     err_ref, _ = H.confidence(res.logits.cpu(), "entropy")
     assert torch.allclose(res.err.cpu().double(), err_ref, atol=2e-5, rtol=0)
+
+
+@pytest.mark.parametrize("m,n,k", [(32, 3072, 1024), (32, 50257, 1024), (160, 4096, 1024),
+                                   (1000, 700, 136), (8192, 2304, 768), (8192, 768, 3072)])
+def test_gemm_bf16_out_and_backbone_shapes(cuda, m, n, k):
+    """Backbone / decode shapes (GPT-2-medium decode at batch 32 and 160, BERT
+    encoder tiles), fp32 and bf16 outputs, against cuBLAS fp32 on the same
+    bf16 operands."""
+    torch = cuda
+    from paper_2312_05385_b200.heads import linear_tc
+
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    x = torch.randn(m, k, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(n, k, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    bias = torch.randn(n, generator=g, device="cuda")
+    ref = torch.nn.functional.linear(x.float(), w.float(), bias)
+    scale = ref.abs().max().item()
+    got = linear_tc(x, w, bias)
+    assert torch.allclose(got, ref, rtol=1e-3, atol=1e-3 * scale), (got - ref).abs().max()
+    gb = linear_tc(x, w, bias, out_bf16=True)
+    assert gb.dtype == torch.bfloat16
+    assert torch.allclose(gb.float(), ref, rtol=1e-2, atol=1e-2 * scale)
