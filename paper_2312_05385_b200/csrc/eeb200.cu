@@ -524,6 +524,7 @@ struct ee_workspace {
     cudaEvent_t a, b;
   };
   std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;  // recycled by ee_profile_read (no create per launch)
 };
 
 namespace {
@@ -535,10 +536,20 @@ struct ProfScope {
   const char* name;
   ProfScope(ee_workspace* w, cudaStream_t s, const char* n) : ws(w), st(s), name(n) {
     if (ws && ws->profiling) {
-      cudaEventCreate(&a);
-      cudaEventCreate(&b);
+      a = take();
+      b = take();
       cudaEventRecord(a, st);
     }
+  }
+  cudaEvent_t take() {
+    cudaEvent_t e = nullptr;
+    if (!ws->event_pool.empty()) {
+      e = ws->event_pool.back();
+      ws->event_pool.pop_back();
+    } else {
+      cudaEventCreate(&e);
+    }
+    return e;
   }
   ~ProfScope() {
     if (a) {
@@ -692,6 +703,8 @@ int ee_workspace_destroy(ee_workspace* ws) {
   if (ws->d_buf) cudaFree(ws->d_buf);
   if (ws->d_diag_acc) cudaFree(ws->d_diag_acc);
   if (ws->d_in) cudaFree(ws->d_in);
+  for (auto& m : ws->marks) cudaEventDestroy(m.a), cudaEventDestroy(m.b);
+  for (auto e : ws->event_pool) cudaEventDestroy(e);
   if (ws->h_bits) cudaFreeHost(ws->h_bits);
   if (ws->h_stage) cudaFreeHost(ws->h_stage);
   if (ws->staged) cudaEventDestroy(ws->staged);
@@ -1494,8 +1507,8 @@ int ee_profile_read(ee_workspace* ws, char* buf, int64_t cap) {
     }
     it->launches += 1;
     it->ms += ms;
-    cudaEventDestroy(m.a);
-    cudaEventDestroy(m.b);
+    ws->event_pool.push_back(m.a);
+    ws->event_pool.push_back(m.b);
   }
   ws->marks.clear();
   std::string js = "{";

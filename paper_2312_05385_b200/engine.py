@@ -223,9 +223,10 @@ class WindowEvaluator:
         torch = self._torch
         lib = nat.load_library()
         c = th.shape[0]
-        acc = None if counts_only else torch.empty(c, dtype=torch.float64, device="cuda")
-        sav = None if counts_only else torch.empty(c, dtype=torch.float64, device="cuda")
-        ok = torch.empty(c, dtype=torch.int64, device="cuda")
+        out = torch.empty((3, c), dtype=torch.float64, device="cuda")  # one allocation per call
+        acc = None if counts_only else out[0]
+        sav = None if counts_only else out[1]
+        ok = out[2].view(torch.int64)
         hist = torch.empty((c, self.r + 1), dtype=torch.int64, device="cuda") if want_hist else None
         nat.check(lib.ee_eval_thresholds(
             nat.workspace(), nat.ptr(self.d_scores), self.d_bits.data_ptr(), self.n, self.r,
