@@ -408,13 +408,16 @@ def cpu_baseline(args, arrays, prof, sites, th, acc_gpu, sav_gpu):
 def other_configs():
     """The other BASELINE configs, each in its own process after the timed region:
     1-3 EE batch inference (samples/s, p50 batch and per-request release latency;
-    tools/bench_ee.py) and 5 token-level EE decode (time-per-token p50 vs vanilla;
-    tools/bench_gen.py). Reported beside the config-4 metric, not instead of it."""
+    tools/bench_ee.py), 5 token-level EE decode (time-per-token p50 vs vanilla;
+    tools/bench_gen.py) and the closed serving loop on config 1 (p50 latency,
+    throughput, GPU retunes; tools/bench_serve_live.py). Reported beside the
+    config-4 metric, not instead of it."""
     import subprocess
 
     out = {}
     for key, cmd, t in (("ee_inference", ["tools/bench_ee.py"], 420),
-                        ("generative", ["tools/bench_gen.py"], 300)):
+                        ("generative", ["tools/bench_gen.py"], 300),
+                        ("serving_loop", ["tools/bench_serve_live.py"], 300)):
         try:
             r = subprocess.run([sys.executable, os.path.join(ROOT, *cmd[0].split("/"))] + cmd[1:],
                                capture_output=True, text=True, timeout=t, cwd=ROOT)
