@@ -36,7 +36,7 @@
 
 namespace diag2 {
 
-constexpr int THREADS = 512;  // 148 x 512 launches ~3 us cheaper than 148 x 1024 (tools/micro/params2.cu)
+constexpr int THREADS = 1024;
 constexpr int WARPS = THREADS / 32;
 constexpr int MAX_M = 127;  // distinct thresholds (7-bit keys)
 constexpr int NB = 256;     // bins
@@ -173,10 +173,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
   const int64_t nchunks = (n + 31) >> 5;
   const int64_t G = (int64_t)gridDim.x * WARPS;
   int64_t ch = (int64_t)blockIdx.x * WARPS + warp;
-  // two chunks in flight per warp (register double buffer)
-  double2 va[R / 2], vb[R / 2];
-  uint32_t cba = 0, cbb = 0;
-  auto load = [&](double2 (&v)[R / 2], uint32_t& cb, int64_t c) {
+  double2 v[R / 2];
+  uint32_t cb = 0;
+  auto load = [&](int64_t c) {
     if (c >= nchunks) return;
     const int64_t s0 = c << 5;
     const double2* src = reinterpret_cast<const double2*>(P.s + s0 * R);
@@ -195,8 +194,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
     }
   };
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 0] = gtimer();
-  load(va, cba, ch);  // the first HBM round trips overlap the prologue
-  load(vb, cbb, ch + G);
+  load(ch);  // first HBM round trip overlaps the prologue
 
   // ---- prologue: thresholds, the replicated bin table (built on the host), zeroed counters
   for (int i = warp; i <= MAX_M; i += WARPS)  // warp-uniform parameter reads (broadcast LDC)
@@ -225,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
   unsigned char* kb = skey + warp * 32 * R;
   unsigned corr = 0;
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 1] = gtimer();
-  auto step = [&](double2 (&v)[R / 2], uint32_t& cb, int64_t c) {
+  for (; ch < nchunks; ch += G) {
     __syncwarp();  // previous chunk's key reads are done
 #pragma unroll
     for (int k = 0; k < R / 2; ++k) {
@@ -234,7 +232,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
           (unsigned short)__byte_perm(k0, k1, 0x0040);
     }
     const uint32_t cbc = cb;
-    load(v, cb, c + 2 * G);  // refill this buffer while the chunk is counted
+    load(ch + G);  // next chunk in flight while this one is counted
     __syncwarp();
     uint32_t kw[NW];
     if constexpr (R % 16 == 0) {
@@ -284,10 +282,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
     corr += cr;
     if (__any_sync(FULL, cr == 0u))  // Z(p) = #{c_r = 0, b_{r-1} > p}: -1 at b_{r-1}
       red_shared<R * ROWB * 4>(cr == 0u ? dB + 8u * prev : dummy, -1);
-  };
-  for (; ch < nchunks; ch += 2 * G) {
-    step(va, cba, ch);
-    if (ch + G < nchunks) step(vb, cbb, ch + G);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) corr += __shfl_xor_sync(FULL, corr, o);
