@@ -399,7 +399,15 @@ def cpu_baseline(args, arrays, prof, sites, th, acc_gpu, sav_gpu):
     procs = os.cpu_count() or 1
     dt, acc, sav = cpu_sweep(kernel, scores, cext, serve, vanilla, th, procs, args.n)
     agree = bool(np.array_equal(acc, acc_gpu) and np.allclose(sav, sav_gpu, rtol=1e-9))
+    # the reference as shipped: one process, the GIL-holding Cython loop, on a bounded
+    # sample scaled to the full window
+    ns = min(args.n, 100_000)
+    t0 = time.perf_counter()
+    kernel.eval_thresholds(scores[:ns], cext[:ns], serve, vanilla, th)
+    one = (time.perf_counter() - t0) * args.n / ns
     return {"value": th.shape[0] / dt, "unit": UNIT, "cores": procs, "kind": kind,
+            "single_core_value": th.shape[0] / one,
+            "single_core_sample": f"{ns} of {args.n} samples, 1 process, scaled to the full window",
             "sample": f"full workload ({args.n} samples x {th.shape[0]} candidates), one pass, "
                       f"{procs} forked processes over sample shards",
             "agrees_with_gpu": agree}
@@ -417,7 +425,8 @@ def other_configs():
     out = {}
     for key, cmd, t in (("ee_inference", ["tools/bench_ee.py"], 420),
                         ("generative", ["tools/bench_gen.py"], 300),
-                        ("serving_loop", ["tools/bench_serve_live.py"], 300)):
+                        ("serving_loop", ["tools/bench_serve_live.py"], 300),
+                        ("candidate_families", ["tools/bench_families.py"], 300)):
         try:
             r = subprocess.run([sys.executable, os.path.join(ROOT, *cmd[0].split("/"))] + cmd[1:],
                                capture_output=True, text=True, timeout=t, cwd=ROOT)
@@ -426,9 +435,33 @@ def other_configs():
                 out[key] = {"error": (r.stderr or r.stdout)[-400:]}
             else:
                 out[key] = lines if key == "ee_inference" else lines[-1]
+                if key == "ee_inference":
+                    _tensor_roofline(out[key])
         except Exception as exc:  # reported, never fatal to the main line
             out[key] = {"error": repr(exc)[:400]}
     return out
+
+
+# backbone FLOPs per sample, SURVEY §8d (C1 ResNet-18 CIFAR, C2 BERT-base seq 128,
+# C3 ResNet-50 224^2); ramps excluded
+_FLOPS_PER_SAMPLE = {"resnet18_cifar_6ramps": 1.11e9, "bert_base_12ramps_seq128_entropy": 22.35e9,
+                     "resnet50_imagenet_16ramps": 8.2e9}
+
+
+def _tensor_roofline(entries):
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = float(json.load(fh)["bf16_tflops"])
+    except Exception:
+        peak = 2250.0
+    for e in entries:
+        f = _FLOPS_PER_SAMPLE.get(e.get("config"))
+        if not f or "feedback_graph" not in e:
+            continue
+        ach = f * e["feedback_graph"]["samples_per_s"] / 1e12
+        e["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak, "flops_per_sample": f,
+                         "note": "backbone FLOPs x feedback-graph samples/s; batch-limited"}
 
 
 def traffic_from_profiles():
