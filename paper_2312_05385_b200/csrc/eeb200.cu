@@ -1656,10 +1656,16 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
   int rc = exit_out(ws, st, b, d_slot, site, d_err, d_label, d_exit, nullptr, d_keep, d_nkeep,
                     d_slot_label, d_slot_err, d_slot_site, &o);
   if (rc) return rc;
-  ProfScope ps(ws, st, "k_exit_logits");
-  const int rows_per = exitc::THREADS / 32;
-  exitc::k_exit_logits<<<(unsigned)ceil_div(b, rows_per), exitc::THREADS, 0, st>>>(
-      d_logits_in, b, k, conf, threshold, d_threshold, d_alive, o);
+  if (k > 2048) {  // wide head (LM-head ramp): a CTA per row
+    ProfScope ps(ws, st, "k_exit_logits_row");
+    exitc::k_exit_logits_row<<<(unsigned)b, exitc::ROW_THREADS, 0, st>>>(
+        d_logits_in, b, k, conf, threshold, d_threshold, d_alive, o);
+  } else {
+    ProfScope ps(ws, st, "k_exit_logits");
+    const int rows_per = exitc::THREADS / 32;
+    exitc::k_exit_logits<<<(unsigned)ceil_div(b, rows_per), exitc::THREADS, 0, st>>>(
+        d_logits_in, b, k, conf, threshold, d_threshold, d_alive, o);
+  }
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

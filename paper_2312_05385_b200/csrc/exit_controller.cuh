@@ -171,6 +171,15 @@ __global__ void __launch_bounds__(THREADS)
       for (int p = 0; p < HW; ++p) acc += ld_f32(base, (int64_t)p * C + c);
       pooled[c] = acc * inv;
     }
+  } else if (HW <= 64) {
+    // NCHW, small planes (late CNN stages, 4x4 .. 8x8): a thread per channel,
+    // no per-channel warp reduction on the load-latency chain
+    const TF* base = feat + row * (int64_t)C * HW;
+    for (int c = threadIdx.x; c < C; c += THREADS) {
+      float acc = 0.f;
+      for (int p = 0; p < HW; ++p) acc += ld_f32(base, (int64_t)c * HW + p);
+      pooled[c] = acc * inv;
+    }
   } else {
     // NCHW: one warp per channel, lanes over the contiguous HW plane
     const TF* base = feat + row * (int64_t)C * HW;
@@ -228,6 +237,75 @@ __global__ void __launch_bounds__(THREADS)
       o.exits[row] = ex ? 1 : 0;
       if (ex && alive_in) alive_in[row] = 0;
     }
+  }
+  if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
+}
+
+// Wide heads (an LM-head ramp: K = 50257): one CTA per row, block-wide
+// reductions. Same two passes and tie-breaks as confidence(): first maximum
+// (label), then sum exp(l - max) and sum (l - max) exp(l - max).
+constexpr int ROW_THREADS = 512;
+__global__ void __launch_bounds__(ROW_THREADS)
+    k_exit_logits_row(const float* __restrict__ logits_in, int64_t B, int K, int conf,
+                      double threshold, const double* __restrict__ d_threshold,
+                      uint8_t* __restrict__ alive_in, Out o) {
+  if (d_threshold) threshold = *d_threshold;
+  constexpr int NW = ROW_THREADS / 32;
+  __shared__ float s_mx[NW], s_se[NW], s_sle[NW];
+  __shared__ int s_arg[NW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x;
+  const float* l = logits_in + row * K;
+  float mx = -INFINITY;
+  int arg = 0x7fffffff;
+  for (int k = threadIdx.x; k < K; k += ROW_THREADS) {
+    const float v = __ldg(l + k);
+    if (v > mx || (v == mx && k < arg)) {
+      mx = v;
+      arg = k;
+    }
+  }
+#pragma unroll
+  for (int of = 16; of; of >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, of);
+    const int a2 = __shfl_xor_sync(0xffffffffu, arg, of);
+    if (m2 > mx || (m2 == mx && a2 < arg)) mx = m2, arg = a2;
+  }
+  if (lane == 0) s_mx[wid] = mx, s_arg[wid] = arg;
+  __syncthreads();
+  mx = s_mx[0];
+  arg = s_arg[0];
+  for (int w = 1; w < NW; ++w)
+    if (s_mx[w] > mx || (s_mx[w] == mx && s_arg[w] < arg)) mx = s_mx[w], arg = s_arg[w];
+  float se = 0.f, sle = 0.f;
+  for (int k = threadIdx.x; k < K; k += ROW_THREADS) {
+    const float d = __ldg(l + k) - mx;
+    const float e = expf(d);
+    se += e;
+    sle += d * e;
+  }
+  se = warp_sum(se);
+  sle = warp_sum(sle);
+  if (lane == 0) s_se[wid] = se, s_sle[wid] = sle;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    se = 0.f;
+    sle = 0.f;
+    for (int w = 0; w < NW; ++w) se += s_se[w], sle += s_sle[w];
+    float err;
+    if (conf == 0) {
+      err = 1.f - 1.f / se;
+    } else {
+      const float H = logf(se) - sle / se;
+      err = K > 1 ? H / logf((float)K) : 0.f;
+    }
+    err = fminf(fmaxf(err, 0.f), 1.f);
+    const bool alive = alive_in ? alive_in[row] != 0 : true;
+    const bool ex = alive && (double)err < threshold;
+    o.err[row] = err;
+    o.label[row] = arg;
+    o.exits[row] = ex ? 1 : 0;
+    if (ex && alive_in) alive_in[row] = 0;
   }
   if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
 }

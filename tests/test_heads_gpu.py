@@ -116,3 +116,27 @@ def test_exit_rule_is_strict(cuda):
     assert res.exits.cpu().tolist() == [0, 0]
     res = exit_from_logits(logits, np.nextafter(1.0 - 1.0 / k, 2.0), conf="maxprob")
     assert res.exits.cpu().tolist() == [1, 1]
+
+
+@pytest.mark.parametrize("k,conf", [(50257, "maxprob"), (50257, "entropy"), (3000, "maxprob")])
+def test_wide_head_epilogue_matches_torch(cuda, k, conf):
+    """The CTA-per-row epilogue for wide heads (LM-head ramps) against torch fp32:
+    argmax (first maximum), confidence, strict compare."""
+    torch = cuda
+    from paper_2312_05385_b200.heads import exit_from_logits
+
+    g = torch.Generator(device="cuda").manual_seed(k)
+    logits = torch.randn(32, k, generator=g, device="cuda") * 3.0
+    logits[5, 17] = logits[5].max() + 1.0
+    logits[5, 18] = logits[5, 17]  # tie: the first index wins
+    p = torch.softmax(logits.double(), dim=1)
+    if conf == "maxprob":
+        err_ref = 1.0 - p.max(dim=1).values
+    else:
+        err_ref = -(p * torch.log(p.clamp_min(1e-300))).sum(dim=1) / np.log(k)
+    thr = float(err_ref.median())
+    res = exit_from_logits(logits, thr, conf=conf)
+    assert torch.equal(res.label.long().cpu(), torch.argmax(logits, dim=1).cpu())
+    assert int(res.label[5]) == 17
+    assert torch.allclose(res.err.double().cpu(), err_ref.cpu(), atol=2e-5, rtol=0)
+    assert torch.equal(res.exits.bool().cpu(), (res.err.double() < thr).cpu())
