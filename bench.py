@@ -302,6 +302,10 @@ def run_ours(args):
     generic = {"ms_per_step": g_ms, "value": c / (g_ms / 1e3), "unit": UNIT,
                "path": "generic SWAR scan (k_keys + k_count), family specialisation off"}
 
+    # one traced launch (outside the timed region): where the kernel's time goes
+    phases = phase_timeline(sweep, th, flush, n_local=shard_range(args.n, rank, world)[1]
+                            - shard_range(args.n, rank, world)[0], r=r, c=c)
+
     # ------------- end to end: the reference-facing plugin call with host buffers
     e2e = e2e_run(args, arrays, prof, sites, th, rank, world)
 
@@ -317,6 +321,7 @@ def run_ours(args):
         "frac": achieved / peak, "traffic": traffic_from_profiles(),
         "kernel": "sweep = " + " + ".join(sorted(kern)) + f" (dominant: {dominant})",
         "algorithmic_bytes_per_step": b_alg, "peak_source": peak_src,
+        "phase_timeline": phases,
         "kernels": {k: {"launches_per_step": v["launches"] / args.steps,
                         "ms_per_launch": v["ms"] / v["launches"],
                         "share": v["ms"] / max(1e-12, sum(x["ms"] for x in kern.values()))}
@@ -341,6 +346,42 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def phase_timeline(sweep, th, flush, *, n_local, r, c):
+    """k_diag2's own %globaltimer stamps (ee_diag_trace) for one launch: prologue,
+    the streaming sweep loop (bytes / loop time = in-kernel GB/s), the cross-CTA
+    merge and finalise tail. Launch/teardown overhead is what the CUDA events add
+    on top (an empty 148 x 1024-thread kernel measures ~8-10 us between events on
+    B200, tools/micro/params2.cu)."""
+    import torch
+
+    from paper_2312_05385_b200 import _native as nat
+
+    lib = nat.load_library()
+    grid = 1024
+    tr = torch.zeros(grid * 6, dtype=torch.int64, device="cuda")
+    try:
+        flush.zero_()
+        torch.cuda.synchronize()
+        nat.check(lib.ee_diag_trace(nat.workspace(), tr.data_ptr()))
+        sweep.evaluate_many(th, to_host=False)
+        torch.cuda.synchronize()
+    finally:
+        nat.check(lib.ee_diag_trace(nat.workspace(), None))
+    t = tr.cpu().numpy().reshape(grid, 6).astype(np.float64)
+    used = t[:, 0] > 0
+    if not used.any():
+        return None
+    t = t[used]
+    t0 = t[:, 0].min()
+    t = (t - t0) / 1e3
+    loop_us = float(np.median(t[:, 2]) - np.median(t[:, 1]))
+    return {"unit": "us from the first CTA's start", "prologue_end_median": float(np.median(t[:, 1])),
+            "sweep_loop_end_median": float(np.median(t[:, 2])),
+            "sweep_loop_end_max": float(t[:, 2].max()), "kernel_end": float(t[:, 4].max()),
+            "sweep_loop_gbps": algorithmic_bytes(n_local, r, c) / (loop_us * 1e-6) / 1e9,
+            "source": "ee_diag_trace (%globaltimer per CTA), one launch after the timed region"}
 
 
 def e2e_run(args, arrays, prof, sites, th, rank, world):
