@@ -239,9 +239,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; EEB200_DIST_BACKEND=gloo lets a single-GPU box run the N > 1
+    # code path with every rank on cuda:0 (a functional check, not a measurement)
+    backend = os.environ.get("EEB200_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     prof, sites, arrays = window(args.n)
     r = len(sites)
     th = candidates(args.family, args.c, r)
