@@ -1417,28 +1417,54 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
   return EE_OK;
 }
 
+}  // extern "C"
+// serve table by value: the finalisation after an all-reduce is one launch with
+// no staging copy and no host synchronisation
+struct ServeTab {
+  double v[EE_MAX_RAMPS + 1];
+};
+__global__ void k_finalize_p(const unsigned long long* __restrict__ hist,
+                             const unsigned long long* __restrict__ okc, int64_t C, int r,
+                             int64_t n, const __grid_constant__ ServeTab serve, double vanilla,
+                             double* __restrict__ acc, double* __restrict__ sav) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const unsigned long long* h = hist + c * (r + 1);
+  double hi = 0.0, lo = 0.0;
+  for (int site = 0; site <= r; ++site) {  // same arithmetic as k_finalize
+    const double x = (double)h[site];
+    const double p = __dmul_rn(x, serve.v[site]);
+    const double pe = __fma_rn(x, serve.v[site], -p);
+    double s, e;
+    two_sum(hi, p, s, e);
+    hi = s;
+    lo = __dadd_rn(lo, __dadd_rn(e, pe));
+  }
+  double s, e;
+  two_sum(hi, lo, s, e);
+  const double dn = (double)n;
+  acc[c] = __ddiv_rn((double)okc[c], dn);
+  sav[c] = __dsub_rn(vanilla, __ddiv_rn(s, dn));
+}
+extern "C" {
+
 int ee_finalize_hist(ee_workspace* ws, const int64_t* d_hist, const int64_t* d_ok, int64_t c,
                      int32_t r, int64_t n, const double* h_serve, double vanilla, double* d_acc,
                      double* d_sav, void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
   if (c < 0 || r < 0 || n < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
   if (c == 0) return EE_OK;
   if (!d_hist || !d_ok || !h_serve || !d_acc || !d_sav) return fail(EE_ERR_ARG, "null pointer");
   std::lock_guard<std::mutex> lock(ws->mu);
   auto st = (cudaStream_t)stream;
-  const size_t need = align_up((size_t)(r + 1) * 8, 256);
-  int rc = ws_reserve(ws, need, need);
-  if (rc) return rc;
-  std::memcpy(ws->h_stage, h_serve, (size_t)(r + 1) * 8);
-  EE_CUDA(cudaMemcpyAsync(ws->d_buf, ws->h_stage, need, cudaMemcpyHostToDevice, st));
-  EE_CUDA(cudaEventRecord(ws->staged, st));
+  ServeTab tab{};
+  for (int j = 0; j <= r; ++j) tab.v[j] = h_serve[j];
   {
     ProfScope ps(ws, st, "k_finalize");
-    // histogram rows are dense [c][r+1] here: slot r is the no-exit site
-    k_finalize<<<(unsigned)ceil_div(c, 128), 128, 0, st>>>(
+    k_finalize_p<<<(unsigned)ceil_div(c, 128), 128, 0, st>>>(
         reinterpret_cast<const unsigned long long*>(d_hist),
-        reinterpret_cast<const unsigned long long*>(d_ok), c, r, r, n,
-        static_cast<const double*>(ws->d_buf), vanilla, nullptr, nullptr, d_acc, d_sav);
+        reinterpret_cast<const unsigned long long*>(d_ok), c, r, n, tab, vanilla, d_acc, d_sav);
   }
   EE_LAUNCH_CHECK();
   return EE_OK;

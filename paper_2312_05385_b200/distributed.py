@@ -42,6 +42,15 @@ def reduce_counts(hist, ok, group=None):
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return hist, ok
     c, r1 = hist.shape
+    base = hist.untyped_storage().data_ptr()
+    if (hist.is_contiguous() and ok.is_contiguous() and hist.data_ptr() == base
+            and ok.data_ptr() == base + hist.numel() * 8
+            and hist.untyped_storage().nbytes() == (hist.numel() + ok.numel()) * 8):
+        # already one buffer (WindowEvaluator counts-only): all-reduce it in place
+        buf = torch.empty(0, dtype=torch.int64, device=hist.device).set_(
+            hist.untyped_storage(), 0, (hist.numel() + ok.numel(),))
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        return hist, ok
     buf = torch.cat([hist.reshape(-1), ok.reshape(-1)])
     dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return buf[: c * r1].view(c, r1), buf[c * r1:]

@@ -223,11 +223,17 @@ class WindowEvaluator:
         torch = self._torch
         lib = nat.load_library()
         c = th.shape[0]
-        out = torch.empty((3, c), dtype=torch.float64, device="cuda")  # one allocation per call
-        acc = None if counts_only else out[0]
-        sav = None if counts_only else out[1]
-        ok = out[2].view(torch.int64)
-        hist = torch.empty((c, self.r + 1), dtype=torch.int64, device="cuda") if want_hist else None
+        if counts_only:
+            # hist then ok in ONE int64 buffer: a cross-rank all-reduce sums it in place
+            buf = torch.empty(c * (self.r + 2), dtype=torch.int64, device="cuda")
+            acc = sav = None
+            hist = buf[: c * (self.r + 1)].view(c, self.r + 1)
+            ok = buf[c * (self.r + 1):]
+        else:
+            out = torch.empty((3, c), dtype=torch.float64, device="cuda")  # one allocation per call
+            acc, sav = out[0], out[1]
+            ok = out[2].view(torch.int64)
+            hist = torch.empty((c, self.r + 1), dtype=torch.int64, device="cuda") if want_hist else None
         nat.check(lib.ee_eval_thresholds(
             nat.workspace(), nat.ptr(self.d_scores), self.d_bits.data_ptr(), self.n, self.r,
             self.serve.ctypes.data, float(self.vanilla_ms), th.ctypes.data if th.size else None,
