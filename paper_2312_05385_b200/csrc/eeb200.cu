@@ -516,6 +516,13 @@ struct ee_workspace {
   size_t d_in_cap = 0;
   uint32_t* h_bits = nullptr;
   size_t h_bits_cap = 0;
+  // pageable-input staging: per copy thread, two pinned chunks + a stream + events
+  struct Stager {
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    cudaStream_t stream = nullptr;
+  };
+  std::vector<Stager> stagers;
   long long* d_diag_acc = nullptr;
   bool diag_acc_dirty = true;
   unsigned long long* d_diag_trace = nullptr;  // set by ee_diag_trace (profiling)
@@ -706,6 +713,13 @@ int ee_workspace_destroy(ee_workspace* ws) {
   for (auto& m : ws->marks) cudaEventDestroy(m.a), cudaEventDestroy(m.b);
   for (auto e : ws->event_pool) cudaEventDestroy(e);
   if (ws->h_bits) cudaFreeHost(ws->h_bits);
+  for (auto& sg : ws->stagers) {
+    for (int i = 0; i < 2; ++i) {
+      if (sg.buf[i]) cudaFreeHost(sg.buf[i]);
+      if (sg.done[i]) cudaEventDestroy(sg.done[i]);
+    }
+    if (sg.stream) cudaStreamDestroy(sg.stream);
+  }
   if (ws->h_stage) cudaFreeHost(ws->h_stage);
   if (ws->staged) cudaEventDestroy(ws->staged);
   delete ws;
@@ -1354,6 +1368,78 @@ int ee_pack_correct_host(const double* h_correct_ext, int64_t n, int32_t r1, uin
   return EE_OK;
 }
 
+// H2D of a host buffer. Pinned (page-locked or registered) memory goes as one
+// async copy. Pageable memory would otherwise be staged by the driver at a
+// fraction of PCIe speed, so it is streamed through kStagers copy threads,
+// each double-buffering 8 MiB pinned chunks on its own stream; `st` then
+// waits on every stager's last copy.
+static constexpr int kStagers = 4;
+static constexpr size_t kChunk = 8u << 20;
+
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, p) == cudaSuccess &&
+                      (pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeManaged);
+  cudaGetLastError();  // clear a failed query on plain pageable memory
+  return pinned;
+}
+
+static cudaError_t copy_to_device(ee_workspace* ws, void* dst, const void* src, size_t bytes,
+                                  cudaStream_t st) {
+  if (bytes <= kChunk || host_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  if (ws->stagers.empty()) {
+    ws->stagers.resize(kStagers);
+    for (auto& sg : ws->stagers) {
+      for (int i = 0; i < 2; ++i) {
+        cudaError_t e = cudaHostAlloc(&sg.buf[i], kChunk, cudaHostAllocDefault);
+        if (e != cudaSuccess) return e;
+        e = cudaEventCreateWithFlags(&sg.done[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+      }
+      cudaError_t e = cudaStreamCreateWithFlags(&sg.stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  // the stagers' streams must not overtake work already queued on st (dst reuse)
+  cudaEvent_t ready;
+  cudaError_t e0 = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e0 != cudaSuccess) return e0;
+  cudaEventRecord(ready, st);
+  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  std::vector<cudaError_t> errs(kStagers, cudaSuccess);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < kStagers; ++t)
+    pool.emplace_back([&, t] {
+      auto& sg = ws->stagers[t];
+      cudaStreamWaitEvent(sg.stream, ready, 0);
+      int use = 0;
+      for (size_t c = (size_t)t; c < nchunks; c += kStagers, use ^= 1) {
+        const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+        cudaEventSynchronize(sg.done[use]);  // this pinned chunk's previous copy has landed
+        std::memcpy(sg.buf[use], static_cast<const char*>(src) + off, len);
+        cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, sg.buf[use], len,
+                                        cudaMemcpyHostToDevice, sg.stream);
+        if (e == cudaSuccess) e = cudaEventRecord(sg.done[use], sg.stream);
+        if (e != cudaSuccess) {
+          errs[t] = e;
+          return;
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  cudaEventDestroy(ready);
+  for (int t = 0; t < kStagers; ++t) {
+    if (errs[t] != cudaSuccess) return errs[t];
+    cudaEvent_t fin;
+    cudaError_t e = cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    cudaEventRecord(fin, ws->stagers[t].stream);
+    cudaStreamWaitEvent(st, fin, 0);
+    cudaEventDestroy(fin);
+  }
+  return cudaSuccess;
+}
+
 int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
                             int64_t n, int32_t r, const double* h_serve, double vanilla,
                             const double* h_th, int64_t c, int32_t mode, double* h_acc,
@@ -1392,12 +1478,18 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
   // on worker threads while the scores stream to the device
   int prc = EE_OK;
   std::string perr;
+  // leave kStagers cores to the score copy threads when the scores are pageable
+  const bool staged = n > 0 && r > 0 && (size_t)n * r * 8 > kChunk && !host_pinned(h_scores);
+  const int pack_threads =
+      n_threads > 0 ? n_threads
+      : staged      ? std::max(1, (int)std::thread::hardware_concurrency() - kStagers)
+                    : 0;
   std::thread packer([&] {
-    prc = ee_pack_correct_host(h_correct_ext, n, r + 1, ws->h_bits, n_threads);
+    prc = ee_pack_correct_host(h_correct_ext, n, r + 1, ws->h_bits, pack_threads);
     if (prc) perr = g_err;  // thread-local
   });
   cudaError_t ce = cudaSuccess;
-  if (n > 0 && r > 0) ce = cudaMemcpyAsync(d_scores, h_scores, (size_t)n * r * 8, cudaMemcpyHostToDevice, st);
+  if (n > 0 && r > 0) ce = copy_to_device(ws, d_scores, h_scores, (size_t)n * r * 8, st);
   packer.join();
   if (prc) {
     cudaStreamSynchronize(st);  // the caller's buffers stay in use until the copy is done
