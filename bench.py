@@ -488,7 +488,8 @@ def other_configs():
     for key, cmd, t in (("ee_inference", ["tools/bench_ee.py"], 420),
                         ("generative", ["tools/bench_gen.py"], 300),
                         ("serving_loop", ["tools/bench_serve_live.py"], 300),
-                        ("candidate_families", ["tools/bench_families.py"], 300)):
+                        ("candidate_families", ["tools/bench_families.py"], 300),
+                        ("tune", ["tools/bench_tune.py"], 300)):
         try:
             r = subprocess.run([sys.executable, os.path.join(ROOT, *cmd[0].split("/"))] + cmd[1:],
                                capture_output=True, text=True, timeout=t, cwd=ROOT)

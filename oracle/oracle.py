@@ -155,8 +155,12 @@ def brute_window(records, active, profile, k: int = 1):
     return ok / n, sav / n, {p: c / n for p, c in exits.items()}
 
 
-def tune(records, ramps, profile, budget=0.01, init_step=0.1, min_step=0.01, k=1):
-    """Algorithm 1 over the C oracle kernel; returns (thresholds, sav, acc, rounds, evals, trace)."""
+def tune(records, ramps, profile, budget=0.01, init_step=0.1, min_step=0.01, k=1, kernel=None):
+    """Algorithm 1 (tuner.py:97-171) over the C oracle kernel, or over `kernel`
+    (any module with the `_kernels` eval_thresholds signature, e.g. the
+    reference's compiled Cython backend); returns (thresholds, sav, acc,
+    rounds, evals, trace)."""
+    eval_thresholds_ = kernel.eval_thresholds if kernel is not None else eval_thresholds
     if not ramps:
         return [], 0.0, 1.0, 0, 0, ()
     scores, cext = pack_window(records, ramps, k)
@@ -166,7 +170,7 @@ def tune(records, ramps, profile, budget=0.01, init_step=0.1, min_step=0.01, k=1
     th = np.zeros(r)
     steps = np.full(r, init_step)
     floor = 1.0 - budget
-    a, s = eval_thresholds(scores, cext, serve, vanilla, th.reshape(1, r))
+    a, s = eval_thresholds_(scores, cext, serve, vanilla, th.reshape(1, r))
     acc_cur, sav_cur = float(a[0]), float(s[0])
     rounds, evals, trace = 0, 1, [tuple(steps)]
     while True:
@@ -177,7 +181,7 @@ def tune(records, ramps, profile, budget=0.01, init_step=0.1, min_step=0.01, k=1
         rows = np.repeat(th.reshape(1, r), len(elig), axis=0)
         for p, i in enumerate(elig):
             rows[p, i] = min(1.0, th[i] + steps[i])
-        accs, savs = eval_thresholds(scores, cext, serve, vanilla, rows)
+        accs, savs = eval_thresholds_(scores, cext, serve, vanilla, rows)
         evals += len(elig)
         best, best_key, viol = None, None, []
         for p, i in enumerate(elig):

@@ -1,6 +1,8 @@
-"""Config-1 style threshold tuning: tune() over a 1000-record x 6-ramp window,
-GPU (device-resident Algorithm 1, and host loop) vs the reference CPU path
-(oracle restatement over the compiled reference kernel). Prints one JSON line."""
+"""Algorithm 1 (tuner.tune, §8 A7): the device-resident hill climb vs the
+reference's CPU path (Algorithm 1 over the reference's compiled Cython kernel,
+oracle/_ref, packing the window per call as engine.WindowEvaluator does), on
+the default 128-record tuning history and config 1's 1,000-record window.
+Thresholds must agree bit for bit. One JSON line."""
 import json
 import os
 import sys
@@ -20,31 +22,29 @@ from paper_2312_05385_b200.tuner import TunerParams, tune
 prof = synth.config4_profile()
 s13 = find_feasible_sites(prof)
 curve = {x.position: 0.5 + (0.95 - 0.5) * i / 11 for i, x in enumerate(s13)}
-w = synthesize_workload(prof, 1000, 0.7, curve, seed=42, miscalibration=0.1)
 ramps = [s13[0], s13[2], s13[4], s13[6], s13[8], s13[10]]
-recs = list(w.records)
-ev = WindowEvaluator(recs, ramps, prof)
-out = {}
-for name, dev in (("device_loop", True), ("host_loop", False)):
-    for _ in range(3):
-        res = tune(recs, ramps, TunerParams(), prof, evaluator=ev, device_loop=dev)
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(20):
-        t0 = time.perf_counter()
-        res = tune(recs, ramps, TunerParams(), prof, evaluator=ev, device_loop=dev)
-        ts.append(time.perf_counter() - t0)
-    out[name] = {"ms_median": 1e3 * float(np.median(ts)), "rounds": res.rounds, "evals": res.evals}
-# reference CPU path: Algorithm 1 over the compiled reference kernel (oracle/_ref) on a packed window
 ref = O.reference_kernel()
-scores, cext = O.pack_window(recs, ramps)
-serve = O.serve_table(ramps, prof, 1)
-van = prof.model_latency(1)
-kern = ref if ref is not None else O
-def ref_tune():
-    return O.tune(recs, ramps, prof)
-ts = []
-for _ in range(10):
-    t0 = time.perf_counter(); ref_tune(); ts.append(time.perf_counter() - t0)
-out["cpu_oracle_tune_ms_median_incl_packing"] = 1e3 * float(np.median(ts))
+out = {"cpu_kind": "reference (oracle/_ref Cython)" if ref is not None else "port (C oracle)"}
+for n in (128, 1000):
+    recs = list(synthesize_workload(prof, n, 0.7, curve, seed=42, miscalibration=0.1).records)
+
+    def ours():
+        return tune(recs, ramps, TunerParams(), prof)  # packs + uploads the window, one launch
+
+    ev = WindowEvaluator(recs, ramps, prof)
+    for _ in range(3):
+        res = ours()
+    torch.cuda.synchronize()
+    ts, tr = [], []
+    for _ in range(20):
+        t0 = time.perf_counter(); res = ours(); ts.append(time.perf_counter() - t0)
+        t0 = time.perf_counter(); tune(recs, ramps, TunerParams(), prof, evaluator=ev); tr.append(time.perf_counter() - t0)
+    tc = []
+    for _ in range(10):
+        t0 = time.perf_counter(); th, *_ = O.tune(recs, ramps, prof, kernel=ref); tc.append(time.perf_counter() - t0)
+    out[f"n{n}"] = {"gpu_tune_ms": 1e3 * float(np.median(ts)),
+                    "gpu_tune_resident_window_ms": 1e3 * float(np.median(tr)),
+                    "cpu_reference_tune_ms": 1e3 * float(np.median(tc)),
+                    "rounds": res.rounds, "evals": res.evals,
+                    "bit_identical_thresholds": res.threshold_vector(ramps) == th}
 print(json.dumps(out))
