@@ -42,6 +42,11 @@ extern "C" {
 #define EE_MODE_AUTO 0  /* exact below EE_EXACT_N_MAX samples, histogram above */
 #define EE_MODE_EXACT 1 /* per-candidate in-order fp64 sums: bit-identical to _exitcore.pyx:43-55 */
 #define EE_MODE_HIST 2  /* integer exit-site histograms; acc exact, sav exactly rounded */
+/* OR-ed into `mode`: scores/bits are immutable device buffers (a resident window
+ * whose producers completed before this call). The diagonal sweep may then start
+ * streaming them while the previous sweep on the stream finishes (programmatic
+ * dependent launch); its own side effects still wait for that sweep. */
+#define EE_MODE_FLAG_RESIDENT 0x100
 #define EE_EXACT_N_MAX 4096
 
 #define EE_MAX_RAMPS 31

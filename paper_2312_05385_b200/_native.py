@@ -25,6 +25,7 @@ EE_ERR_RAMPS = -4
 MODE_AUTO = 0
 MODE_EXACT = 1
 MODE_HIST = 2
+MODE_FLAG_RESIDENT = 0x100  # EE_MODE_FLAG_RESIDENT: immutable resident window
 MODES = {"auto": MODE_AUTO, "exact": MODE_EXACT, "hist": MODE_HIST}
 EXACT_N_MAX = 4096
 TUNE_N_MAX = 65536
@@ -161,8 +162,9 @@ def workspace() -> ctypes.c_void_p:
     return ws.handle
 
 
-def set_diag_version(version: int = 2) -> None:
-    """2 = k_diag2 where it applies (default), 1 = the first diagonal kernel only."""
+def set_diag_version(version: int = 4) -> None:
+    """4 = k_diag3 where it applies, else k_diag2 (default); 2 = k_diag2 where it
+    applies; 1 = the first diagonal kernel only."""
     check(load_library().ee_workspace_set_diag_version(workspace(), int(version)))
 
 

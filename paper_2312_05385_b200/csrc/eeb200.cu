@@ -467,6 +467,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 }  // namespace
 #include "sweep_diag.cuh"
 #include "sweep_diag2.cuh"
+#include "sweep_diag3.cuh"
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
 #include "gemm_tc.cuh"
@@ -507,7 +508,9 @@ struct ee_workspace {
   // this workspace launches, on the launching stream
   bool profiling = false;
   bool allow_special = true;  // family-specialised sweeps (diagonal); off = generic SWAR path
-  int diag_version = 2;       // 2 = k_diag2 where it applies, 1 = k_diag only (A/B, tests)
+  bool resident = false;      // current call carries EE_MODE_FLAG_RESIDENT (set under mu)
+  int diag_version = 4;       // 4 = k_diag3 where it applies, else k_diag2; 2 = k_diag2;
+                              // 3 = k_diag2 with branched updates; 1 = k_diag only (A/B, tests)
   // k_diag2 global accumulator: zero between launches (each launch leaves it
   // zeroed), so calls on one workspace must be stream-ordered
   // inputs staged by ee_eval_thresholds_host: device scores/bits/outputs and
@@ -1006,23 +1009,56 @@ static int eval_diag(ee_workspace* ws, const double* d_scores, const uint32_t* d
 // envelope (odd or > 16 ramps, misaligned scores, > 127 distinct thresholds,
 // no single-threshold bin grid) so the caller runs k_diag instead.
 }  // extern "C"
+// Grid of the diagonal sweeps: one 1024-thread CTA per SM. Resident windows
+// leave one SM to the previous sweep's finalising CTA, so a stream of sweeps
+// overlaps each tail with the next sweep's loop.
+static unsigned diag_grid(const ee_workspace* ws, int64_t n) {
+  const int64_t nchunks = ceil_div(n, 32);
+  const int sms = ws->resident ? std::max(1, sm_count() - 1) : sm_count();
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(nchunks, diag2::WARPS)));
+}
+template <class K>
+static cudaError_t launch_diag_kernel(K k, const char* name, int smem, bool& attr_set,
+                                      const diag2::Params& p, int64_t n, cudaStream_t st,
+                                      ee_workspace* ws) {
+  if (!attr_set) {  // once per instantiation (a driver call)
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const unsigned grid = diag_grid(ws, n);
+  ProfScope ps(ws, st, name);  // events bracket the launch itself
+  if (!ws->resident) {
+    k<<<grid, diag2::THREADS, smem, st>>>(p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(diag2::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, p);
+}
 template <int R>
 static cudaError_t launch_diag2(const diag2::Params& p, int64_t n, int upd, cudaStream_t st,
                                 ee_workspace* ws) {
-  auto k = upd == 1 ? diag2::k_diag2<R, 1> : diag2::k_diag2<R, 0>;
-  constexpr int smem = diag2::smem_bytes<R>();
-  static bool attr_set[2] = {false, false};  // once per instantiation (a driver call)
-  if (!attr_set[upd]) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set[upd] = true;
-  }
-  const int64_t nchunks = ceil_div(n, 32);
-  const unsigned grid =
-      (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), ceil_div(nchunks, diag2::WARPS)));
-  ProfScope ps(ws, st, "k_diag2");  // events bracket the launch itself
-  k<<<grid, diag2::THREADS, smem, st>>>(p);
-  return cudaGetLastError();
+  static bool attr_set[2] = {false, false};
+  return upd == 1 ? launch_diag_kernel(diag2::k_diag2<R, 1>, "k_diag2", diag2::smem_bytes<R>(),
+                                       attr_set[1], p, n, st, ws)
+                  : launch_diag_kernel(diag2::k_diag2<R, 0>, "k_diag2", diag2::smem_bytes<R>(),
+                                       attr_set[0], p, n, st, ws);
+}
+template <int R>
+static cudaError_t launch_diag3(const diag2::Params& p, int64_t n, cudaStream_t st,
+                                ee_workspace* ws) {
+  static bool attr_set = false;
+  return launch_diag_kernel(diag3::k_diag3<R>, "k_diag3", diag3::smem_bytes<R>(), attr_set, p, n,
+                            st, ws);
 }
 extern "C" {
 
@@ -1062,7 +1098,7 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
   for (int k = 0, lo = 0; k < diag2::NB; ++k) {
     while (lo < m && bu[lo] < (unsigned)k) ++lo;
     const int cmp = (lo < m && bu[lo] == (unsigned)k) ? lo : diag2::SENT;
-    p.tab[k] = (uint32_t)lo | ((uint32_t)(cmp * 8) << 16);
+    p.tab[k] = (uint32_t)lo | ((uint32_t)(cmp * diag2::SU_STRIDE) << 16);
   }
   if (!ws->d_diag_acc) {
     EE_CUDA(cudaMalloc(&ws->d_diag_acc, (size_t)diag2::ACC_WORDS * 8));
@@ -1106,7 +1142,21 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
   }
   cudaError_t e;
   const int upd = ws->diag_version == 3 ? 0 : 1;
-  {
+  // k_diag3 (lane-private cumulative counters) where its envelope holds
+  const bool v3 = ws->diag_version >= 4 && m <= diag3::MAX_M &&
+                  ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n) * diag2::WARPS) <= diag3::MAX_ITERS;
+  if (v3) {
+    switch (r) {
+      case 2: e = launch_diag3<2>(p, n, st, ws); break;
+      case 4: e = launch_diag3<4>(p, n, st, ws); break;
+      case 6: e = launch_diag3<6>(p, n, st, ws); break;
+      case 8: e = launch_diag3<8>(p, n, st, ws); break;
+      case 10: e = launch_diag3<10>(p, n, st, ws); break;
+      case 12: e = launch_diag3<12>(p, n, st, ws); break;
+      case 14: e = launch_diag3<14>(p, n, st, ws); break;
+      default: e = launch_diag3<16>(p, n, st, ws); break;
+    }
+  } else {
     switch (r) {
       case 2: e = launch_diag2<2>(p, n, upd, st, ws); break;
       case 4: e = launch_diag2<4>(p, n, upd, st, ws); break;
@@ -1294,14 +1344,18 @@ int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t*
   if (c == 0) return EE_OK;
   if (!h_serve) return fail(EE_ERR_ARG, "null serve table");
   if (!d_acc != !d_sav) return fail(EE_ERR_ARG, "acc and sav must both be given or both be null");
-  if (!d_acc && (mode != EE_MODE_HIST || !d_hist || !d_ok))
+  if (!d_acc && ((mode & ~EE_MODE_FLAG_RESIDENT) != EE_MODE_HIST || !d_hist || !d_ok))
     return fail(EE_ERR_ARG, "counts-only evaluation needs HIST mode and d_hist/d_ok");
   if (n > 0 && (!d_scores && r > 0)) return fail(EE_ERR_ARG, "null scores");
   if (n > 0 && !d_bits) return fail(EE_ERR_ARG, "null correctness bits");
   if (r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
   std::lock_guard<std::mutex> lock(ws->mu);
-  return eval_dispatch(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, mode, d_hist, d_ok,
-                       d_acc, d_sav, (cudaStream_t)stream);
+  ws->resident = (mode & EE_MODE_FLAG_RESIDENT) != 0;
+  const int rc = eval_dispatch(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c,
+                               mode & ~EE_MODE_FLAG_RESIDENT, d_hist, d_ok, d_acc, d_sav,
+                               (cudaStream_t)stream);
+  ws->resident = false;
+  return rc;
 }
 
 // correct_ext f64 [n, r1] -> bit rows on the host, rows [i0, i1); *bad |= any
@@ -1571,7 +1625,7 @@ int ee_workspace_set_special(ee_workspace* ws, int32_t on) {
 
 int ee_workspace_set_diag_version(ee_workspace* ws, int32_t version) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
-  if (version < 1 || version > 3) return fail(EE_ERR_ARG, "diagonal kernel version must be 1, 2 or 3");
+  if (version < 1 || version > 4) return fail(EE_ERR_ARG, "diagonal kernel version must be 1..4");
   std::lock_guard<std::mutex> lock(ws->mu);
   ws->diag_version = version;
   return EE_OK;

@@ -49,11 +49,17 @@ constexpr int ROWB = 2 * W + 32;  // ints per site row: [p][correct] + one dummy
 constexpr int CORR_IDX = (RMAX + 1) * W;
 constexpr int ACC_WORDS = CORR_IDX + 2;
 constexpr int SENT = MAX_M;                  // su[SENT] is a NaN sentinel (never <= x)
+// Thresholds are replicated 16x (entry t, copy q at byte 128 t + 8 q) and lane l
+// reads copy l % 16: a half-warp's 64-bit loads then hit 16 distinct bank pairs
+// whatever thresholds its lanes need (one copy measured ~50 conflict wavefronts
+// per warp-chunk, the largest item on the shared-memory pipe).
+constexpr int SU_REP = 16;
+constexpr int SU_STRIDE = SU_REP * 8;  // bytes per threshold
 
 // dynamic shared memory layout (compile-time offsets -> immediate addressing)
 constexpr int OFF_TAB = 0;                       // u32 [NB][32]: lo | (8*cmp) << 16
-constexpr int OFF_SU = OFF_TAB + NB * 32 * 4;    // f64 [MAX_M + 1]
-constexpr int OFF_KEY = OFF_SU + (MAX_M + 1) * 8;  // u8 [WARPS][32 R]
+constexpr int OFF_SU = OFF_TAB + NB * 32 * 4;    // f64 [MAX_M + 1][SU_REP]
+constexpr int OFF_KEY = OFF_SU + (MAX_M + 1) * SU_STRIDE;  // u8 [WARPS][32 R]
 template <int R>
 __host__ __device__ constexpr int off_d() { return OFF_KEY + WARPS * 32 * R; }
 template <int R>
@@ -86,7 +92,7 @@ struct Params {
   double vanilla;
   double serve[RMAX + 1];
   double u[MAX_M + 1];
-  uint32_t tab[NB];  // bin k: lo = #{u < bin k} | (8 * index of the bin's own threshold, or SENT) << 16
+  uint32_t tab[NB];  // bin k: lo = #{u < bin k} | (SU_STRIDE * index of the bin's own threshold, or SENT) << 16
   unsigned char pos[MAX_POS];  // position of candidate c in u, 255 = NaN row
   unsigned long long* trace;   // optional: per-CTA %globaltimer stamps [grid][6] (profiling)
 };
@@ -197,8 +203,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
   load(ch);  // first HBM round trip overlaps the prologue
 
   // ---- prologue: thresholds, the replicated bin table (built on the host), zeroed counters
-  for (int i = warp; i <= MAX_M; i += WARPS)  // warp-uniform parameter reads (broadcast LDC)
-    if (lane == 0) su[i] = i < m ? P.u[i] : __longlong_as_double(0x7ff8000000000000LL);
+  for (int i = tid; i < (MAX_M + 1) * SU_REP; i += THREADS) {
+    const int t = i / SU_REP;
+    su[i] = t < m ? P.u[t] : __longlong_as_double(0x7ff8000000000000LL);
+  }
   for (int i = tid; i < DSTRIDE; i += THREADS) sD[i] = 0;
 #pragma unroll
   for (int q = tid; q < NB * 32; q += THREADS) stab[q] = P.tab[q >> 5];  // warp-uniform LDC
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
   const double pa = P.a, pc0 = P.c0;
   const uint32_t smb = (uint32_t)__cvta_generic_to_shared(sm);
   const uint32_t tb = smb + OFF_TAB + (uint32_t)lane * 4;  // this lane's bank of the table
-  const uint32_t sub = smb + OFF_SU;
+  const uint32_t sub = smb + OFF_SU + (uint32_t)(lane % SU_REP) * 8;  // this lane's copy
   const uint32_t dB = smb + OFF_D;  // 16-byte aligned: bit 2 is free for the correct column
   const uint32_t dummy = dB + 2 * W * 4 + (uint32_t)lane * 4;  // + row offset
   // key(x) = #{u_k <= x} (7 bits; garbage above bit 7 is dropped by the byte pack)
@@ -286,6 +294,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
 #pragma unroll
   for (int o = 16; o; o >>= 1) corr += __shfl_xor_sync(FULL, corr, o);
   if (P.trace && lane == 0) atomicMax(P.trace + blockIdx.x * 6 + 2, gtimer());  // last warp out
+  // Back-to-back sweeps over resident windows (EE_MODE_FLAG_RESIDENT): the next
+  // sweep on the stream may be scheduled once every CTA has left its loop, so
+  // its CTAs take the SMs this grid frees and stream their window while our last
+  // CTA finalises. Everything before this point only reads immutable inputs;
+  // every global side effect below sits after griddepcontrol.wait (= the
+  // previous sweep has fully completed and its memory is visible). Both are
+  // no-ops for a normal launch.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __syncthreads();
   // per-CTA counts, in place: prefix over p of this CTA's difference rows
   // (non-negative for sites < r; site r holds -Z's partial, only -1 events)
@@ -317,6 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag2(const __grid_constant__ Pa
   if (tid == 0) s_corr = 0;
   __syncthreads();
   if (lane == 0 && corr) atomicAdd(&s_corr, (unsigned long long)corr);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous sweep done: gD/done/outputs are ours
   if (tid == 0) s_last = atomicAdd(P.done, 1u) == gridDim.x - 1;  // loops finished
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 3] = gtimer();
   __syncthreads();

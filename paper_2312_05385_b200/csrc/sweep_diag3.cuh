@@ -1,0 +1,358 @@
+// sweep_diag3.cuh — k_diag3: the diagonal-family sweep with lane-private
+// cumulative counters. Same inputs, planning (diag2::Params) and outputs as
+// k_diag2; what changes is how a sample is counted.
+//
+// With b_j = min(b_{j-1}, key_j) (b_{-1} = m) the sample exits at site j for
+// positions b_j <= p < b_{j-1}. Because b is non-increasing,
+//   1[b_j <= p < b_{j-1}] = 1[b_j <= p] - 1[b_{j-1} <= p],
+// so with F_j(p) = #{i : b_j(i) <= p} (a cumulative count of b_j)
+//   hist_j(p) = F_j(p) - F_{j-1}(p),   hist_r(p) = n - F_{r-1}(p),
+// and, collecting the correctness bits c_j by the same identity,
+//   ok(p) = #{c_r = 1} + sum_j #{i : b_j(i) <= p} weighted by (c_j - c_{j+1}).
+// Every (sample, ramp) is therefore ONE shared-memory update at cell b_j of
+// ramp j: +1 in the low half-word (the count) and c_j - c_{j+1} in the high
+// half-word. The count never reaches 2^16, so nothing carries out of the low
+// half and the high half holds the exact signed sum modulo 2^16 (|sum| < 2^15).
+// k_diag2 needs two updates per drop and its updates collide in shared-memory
+// banks (ncu: 2.8 wavefronts per ATOMS, 69 of the ~120 wavefronts per warp-chunk);
+// here every lane owns its own copy of each cell (cell p, lane l at word
+// 32 p + l, i.e. bank l), so each update instruction is exactly one wavefront
+// and no lane ever waits for a dummy or a branch.
+//
+// Envelope (else the host runs k_diag2): m <= 64 distinct thresholds (cells
+// 0..m, cell m is the "never exits" sink), and at most 32767 samples per
+// lane copy per CTA (n <= ~154M at 147 CTAs) so the half-words stay exact.
+#pragma once
+
+namespace diag3 {
+
+using diag2::Params;
+constexpr int THREADS = diag2::THREADS;
+constexpr int WARPS = diag2::WARPS;
+constexpr int MAX_M = 64;
+constexpr int CELLS = MAX_M + 1;          // positions 0..m (m = sink)
+constexpr int ROWC = CELLS * 32 * 4;      // bytes per ramp: [cell][lane] u32
+constexpr int MAX_ITERS = 1023;           // chunk iterations per warp (32 warps x 1023 < 2^15)
+constexpr int OFF_TAB = diag2::OFF_TAB;
+constexpr int OFF_SU = diag2::OFF_SU;
+constexpr int OFF_KEY = diag2::OFF_KEY;
+template <int R>
+__host__ __device__ constexpr int off_c() { return OFF_KEY + WARPS * 32 * R; }
+template <int R>
+__host__ __device__ constexpr int smem_bytes() { return off_c<R>() + R * ROWC; }
+// after the loop: per-CTA F [R][64] (i32) in the key buffer
+// last CTA: finalisation scratch over the cell rows
+template <int R>
+__host__ __device__ constexpr int fin_bytes() {
+  return 3 * (R + 1) * CELLS * 8 + 3 * CELLS * 8;
+}
+
+template <int R>
+__global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Params P) {
+  static_assert(R % 2 == 0 && R >= 2 && R <= diag2::RMAX, "even R only");
+  static_assert(fin_bytes<R>() <= R * ROWC, "finalisation scratch fits the cell rows");
+  static_assert(R * MAX_M * 4 <= WARPS * 32 * R, "per-CTA sums fit the key buffer");
+  constexpr int NW = (R + 3) / 4;
+  constexpr int OFF_C = off_c<R>();
+  using diag2::lds_f64;
+  using diag2::lds_u32;
+  using diag2::Unroll;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int m = P.m;
+  uint32_t* stab = reinterpret_cast<uint32_t*>(sm + OFF_TAB);
+  double* su = reinterpret_cast<double*>(sm + OFF_SU);
+  unsigned char* skey = sm + OFF_KEY;
+  uint32_t* cells = reinterpret_cast<uint32_t*>(sm + OFF_C);
+  __shared__ unsigned s_last;
+  __shared__ unsigned long long s_corr;
+  __shared__ int s_osum[MAX_M];  // sum over ramps of the O cells, per position
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+
+  const int64_t n = P.n;
+  const int64_t nchunks = (n + 31) >> 5;
+  const int64_t G = (int64_t)gridDim.x * WARPS;
+  int64_t ch = (int64_t)blockIdx.x * WARPS + warp;
+  double2 v[R / 2];
+  uint32_t cb = 0;
+  auto load = [&](int64_t c) {
+    if (c >= nchunks) return;
+    const int64_t s0 = c << 5;
+    const double2* src = reinterpret_cast<const double2*>(P.s + s0 * R);
+    if (s0 + 32 <= n) {
+#pragma unroll
+      for (int k = 0; k < R / 2; ++k) v[k] = __ldcs(src + k * 32 + lane);
+      cb = __ldcs(P.bits + s0 + lane);
+    } else {
+      const int64_t npairs = (n - s0) * (R / 2);
+#pragma unroll
+      for (int k = 0; k < R / 2; ++k) {
+        const int t = k * 32 + lane;
+        v[k] = t < npairs ? __ldcs(src + t) : make_double2(INF, INF);  // key m: the sink
+      }
+      cb = s0 + lane < n ? __ldcs(P.bits + s0 + lane) : 0u;
+    }
+  };
+  if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 0] = diag2::gtimer();
+  load(ch);  // first HBM round trip overlaps the prologue
+
+  // ---- prologue (vector stores): replicated bin table, replicated thresholds, biased cells
+  {
+    uint4* t4 = reinterpret_cast<uint4*>(stab);
+    for (int q = tid; q < diag2::NB * 8; q += THREADS) {  // 8 uint4 per bin (32 copies)
+      const uint32_t e = P.tab[q >> 3];
+      t4[q] = make_uint4(e, e, e, e);
+    }
+    double2* s2 = reinterpret_cast<double2*>(su);
+    for (int q = tid; q < (diag2::MAX_M + 1) * diag2::SU_REP / 2; q += THREADS) {
+      const int t = q / (diag2::SU_REP / 2);
+      const double x = t < m ? P.u[t] : __longlong_as_double(0x7ff8000000000000LL);
+      s2[q] = make_double2(x, x);
+    }
+    uint4* c4 = reinterpret_cast<uint4*>(cells);
+    const int per_ramp = (m + 1) * 8;  // uint4 per ramp row in use (cells 0..m)
+    for (int q = tid; q < R * per_ramp; q += THREADS) {
+      const int j = q / per_ramp;
+      c4[j * CELLS * 8 + (q - j * per_ramp)] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (tid < MAX_M) s_osum[tid] = 0;
+    if (tid == 0) s_corr = 0;
+  }
+  __syncthreads();
+
+  const double pa = P.a, pc0 = P.c0;
+  const uint32_t smb = (uint32_t)__cvta_generic_to_shared(sm);
+  const uint32_t tb = smb + OFF_TAB + (uint32_t)lane * 4;
+  const uint32_t sub = smb + OFF_SU + (uint32_t)(lane % diag2::SU_REP) * 8;
+  const uint32_t cB = smb + OFF_C + (uint32_t)lane * 4;  // this lane's copy of every cell
+  auto keyof = [&](double x) -> uint32_t {
+    uint32_t e = lds_u32(tb + diag2::bin_of(x, pa, pc0) * 128u);
+    const double t = lds_f64(sub + (e >> 16));
+    asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+        : "+r"(e)
+        : "d"(t), "d"(x));
+    return e;
+  };
+
+  unsigned char* kb = skey + warp * 32 * R;
+  unsigned corr = 0;
+  if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 1] = diag2::gtimer();
+  for (; ch < nchunks; ch += G) {
+    __syncwarp();  // previous chunk's key reads are done
+    // Each pair's registers are refilled with the next chunk as soon as its two
+    // keys are taken, so the next chunk's loads leave during the keying (ncu:
+    // the top-of-loop wait on the loads was the largest stall).
+    const int64_t nx = ch + G;
+    const int64_t s1 = nx << 5;
+    const double2* src = reinterpret_cast<const double2*>(P.s + s1 * R);
+    const int64_t npairs = nx < nchunks ? (n - s1) * (R / 2) : 0;  // valid pairs of the next chunk
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      const uint32_t k0 = keyof(v[k].x), k1 = keyof(v[k].y);
+      *reinterpret_cast<unsigned short*>(kb + 2 * (k * 32 + lane)) =
+          (unsigned short)__byte_perm(k0, k1, 0x0040);
+      const int t = k * 32 + lane;
+      if (npairs >= 32 * (R / 2))
+        v[k] = __ldcs(src + t);
+      else if (npairs > 0)
+        v[k] = t < npairs ? __ldcs(src + t) : make_double2(INF, INF);
+    }
+    const uint32_t cbc = cb;
+    if (nx < nchunks) cb = s1 + lane < n ? __ldcs(P.bits + s1 + lane) : 0u;
+    __syncwarp();
+    uint32_t kw[NW];
+    if constexpr (R % 16 == 0) {
+#pragma unroll
+      for (int q = 0; q < NW / 4; ++q) {
+        const uint4 t = reinterpret_cast<const uint4*>(kb + lane * R)[q];
+        kw[4 * q] = t.x, kw[4 * q + 1] = t.y, kw[4 * q + 2] = t.z, kw[4 * q + 3] = t.w;
+      }
+    } else if constexpr (R % 8 == 0) {
+#pragma unroll
+      for (int q = 0; q < NW / 2; ++q) {
+        const uint2 t = reinterpret_cast<const uint2*>(kb + lane * R)[q];
+        kw[2 * q] = t.x, kw[2 * q + 1] = t.y;
+      }
+    } else if constexpr (R % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < NW; ++q) kw[q] = reinterpret_cast<const uint32_t*>(kb + lane * R)[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < NW; ++q) kw[q] = 0;
+#pragma unroll
+      for (int h = 0; h < R / 2; ++h)
+        kw[h >> 1] |= (uint32_t)reinterpret_cast<const unsigned short*>(kb + lane * R)[h]
+                      << (16 * (h & 1));
+    }
+    // one update per ramp: cell b_j += 1 + ((c_j - c_{j+1}) << 16)
+    uint32_t prev = (uint32_t)m;
+    Unroll<R>::run([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      const uint32_t kj = __byte_perm(kw[j >> 2], 0, 0x4440 | (j & 3));
+      prev = kj < prev ? kj : prev;
+      const uint32_t val = 1u + ((cbc << (16 - j)) & 0x10000u) - ((cbc << (15 - j)) & 0x10000u);
+      diag2::red_shared<j * ROWC>(cB + prev * 128u, (int)val);
+    });
+    corr += (cbc >> R) & 1u;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) corr += __shfl_xor_sync(FULL, corr, o);
+  if (P.trace && lane == 0) atomicMax(P.trace + blockIdx.x * 6 + 2, diag2::gtimer());
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see sweep_diag2.cuh
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous sweep done: gD/done/outputs are ours
+  __syncthreads();
+  // Elect the last CTA now; the round trip overlaps the fold below (the last
+  // thread has no cell to fold unless R * m = 1024).
+  if (tid == THREADS - 1) s_last = atomicAdd(P.done, 1u) == gridDim.x - 1;
+  if (lane == 0 && corr) atomicAdd(&s_corr, (unsigned long long)corr);
+
+  // ---- per-CTA sums: fold the 32 lane copies of each cell (rotated so a warp's
+  // reads hit 32 distinct banks). F stays per ramp; O is summed over ramps. The
+  // prefix over positions is linear, so only the last CTA takes it, on totals.
+  int* cF = reinterpret_cast<int*>(skey);  // F [R][MAX_M] raw per-position counts
+  for (int q = tid; q < R * m; q += THREADS) {
+    const int j = q / m, p = q - j * m;
+    const uint32_t* cell = cells + (j * CELLS + p) * 32;
+    int lo = 0, hi = 0;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t w = cell[(k + lane) & 31];
+      lo += (int)(w & 0xffffu);
+      hi += (int)(short)(w >> 16);  // each copy's high half is its exact signed sum mod 2^16
+    }
+    cF[j * MAX_M + p] = lo;
+    if (hi) atomicAdd(&s_osum[p], hi);
+  }
+  __syncthreads();
+  if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 3] = diag2::gtimer();
+  long long* gD = P.gD;  // [j * W + p]: F_j[p] for j < R, row R: sum_j O_j[p] (two's complement)
+  if (!s_last) {
+    for (int q = tid; q < (R + 1) * m; q += THREADS) {
+      const int j = q / m, p = q - j * m;
+      const long long x = j < R ? (long long)cF[j * MAX_M + p] : (long long)s_osum[p];
+      if (x) atomicAdd(reinterpret_cast<unsigned long long*>(gD + j * diag2::W + p),
+                       (unsigned long long)x);
+    }
+    if (tid == 0 && s_corr)
+      atomicAdd(reinterpret_cast<unsigned long long*>(gD + diag2::CORR_IDX), s_corr);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) atomicAdd(P.done + 1, 1u);
+    return;
+  }
+
+  // ---- the last CTA: wait for the others' merges, fold its own sums in, finalise
+  if (tid == 0) {
+    unsigned v2;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v2) : "l"(P.done + 1) : "memory");
+    } while (v2 < gridDim.x - 1);
+  }
+  __syncthreads();
+  if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 1] = diag2::gtimer();
+  const int M1 = m + 1;
+  long long* hst = reinterpret_cast<long long*>(sm + OFF_C);  // [R+1][M1] (F_j first)
+  long long* okp = hst + (R + 1) * M1;
+  double* prs = reinterpret_cast<double*>(okp + M1);
+  double* pes = prs + (R + 1) * M1;
+  double* accp = pes + (R + 1) * M1;
+  double* savp = accp + M1;
+  __shared__ long long s_corr_all;
+  if (tid == 0) {
+    s_corr_all = (long long)(__ldcg(gD + diag2::CORR_IDX) + s_corr);
+    gD[diag2::CORR_IDX] = 0;
+    P.done[0] = 0u;
+    P.done[1] = 0u;
+  }
+  for (int q = tid; q < (R + 1) * m; q += THREADS) {  // global + own, zero for the next launch
+    const int j = q / m, p = q - j * m;
+    const long long g = __ldcg(gD + j * diag2::W + p);
+    gD[j * diag2::W + p] = 0;
+    hst[j * M1 + p] = g + (j < R ? (long long)cF[j * MAX_M + p] : (long long)s_osum[p]);
+  }
+  __syncthreads();
+  for (int row = warp; row <= R; row += WARPS) {  // inclusive prefix over p < m: F_j(p), O(p)
+    long long* a = hst + row * M1;
+    long long carry = 0;
+    for (int p0 = 0; p0 < m; p0 += 32) {
+      const int p = p0 + lane;
+      long long x = p < m ? a[p] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      x += carry;
+      if (p < m) a[p] = x;
+      carry = __shfl_sync(FULL, x, 31);
+    }
+  }
+  __syncthreads();
+  const long long corrR = s_corr_all;
+  for (int p = tid; p < M1; p += THREADS) {  // F -> histograms, O -> correct counts
+    if (p == m) {  // NaN threshold row: nothing exits
+      for (int j = 0; j < R; ++j) hst[j * M1 + p] = 0;
+      hst[R * M1 + p] = n;
+      okp[p] = corrR;
+      continue;
+    }
+    okp[p] = corrR + hst[R * M1 + p];
+    long long fprev = 0;
+    for (int j = 0; j < R; ++j) {
+      const long long f = hst[j * M1 + p];
+      hst[j * M1 + p] = f - fprev;
+      fprev = f;
+    }
+    hst[R * M1 + p] = n - fprev;
+  }
+  __syncthreads();
+  for (int i = tid; i < (R + 1) * M1; i += THREADS) {  // error-free products
+    const int site = i / M1;
+    const double x = (double)hst[i];
+    const double pr = __dmul_rn(x, P.serve[site]);
+    prs[i] = pr;
+    pes[i] = __fma_rn(x, P.serve[site], -pr);
+  }
+  __syncthreads();
+  for (int p = tid; p < M1; p += THREADS) {  // the ordered TwoSum chain of k_finalize
+    double hi = 0.0, lo = 0.0;
+#pragma unroll
+    for (int site = 0; site <= R; ++site) {
+      double s2, e;
+      two_sum(hi, prs[site * M1 + p], s2, e);
+      hi = s2;
+      lo = __dadd_rn(lo, __dadd_rn(e, pes[site * M1 + p]));
+    }
+    double tot2, e;
+    two_sum(hi, lo, tot2, e);
+    const double dn = (double)n;
+    accp[p] = __ddiv_rn((double)okp[p], dn);
+    savp[p] = __dsub_rn(P.vanilla, __ddiv_rn(tot2, dn));
+  }
+  __syncthreads();
+  auto posof = [&](int64_t c) -> int {
+    const int q = P.C <= diag2::MAX_POS ? P.pos[c] : P.pos_dev[c];
+    return q == 255 ? m : q;
+  };
+  if (P.hist)
+    for (int64_t i = tid; i < P.C * (R + 1); i += THREADS) {
+      const int64_t c = i / (R + 1);
+      const int site = (int)(i - c * (R + 1));
+      P.hist[i] = hst[site * M1 + posof(c)];
+    }
+  for (int64_t c = tid; c < P.C; c += THREADS) {
+    const int p = posof(c);
+    if (P.ok) P.ok[c] = okp[p];
+    if (P.acc) {
+      P.acc[c] = accp[p];
+      P.sav[c] = savp[p];
+    }
+  }
+  if (P.trace) {
+    __syncthreads();
+    if (tid == 0) P.trace[blockIdx.x * 6 + 4] = diag2::gtimer();
+  }
+}
+
+}  // namespace diag3

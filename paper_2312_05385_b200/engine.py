@@ -143,6 +143,10 @@ def _pack_bits(correct: np.ndarray) -> np.ndarray:
     return np.packbits(padded, axis=1, bitorder="little").view("<u4").reshape(n)
 
 
+# Sweeps over an evaluator's own (immutable) device window are launched with
+# EE_MODE_FLAG_RESIDENT; False forces plain stream-ordered launches (A/B).
+RESIDENT_OVERLAP = True
+
 class WindowEvaluator:
     """Device-resident window: upload once, score many threshold configs.
 
@@ -206,6 +210,9 @@ class WindowEvaluator:
         bits = _pack_bits(arrays.correct)
         self.d_bits = torch.from_numpy(bits.view(np.int32)).to("cuda")
         self._scores_host = None
+        # The window is immutable from here on: once its producers have finished,
+        # sweeps may overlap the previous sweep on the stream (EE_MODE_FLAG_RESIDENT).
+        torch.cuda.current_stream().synchronize()
 
     # host views kept for API parity with the reference attributes
     @property
@@ -237,7 +244,9 @@ class WindowEvaluator:
         nat.check(lib.ee_eval_thresholds(
             nat.workspace(), nat.ptr(self.d_scores), self.d_bits.data_ptr(), self.n, self.r,
             self.serve.ctypes.data, float(self.vanilla_ms), th.ctypes.data if th.size else None,
-            c, self._mode_code if mode_code is None else mode_code, nat.ptr(hist), ok.data_ptr(),
+            c, (self._mode_code if mode_code is None else mode_code)
+            | (nat.MODE_FLAG_RESIDENT if RESIDENT_OVERLAP else 0),
+            nat.ptr(hist), ok.data_ptr(),
             nat.ptr(acc), nat.ptr(sav), nat.stream_handle(torch)))
         return acc, sav, ok, hist
 

@@ -307,10 +307,11 @@ def test_diagonal_family_path_matches_generic(cuda, r, clustered):
                                          (10, 4099, 127, 1), (12, 70001, 64, 1), (12, 2500, 40, 20),
                                          (14, 9000, 100, 1), (16, 12345, 126, 2)])
 def test_diag2_matches_diag1_and_oracle(cuda, r, n, m, c_rep):
-    """k_diag2 (coalesced, replicated bin table, predicated updates, one launch)
-    against k_diag and the C oracle: ragged tails (n % 32 != 0), up to 127
-    distinct thresholds incl. +-inf and +-0, NaN rows and NaN scores, rows whose
-    no-exit bit is 0, and more than 512 candidates (device position map)."""
+    """k_diag3 (lane-private cumulative counters, m <= 64) and k_diag2
+    (coalesced, replicated bin table, one launch) against k_diag and the C
+    oracle: ragged tails (n % 32 != 0), up to 127 distinct thresholds incl.
+    +-inf and +-0, NaN rows and NaN scores, rows whose no-exit bit is 0, and
+    more than 512 candidates (device position map)."""
     from paper_2312_05385_b200 import _native
 
     rng = np.random.default_rng(9100 + r + n)
@@ -329,14 +330,15 @@ def test_diag2_matches_diag1_and_oracle(cuda, r, n, m, c_rep):
     ev = WindowEvaluator.from_arrays(arrays, find_feasible_sites(prof)[:r], prof, mode="hist")
     hist2, ok2 = ev.histograms(th)
     acc2, sav2 = ev.evaluate_many(th)
-    _native.set_diag_version(1)
-    try:
-        hist1, ok1 = ev.histograms(th)
-        acc1, sav1 = ev.evaluate_many(th)
-    finally:
-        _native.set_diag_version(2)
-    assert np.array_equal(hist2, hist1) and np.array_equal(ok2, ok1)
-    assert np.array_equal(acc2, acc1) and np.array_equal(sav2, sav1)
+    for ver in (2, 1):
+        _native.set_diag_version(ver)
+        try:
+            hist1, ok1 = ev.histograms(th)
+            acc1, sav1 = ev.evaluate_many(th)
+        finally:
+            _native.set_diag_version()
+        assert np.array_equal(hist2, hist1) and np.array_equal(ok2, ok1), ver
+        assert np.array_equal(acc2, acc1) and np.array_equal(sav2, sav1), ver
     hist_o, ok_o = O.eval_hist(scores, cext, th)
     assert np.array_equal(hist2, hist_o) and np.array_equal(ok2, ok_o)
     # repeated calls on the same workspace: the accumulator is left zeroed
