@@ -366,14 +366,15 @@ def run_ours(args):
     b_alg = algorithmic_bytes(n_local, r, c)
     # the timed region holds only the K sweeps: average launch duration = region / K
     achieved = b_alg / (step_ms / 1e3) / 1e9
+    kname = max(kern.items(), key=lambda kv: kv[1]["ms"])[0] if kern else "k_diag3"
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": traffic_from_profiles(),
-        "kernel": "k_diag2",
+        "kernel": kname,
         "algorithmic_bytes_per_step": b_alg, "peak_source": peak_src,
         "how": "algorithmic bytes per launch / (CUDA-event time of the timed region / K launches)",
         "phase_timeline": phases,
-        "kernels": {"k_diag2": {"launches_per_step": 1, "ms_per_launch": step_ms,
+        "kernels": {kname: {"launches_per_step": 1, "ms_per_launch": step_ms,
                                 "share": 1.0 if world == 1 else None}},
     }
     line = {

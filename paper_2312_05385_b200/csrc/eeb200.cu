@@ -1144,7 +1144,7 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
   const int upd = ws->diag_version == 3 ? 0 : 1;
   // k_diag3 (lane-private cumulative counters) where its envelope holds
   const bool v3 = ws->diag_version >= 4 && m <= diag3::MAX_M &&
-                  ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n) * diag2::WARPS) <= diag3::MAX_ITERS;
+                  ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n)) <= diag3::MAX_CTA_CHUNKS;
   if (v3) {
     switch (r) {
       case 2: e = launch_diag3<2>(p, n, st, ws); break;

@@ -32,7 +32,7 @@ constexpr int WARPS = diag2::WARPS;
 constexpr int MAX_M = 64;
 constexpr int CELLS = MAX_M + 1;          // positions 0..m (m = sink)
 constexpr int ROWC = CELLS * 32 * 4;      // bytes per ramp: [cell][lane] u32
-constexpr int MAX_ITERS = 1023;           // chunk iterations per warp (32 warps x 1023 < 2^15)
+constexpr int MAX_CTA_CHUNKS = 32767;     // chunks per CTA: updates per lane copy of a cell < 2^15
 constexpr int OFF_TAB = diag2::OFF_TAB;
 constexpr int OFF_SU = diag2::OFF_SU;
 constexpr int OFF_KEY = diag2::OFF_KEY;
@@ -72,12 +72,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
 
   const int64_t n = P.n;
   const int64_t nchunks = (n + 31) >> 5;
-  const int64_t G = (int64_t)gridDim.x * WARPS;
-  int64_t ch = (int64_t)blockIdx.x * WARPS + warp;
+  // Each CTA streams one contiguous, equal share of the chunks (212-213 at
+  // config 4) and its warps interleave over it: a grid-stride split gave 7
+  // chunks per warp to two thirds of the CTAs and 6 to the rest.
+  const int64_t c_end = (int64_t)(blockIdx.x + 1) * nchunks / gridDim.x;
+  int64_t ch = (int64_t)blockIdx.x * nchunks / gridDim.x + warp;
+  constexpr int64_t G = WARPS;
   double2 v[R / 2];
   uint32_t cb = 0;
   auto load = [&](int64_t c) {
-    if (c >= nchunks) return;
+    if (c >= c_end) return;
     const int64_t s0 = c << 5;
     const double2* src = reinterpret_cast<const double2*>(P.s + s0 * R);
     if (s0 + 32 <= n) {
@@ -95,21 +99,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
     }
   };
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 0] = diag2::gtimer();
+  // Parameter reads first: a constant-bank miss issued after the window's
+  // loads queues behind them (measured: a 2 us prologue).
+  static_assert(diag2::NB * 8 == 2 * THREADS && (diag2::MAX_M + 1) * diag2::SU_REP / 2 == THREADS,
+                "one table pair and one threshold pair per thread");
+  const uint32_t te0 = P.tab[tid >> 3], te1 = P.tab[(tid + THREADS) >> 3];
+  const int tu = tid / (diag2::SU_REP / 2);
+  const double ue = tu < m ? P.u[tu] : __longlong_as_double(0x7ff8000000000000LL);
   load(ch);  // first HBM round trip overlaps the prologue
 
-  // ---- prologue (vector stores): replicated bin table, replicated thresholds, biased cells
+  // ---- prologue (vector stores): zeroed cells, replicated bin table and thresholds
   {
-    uint4* t4 = reinterpret_cast<uint4*>(stab);
-    for (int q = tid; q < diag2::NB * 8; q += THREADS) {  // 8 uint4 per bin (32 copies)
-      const uint32_t e = P.tab[q >> 3];
-      t4[q] = make_uint4(e, e, e, e);
-    }
-    double2* s2 = reinterpret_cast<double2*>(su);
-    for (int q = tid; q < (diag2::MAX_M + 1) * diag2::SU_REP / 2; q += THREADS) {
-      const int t = q / (diag2::SU_REP / 2);
-      const double x = t < m ? P.u[t] : __longlong_as_double(0x7ff8000000000000LL);
-      s2[q] = make_double2(x, x);
-    }
     uint4* c4 = reinterpret_cast<uint4*>(cells);
     const int per_ramp = (m + 1) * 8;  // uint4 per ramp row in use (cells 0..m)
     for (int q = tid; q < R * per_ramp; q += THREADS) {
@@ -118,6 +118,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
     }
     if (tid < MAX_M) s_osum[tid] = 0;
     if (tid == 0) s_corr = 0;
+    uint4* t4 = reinterpret_cast<uint4*>(stab);  // 8 uint4 per bin (32 copies)
+    t4[tid] = make_uint4(te0, te0, te0, te0);
+    t4[tid + THREADS] = make_uint4(te1, te1, te1, te1);
+    reinterpret_cast<double2*>(su)[tid] = make_double2(ue, ue);
   }
   __syncthreads();
 
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
   unsigned char* kb = skey + warp * 32 * R;
   unsigned corr = 0;
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 1] = diag2::gtimer();
-  for (; ch < nchunks; ch += G) {
+  for (; ch < c_end; ch += G) {
     __syncwarp();  // previous chunk's key reads are done
     // Each pair's registers are refilled with the next chunk as soon as its two
     // keys are taken, so the next chunk's loads leave during the keying (ncu:
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
     const int64_t nx = ch + G;
     const int64_t s1 = nx << 5;
     const double2* src = reinterpret_cast<const double2*>(P.s + s1 * R);
-    const int64_t npairs = nx < nchunks ? (n - s1) * (R / 2) : 0;  // valid pairs of the next chunk
+    const int64_t npairs = nx < c_end ? (n - s1) * (R / 2) : 0;  // valid pairs of the next chunk
 #pragma unroll
     for (int k = 0; k < R / 2; ++k) {
       const uint32_t k0 = keyof(v[k].x), k1 = keyof(v[k].y);
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
         v[k] = t < npairs ? __ldcs(src + t) : make_double2(INF, INF);
     }
     const uint32_t cbc = cb;
-    if (nx < nchunks) cb = s1 + lane < n ? __ldcs(P.bits + s1 + lane) : 0u;
+    if (nx < c_end) cb = s1 + lane < n ? __ldcs(P.bits + s1 + lane) : 0u;
     __syncwarp();
     uint32_t kw[NW];
     if constexpr (R % 16 == 0) {

@@ -6,4 +6,4 @@ timeout 300 python bench.py --steps 200 --warmup 10 --no-cpu-baseline --e2e-step
 python -c "
 import json;d=json.loads(open('gpurun_out/bench.log').read().strip().splitlines()[-1]);print(d['value'], d['ms_per_step'], json.dumps(d['roofline']))"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv python tools/profile_sweep.py diagonal 20 > /dev/null 2>&1; echo "ncu list rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_diag' -s 3 -c 1 -o gpurun_out/prof_diag2 -f python tools/profile_sweep.py diagonal 8 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_diag' -s 3 -c 1 -o gpurun_out/prof_diag -f python tools/profile_sweep.py diagonal 8 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"

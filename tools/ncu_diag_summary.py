@@ -1,0 +1,66 @@
+"""Summary of one ncu --set full capture of a sweep kernel (profiles/*_ncu_full.txt):
+time, DRAM bytes, issue activity, shared-memory wavefronts/conflicts, stall
+reasons, op mix and the hottest SASS lines. With --traffic also rewrites
+profiles/ncu_traffic.json (DRAM bytes per launch, read by bench.py).
+Usage: ncu_diag_summary.py report.ncu-rep [--traffic]"""
+import csv, io, json, os, subprocess, sys
+from collections import Counter
+
+rep = sys.argv[1]
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+run = lambda *a: subprocess.run(["ncu", "-i", rep, *a], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(run("--page", "raw", "--csv"))))
+h, units, r = rows[0], rows[1], rows[2]
+d = dict(zip(h, r))
+u = dict(zip(h, units))
+num = lambda k: float(d[k].replace(",", ""))
+mb = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+name = d["Kernel Name"]
+out = [f"== {name}"]
+for k in ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+          "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
+          "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+          "launch__registers_per_thread", "sm__warps_active.avg.per_cycle_active",
+          "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+          "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+          "sm__throughput.avg.pct_of_peak_sustained_elapsed"]:
+    if k in d:
+        out.append(f"   {k} = {d[k]} {u[k]}")
+st = sorted(((num(k), k.replace("smsp__pcsamp_warps_issue_stalled_", "")) for k in h
+             if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")
+             and d[k].replace(",", "").replace(".", "").isdigit()), reverse=True)
+out.append("   stalls (pc samples): " + ", ".join(f"{k}={int(v)}" for v, k in st[:8] if v > 0))
+src = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "sass"))))
+sh, sd = src[1], src[2:]
+ix = {k: i for i, k in enumerate(sh)}
+f = lambda row, k: float(row[ix[k]].replace(",", "") or 0) if k in ix and row[ix[k]] else 0.0
+ops, wf, ex = Counter(), Counter(), Counter()
+for row in sd:
+    toks = row[ix["Source"]].split()
+    if not toks:
+        continue
+    op = (toks[1] if toks[0].startswith("@") else toks[0]).split(".")[0]
+    ops[op] += f(row, "Instructions Executed")
+    wf[op] += f(row, "L1 Wavefronts Shared")
+    ex[op] += f(row, "L1 Wavefronts Shared Excessive")
+out.append("   op mix: " + ", ".join(f"{k}={int(v)}" for k, v in ops.most_common(14)))
+out.append("   shared wavefronts by op: " + ", ".join(f"{k}={int(v)} (excess {int(ex[k])})"
+                                                     for k, v in wf.most_common(5) if v))
+hot = sorted(sd, key=lambda row: -f(row, "Warp Stall Sampling (All Samples)"))[:10]
+for row in hot:
+    out.append(f"   hot: {int(f(row, 'Warp Stall Sampling (All Samples)'))} samples, "
+               f"{int(f(row, 'Instructions Executed'))} exec  {row[ix['Source']].strip()[:70]}")
+print("\n".join(out))
+if "--traffic" in sys.argv:
+    rd = num("dram__bytes_read.sum") * mb[u["dram__bytes_read.sum"]] * 1e6
+    wr = num("dram__bytes_write.sum") * mb[u["dram__bytes_write.sum"]] * 1e6
+    alg = 8 * 1_000_000 * 12 + 1_000_000 * 12 // 8 + 8 * 64 * 12 + 16 * 64
+    json.dump({"source": f"{os.path.basename(rep)} (ncu --set full --clock-control none, "
+                         "tools/profile_sweep.py diagonal)",
+               "kernel": name + " (the whole config-4 sweep is this one launch)",
+               "dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
+               "sweep_dram_bytes_per_step": int(rd + wr), "algorithmic_bytes_per_step": alg,
+               "note": "read = 96 MB f64 scores + 4 MB u32 correctness rows (4 B/sample vs the "
+                       "bit-packed 1.5 B/sample algorithmic figure); write = per-CTA count "
+                       f"merges + results. traffic/algorithmic = {(rd + wr) / alg:.3f}"},
+              open(os.path.join(root, "profiles", "ncu_traffic.json"), "w"), indent=1)
