@@ -468,6 +468,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 #include "sweep_diag.cuh"
 #include "sweep_diag2.cuh"
 #include "sweep_diag3.cuh"
+#include "sweep_axis.cuh"
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
 #include "gemm_tc.cuh"
@@ -528,6 +529,11 @@ struct ee_workspace {
   std::vector<Stager> stagers;
   long long* d_diag_acc = nullptr;
   bool diag_acc_dirty = true;
+  // axis-family sweep: per-CTA partial cells and their 64-bit totals
+  uint32_t* d_axis_part = nullptr;
+  size_t axis_part_cap = 0;
+  unsigned long long* d_axis_tot = nullptr;  // [2][ncell]: counts, then deltas/corrects
+  size_t axis_tot_cap = 0;
   unsigned long long* d_diag_trace = nullptr;  // set by ee_diag_trace (profiling)
   struct Mark {
     const char* name;
@@ -712,6 +718,8 @@ int ee_workspace_destroy(ee_workspace* ws) {
   if (ws->staged) cudaEventSynchronize(ws->staged);
   if (ws->d_buf) cudaFree(ws->d_buf);
   if (ws->d_diag_acc) cudaFree(ws->d_diag_acc);
+  if (ws->d_axis_part) cudaFree(ws->d_axis_part);
+  if (ws->d_axis_tot) cudaFree(ws->d_axis_tot);
   if (ws->d_in) cudaFree(ws->d_in);
   for (auto& m : ws->marks) cudaEventDestroy(m.a), cudaEventDestroy(m.b);
   for (auto e : ws->event_pool) cudaEventDestroy(e);
@@ -1062,16 +1070,18 @@ static cudaError_t launch_diag3(const diag2::Params& p, int64_t n, cudaStream_t 
 }
 extern "C" {
 
-static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
-                      int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
-                      const std::vector<double>& u, int64_t* d_hist, int64_t* d_ok, double* d_acc,
-                      double* d_sav, cudaStream_t st) {
+// The single-threshold bin grid of k_diag2/k_diag3/k_axis: a, c0 with the
+// smallest finite threshold in bin 2 and the largest in bin 253, and the
+// 256-entry table (lo = #{thresholds in lower bins}, and the byte offset of the
+// bin's own threshold or of the NaN sentinel). False if some bin would hold
+// two thresholds or a threshold would share bin 255 with NaN.
+// With allow_inf a +inf threshold may take bin 255 (the kernel must then give
+// NaN scores key m itself: NaN shares that bin).
+static bool plan_bins(const std::vector<double>& u, double* pa, double* pc0, uint32_t* tab,
+                      bool allow_inf = false) {
   const int m = (int)u.size();
-  if (ws->diag_version < 2 || r < 2 || r > diag2::RMAX || (r & 1) || m < 1 || m > diag2::MAX_M)
-    return 1;
-  if ((reinterpret_cast<uintptr_t>(d_scores) & 15) != 0) return 1;
-  if (u.back() == std::numeric_limits<double>::infinity()) return 1;  // bin 255 stays threshold-free
-  // grid over the finite thresholds: smallest -> bin 2, largest -> bin 253
+  if (m < 1 || m > diag2::MAX_M) return false;
+  if (u.back() == std::numeric_limits<double>::infinity() && !allow_inf) return false;
   double f0 = 0.0, f1 = 0.0;
   bool any = false;
   for (double x : u)
@@ -1080,26 +1090,36 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
       f1 = x;
       any = true;
     }
-  diag2::Params p{};
   double a = 1e-300;
   if (any && f1 > f0) a = 251.0 / (f1 - f0);
   const double c0 = any ? 2.0 - a * f0 : 2.0;
-  if (!std::isfinite(a) || !(a > 0.0) || !std::isfinite(c0)) return 1;
-  p.a = a;
-  p.c0 = c0;
+  if (!std::isfinite(a) || !(a > 0.0) || !std::isfinite(c0)) return false;
   std::vector<unsigned> bu((size_t)m);
   for (int i = 0; i < m; ++i) {  // one threshold per bin, none in bin 255
-    bu[i] = diag2::bin_of(u[i], p.a, p.c0);
-    if (bu[i] == 255u) return 1;
-    if (i > 0 && bu[i] <= bu[i - 1]) return 1;
+    bu[i] = diag2::bin_of(u[i], a, c0);
+    if (bu[i] == 255u && !(allow_inf && i == m - 1 && std::isinf(u[i]))) return false;
+    if (i > 0 && bu[i] <= bu[i - 1]) return false;
   }
-  // bin table: lo = #{thresholds in lower bins} (all < x), and the byte offset
-  // of the bin's own threshold in u[] (or of the NaN sentinel SENT)
   for (int k = 0, lo = 0; k < diag2::NB; ++k) {
     while (lo < m && bu[lo] < (unsigned)k) ++lo;
     const int cmp = (lo < m && bu[lo] == (unsigned)k) ? lo : diag2::SENT;
-    p.tab[k] = (uint32_t)lo | ((uint32_t)(cmp * diag2::SU_STRIDE) << 16);
+    tab[k] = (uint32_t)lo | ((uint32_t)(cmp * diag2::SU_STRIDE) << 16);
   }
+  *pa = a;
+  *pc0 = c0;
+  return true;
+}
+
+static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                      int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
+                      const std::vector<double>& u, int64_t* d_hist, int64_t* d_ok, double* d_acc,
+                      double* d_sav, cudaStream_t st) {
+  const int m = (int)u.size();
+  if (ws->diag_version < 2 || r < 2 || r > diag2::RMAX || (r & 1) || m < 1 || m > diag2::MAX_M)
+    return 1;
+  if ((reinterpret_cast<uintptr_t>(d_scores) & 15) != 0) return 1;
+  diag2::Params p{};
+  if (!plan_bins(u, &p.a, &p.c0, p.tab)) return 1;
   if (!ws->d_diag_acc) {
     EE_CUDA(cudaMalloc(&ws->d_diag_acc, (size_t)diag2::ACC_WORDS * 8));
     ws->diag_acc_dirty = true;
@@ -1175,6 +1195,155 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
   return EE_OK;
 }
 
+// Single-coordinate family: every row equals a base vector except in at most
+// one column. base[j] = the most frequent value of column j (NaN counts as one
+// value); col[c]/val[c] = the varied column and its value (a row equal to the
+// base is column 0 at base[0]).
+}  // extern "C"
+static bool same_value(double a, double b) { return a == b || (a != a && b != b); }
+static bool axis_rows(const double* th, int64_t C, int r, std::vector<double>& base,
+                      std::vector<int>& col, std::vector<double>& val) {
+  if (r < 2 || C < 1 || C > axis::MAX_C) return false;
+  base.assign((size_t)r, 0.0);
+  std::vector<double> v((size_t)C);
+  for (int j = 0; j < r; ++j) {
+    for (int64_t c = 0; c < C; ++c) {
+      const double x = th[c * r + j];
+      v[c] = x != x ? std::numeric_limits<double>::quiet_NaN() : canon(x);
+    }
+    std::sort(v.begin(), v.end(), [](double a, double b) {  // NaNs last
+      return (a == a && b == b) ? a < b : (a == a);
+    });
+    int64_t best = 0, run = 0;
+    double bv = v[0];
+    for (int64_t c = 0; c < C; ++c) {
+      run = (c > 0 && same_value(v[c], v[c - 1])) ? run + 1 : 1;
+      if (run > best) best = run, bv = v[c];
+    }
+    base[j] = bv;
+  }
+  col.assign((size_t)C, 0);
+  val.assign((size_t)C, base[0]);
+  for (int64_t c = 0; c < C; ++c) {
+    int diff = -1;
+    for (int j = 0; j < r; ++j)
+      if (!same_value(th[c * r + j], base[j])) {
+        if (diff >= 0) return false;
+        diff = j;
+      }
+    if (diff >= 0) col[c] = diff, val[c] = th[c * r + diff];
+  }
+  return true;
+}
+
+template <int R>
+static cudaError_t launch_axis(const axis::Params& p, unsigned grid, cudaStream_t st,
+                               ee_workspace* ws) {
+  static bool attr_set = false;
+  constexpr int smem = axis::Layout<R>::SMEM;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(axis::k_axis<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  ProfScope ps(ws, st, "k_axis");
+  axis::k_axis<R><<<grid, axis::THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+template <int R>
+static cudaError_t launch_axis_fin(const axis::FinParams& p, cudaStream_t st, ee_workspace* ws) {
+  ProfScope ps(ws, st, "k_axis_fin");
+  axis::k_axis_fin<R><<<R, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+extern "C" {
+
+// Returns 1 when the rows are not a single-coordinate family inside the
+// kernel's envelope, so the caller runs the generic path.
+static int eval_axis(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
+                     int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
+                     int64_t* d_hist, int64_t* d_ok, double* d_acc, double* d_sav,
+                     cudaStream_t st) {
+  if (r < 2 || r > diag2::RMAX || (r & 1) || C > axis::MAX_C) return 1;
+  if ((reinterpret_cast<uintptr_t>(d_scores) & 15) != 0) return 1;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), ceil_div(ceil_div(n, 32), axis::WARPS)));
+  if (ceil_div(ceil_div(n, 32), (int64_t)grid) > axis::MAX_CTA_CHUNKS) return 1;
+  std::vector<double> base, val, u;
+  std::vector<int> col;
+  if (!axis_rows(h_th, C, r, base, col, val)) return 1;
+  for (int64_t c = 0; c < C; ++c)
+    if (val[c] == val[c]) u.push_back(canon(val[c]));
+  std::sort(u.begin(), u.end());
+  u.erase(std::unique(u.begin(), u.end()), u.end());
+  if (u.empty() || (int)u.size() > axis::MAX_M) return 1;
+  axis::Params p{};
+  if (!plan_bins(u, &p.a, &p.c0, p.tab, /*allow_inf=*/true)) return 1;
+  const int m = (int)u.size();
+  const int ncell = axis::ncell(r, m);
+  const size_t part_b = (size_t)grid * ncell * 4, tot_b = (size_t)2 * ncell * 8;
+  if (part_b > ws->axis_part_cap) {
+    if (ws->d_axis_part) EE_CUDA(cudaFree(ws->d_axis_part));
+    ws->d_axis_part = nullptr;
+    EE_CUDA(cudaMalloc(&ws->d_axis_part, part_b));
+    ws->axis_part_cap = part_b;
+  }
+  if (tot_b > ws->axis_tot_cap) {
+    if (ws->d_axis_tot) EE_CUDA(cudaFree(ws->d_axis_tot));
+    ws->d_axis_tot = nullptr;
+    EE_CUDA(cudaMalloc(&ws->d_axis_tot, tot_b));
+    ws->axis_tot_cap = tot_b;
+  }
+  p.s = d_scores;
+  p.bits = d_bits;
+  p.n = n;
+  p.part = ws->d_axis_part;
+  p.ncell = ncell;
+  p.m = m;
+  for (int j = 0; j < r; ++j) p.base[j] = base[j];
+  for (int i = 0; i < m; ++i) p.u[i] = u[i];
+  axis::FinParams fp{};
+  fp.tot_cnt = ws->d_axis_tot;
+  fp.tot_x = reinterpret_cast<const long long*>(ws->d_axis_tot + ncell);
+  fp.n = n;
+  fp.m = m;
+  fp.C = C;
+  fp.vanilla = vanilla;
+  for (int j = 0; j <= r; ++j) fp.serve[j] = h_serve[j];
+  fp.hist = d_hist;
+  fp.ok = d_ok;
+  fp.acc = d_acc;
+  fp.sav = d_sav;
+  for (int64_t c = 0; c < C; ++c) {
+    const double x = val[c];
+    const int k = x == x ? (int)(std::lower_bound(u.begin(), u.end(), canon(x)) - u.begin()) : 255;
+    fp.code[c] = (uint16_t)((col[c] << 8) | k);
+  }
+  cudaError_t e;
+  switch (r) {
+#define EE_AXIS_CASE(K) case K: e = launch_axis<K>(p, grid, st, ws); break;
+    EE_AXIS_CASE(2) EE_AXIS_CASE(4) EE_AXIS_CASE(6) EE_AXIS_CASE(8) EE_AXIS_CASE(10)
+    EE_AXIS_CASE(12) EE_AXIS_CASE(14) default: e = launch_axis<16>(p, grid, st, ws); break;
+#undef EE_AXIS_CASE
+  }
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_axis: ") + cudaGetErrorString(e));
+  EE_CUDA(cudaMemsetAsync(ws->d_axis_tot, 0, tot_b, st));
+  {
+    ProfScope ps(ws, st, "k_axis_reduce");
+    axis::k_axis_reduce<<<dim3((unsigned)ceil_div(ncell, 256), axis::REDUCE_SPLIT), 256, 0, st>>>(
+        ws->d_axis_part, (int)grid, ncell, r * m * (r + 1), ws->d_axis_tot,
+        reinterpret_cast<long long*>(ws->d_axis_tot + ncell));
+  }
+  EE_LAUNCH_CHECK();
+  switch (r) {
+#define EE_AXIS_CASE(K) case K: e = launch_axis_fin<K>(fp, st, ws); break;
+    EE_AXIS_CASE(2) EE_AXIS_CASE(4) EE_AXIS_CASE(6) EE_AXIS_CASE(8) EE_AXIS_CASE(10)
+    EE_AXIS_CASE(12) EE_AXIS_CASE(14) default: e = launch_axis_fin<16>(fp, st, ws); break;
+#undef EE_AXIS_CASE
+  }
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_axis_fin: ") + cudaGetErrorString(e));
+  return EE_OK;
+}
+
 static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, int64_t n,
                      int r, const double* h_serve, double vanilla, const double* h_th, int64_t C,
                      int64_t* d_hist, int64_t* d_ok, double* d_acc, double* d_sav,
@@ -1187,6 +1356,11 @@ static int eval_hist(ee_workspace* ws, const double* d_scores, const uint32_t* d
       if (rc != 1) return rc;
       return eval_diag(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, C, u, d_hist, d_ok,
                        d_acc, d_sav, st);
+    }
+    if (ws->allow_special) {
+      const int rc = eval_axis(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, C, d_hist, d_ok,
+                               d_acc, d_sav, st);
+      if (rc != 1) return rc;
     }
   }
   const int rw = std::max(1, (r + 3) / 4);

@@ -303,6 +303,60 @@ def test_diagonal_family_path_matches_generic(cuda, r, clustered):
     assert np.array_equal(hist_d, hist_o) and np.array_equal(ok_d, ok_o)
 
 
+@pytest.mark.parametrize("r,n,nan_base", [(2, 37, False), (6, 5003, True), (12, 40001, False),
+                                          (12, 70001, True), (16, 20011, False)])
+def test_axis_family_path_matches_generic_and_oracle(cuda, r, n, nan_base):
+    """k_axis (rows = a base vector with one coordinate swept over a shared value
+    set, SURVEY 8(d)'s C = 768 family) against the generic SWAR kernel and the C
+    oracle: ragged tails, NaN/inf/-0 scores, NaN and +-inf values, rows equal to
+    the base, a NaN base entry, no-exit bit 0 rows; the k_axis launch is checked."""
+    from paper_2312_05385_b200 import _native
+
+    rng = np.random.default_rng(4400 + r + n)
+    scores, cext, serve, vanilla, _ = random_window(rng, n, r, 1, nan_frac=0.01)
+    scores[rng.random((n, r)) < 0.01] = np.inf
+    scores[rng.random((n, r)) < 0.01] = -0.0
+    scores[rng.random((n, r)) < 0.02] = 0.3  # ties with the base
+    cext[:, r] = (rng.random(n) < 0.8).astype(np.float64)
+    vals = np.concatenate([np.arange(60) / 59.0, [np.inf, -np.inf, -0.0, np.nan]])
+    base = np.full(r, 0.3)
+    if nan_base:
+        base[r // 2] = np.nan
+    rows = [base.copy()] if r < 16 else []  # a row equal to the base (C <= 1024)
+    for j in range(r):
+        for v in vals:
+            row = base.copy()
+            row[j] = v
+            rows.append(row)
+    th = np.array(rows)
+    rng.shuffle(th)
+    assert th.shape[0] <= 1024
+    arrays = WindowArrays(scores, cext.astype(np.uint8))
+    prof = make_chain(r + 1)
+    ev = WindowEvaluator.from_arrays(arrays, find_feasible_sites(prof)[:r], prof, mode="hist")
+    _native.profile_read()
+    _native.profile_enable(True)
+    try:
+        hist_a, ok_a = ev.histograms(th)
+        acc_a, sav_a = ev.evaluate_many(th)
+    finally:
+        _native.profile_enable(False)
+    assert "k_axis" in _native.profile_read()
+    _native.set_special(False)
+    try:
+        hist_g, ok_g = ev.histograms(th)
+        acc_g, sav_g = ev.evaluate_many(th)
+    finally:
+        _native.set_special(True)
+    assert np.array_equal(hist_a, hist_g) and np.array_equal(ok_a, ok_g)
+    assert np.array_equal(acc_a, acc_g) and np.array_equal(sav_a, sav_g)
+    hist_o, ok_o = O.eval_hist(scores, cext, th)
+    assert np.array_equal(hist_a, hist_o) and np.array_equal(ok_a, ok_o)
+    # repeated call: the totals are rebuilt from zero
+    hist2, ok2 = ev.histograms(th)
+    assert np.array_equal(hist2, hist_a) and np.array_equal(ok2, ok_a)
+
+
 @pytest.mark.parametrize("r,n,m,c_rep", [(2, 1, 5, 1), (4, 31, 17, 1), (6, 33, 64, 1),
                                          (10, 4099, 127, 1), (12, 70001, 64, 1), (12, 2500, 40, 20),
                                          (14, 9000, 100, 1), (16, 12345, 126, 2)])
