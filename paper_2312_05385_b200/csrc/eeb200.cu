@@ -1201,10 +1201,39 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
 // base is column 0 at base[0]).
 }  // extern "C"
 static bool same_value(double a, double b) { return a == b || (a != a && b != b); }
+// every row differs from base in at most one column: col/val per row
+static bool fits_base(const double* th, int64_t C, int r, const std::vector<double>& base,
+                      std::vector<int>& col, std::vector<double>& val) {
+  col.assign((size_t)C, 0);
+  val.assign((size_t)C, base[0]);
+  for (int64_t c = 0; c < C; ++c) {
+    int diff = -1;
+    for (int j = 0; j < r; ++j)
+      if (!same_value(th[c * r + j], base[j])) {
+        if (diff >= 0) return false;
+        diff = j;
+      }
+    if (diff >= 0) col[c] = diff, val[c] = th[c * r + diff];
+  }
+  return true;
+}
 static bool axis_rows(const double* th, int64_t C, int r, std::vector<double>& base,
                       std::vector<int>& col, std::vector<double>& val) {
   if (r < 2 || C < 1 || C > axis::MAX_C) return false;
   base.assign((size_t)r, 0.0);
+  // fast path: the base is each column's majority value (Boyer-Moore vote), as in
+  // the sweep families where each column is varied in fewer than half the rows
+  for (int j = 0; j < r; ++j) {
+    double cand = th[j];
+    int64_t cnt = 0;
+    for (int64_t c = 0; c < C; ++c) {
+      const double x = th[c * r + j];
+      if (cnt == 0) cand = x, cnt = 1;
+      else cnt += same_value(x, cand) ? 1 : -1;
+    }
+    base[j] = cand;
+  }
+  if (fits_base(th, C, r, base, col, val)) return true;
   std::vector<double> v((size_t)C);
   for (int j = 0; j < r; ++j) {
     for (int64_t c = 0; c < C; ++c) {
@@ -1222,38 +1251,28 @@ static bool axis_rows(const double* th, int64_t C, int r, std::vector<double>& b
     }
     base[j] = bv;
   }
-  col.assign((size_t)C, 0);
-  val.assign((size_t)C, base[0]);
-  for (int64_t c = 0; c < C; ++c) {
-    int diff = -1;
-    for (int j = 0; j < r; ++j)
-      if (!same_value(th[c * r + j], base[j])) {
-        if (diff >= 0) return false;
-        diff = j;
-      }
-    if (diff >= 0) col[c] = diff, val[c] = th[c * r + diff];
-  }
-  return true;
+  return fits_base(th, C, r, base, col, val);
 }
 
 template <int R>
-static cudaError_t launch_axis(const axis::Params& p, unsigned grid, cudaStream_t st,
+static cudaError_t launch_axis(const axis::Params& p, unsigned grid, bool nanchk, cudaStream_t st,
                                ee_workspace* ws) {
-  static bool attr_set = false;
+  static bool attr_set[2] = {false, false};
   constexpr int smem = axis::Layout<R>::SMEM;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(axis::k_axis<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto k = nanchk ? axis::k_axis<R, true> : axis::k_axis<R, false>;
+  if (!attr_set[nanchk]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[nanchk] = true;
   }
   ProfScope ps(ws, st, "k_axis");
-  axis::k_axis<R><<<grid, axis::THREADS, smem, st>>>(p);
+  k<<<grid, axis::THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
 template <int R>
 static cudaError_t launch_axis_fin(const axis::FinParams& p, cudaStream_t st, ee_workspace* ws) {
   ProfScope ps(ws, st, "k_axis_fin");
-  axis::k_axis_fin<R><<<R, 256, 0, st>>>(p);
+  axis::k_axis_fin<R><<<R, 512, 0, st>>>(p);
   return cudaGetLastError();
 }
 extern "C" {
@@ -1318,11 +1337,12 @@ static int eval_axis(ee_workspace* ws, const double* d_scores, const uint32_t* d
     const int k = x == x ? (int)(std::lower_bound(u.begin(), u.end(), canon(x)) - u.begin()) : 255;
     fp.code[c] = (uint16_t)((col[c] << 8) | k);
   }
+  const bool nanchk = std::isinf(u.back()) && u.back() > 0;
   cudaError_t e;
   switch (r) {
-#define EE_AXIS_CASE(K) case K: e = launch_axis<K>(p, grid, st, ws); break;
+#define EE_AXIS_CASE(K) case K: e = launch_axis<K>(p, grid, nanchk, st, ws); break;
     EE_AXIS_CASE(2) EE_AXIS_CASE(4) EE_AXIS_CASE(6) EE_AXIS_CASE(8) EE_AXIS_CASE(10)
-    EE_AXIS_CASE(12) EE_AXIS_CASE(14) default: e = launch_axis<16>(p, grid, st, ws); break;
+    EE_AXIS_CASE(12) EE_AXIS_CASE(14) default: e = launch_axis<16>(p, grid, nanchk, st, ws); break;
 #undef EE_AXIS_CASE
   }
   if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_axis: ") + cudaGetErrorString(e));

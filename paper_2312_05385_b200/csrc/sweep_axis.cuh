@@ -77,7 +77,8 @@ struct Layout {
   static constexpr int SMEM = OFF_DUM + 32 * 4;
 };
 
-template <int R>
+// NANCHK: V holds +inf, which shares bin 255 with NaN, so NaN is keyed explicitly.
+template <int R, bool NANCHK>
 __global__ void __launch_bounds__(THREADS, 1) k_axis(const __grid_constant__ Params P) {
   static_assert(R % 2 == 0 && R >= 2 && R <= diag2::RMAX, "even R only");
   using L = Layout<R>;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_axis(const __grid_constant__ Par
     asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
         : "+r"(key)
         : "d"(t), "d"(x));
-    key = x != x ? (uint32_t)m : key;  // NaN never exits (it shares bin 255 with a +inf value)
+    if constexpr (NANCHK) key = x != x ? (uint32_t)m : key;  // NaN never exits
     return key | (x < b ? 0x80u : 0u);
   };
   unsigned char* kb = sm + diag2::OFF_KEY + warp * 32 * R;
@@ -238,7 +239,7 @@ __global__ void k_axis_reduce(const uint32_t* __restrict__ part, int grid, int n
 
 // one CTA per column j: prefix over keys, then every candidate of column j
 template <int R>
-__global__ void __launch_bounds__(256) k_axis_fin(const __grid_constant__ FinParams P) {
+__global__ void __launch_bounds__(512) k_axis_fin(const __grid_constant__ FinParams P) {
   constexpr int R1 = R + 1;
   const int j = blockIdx.x, m = P.m, tid = threadIdx.x;
   __shared__ long long pc[MAX_M * R1], pd[MAX_M * R1];
@@ -255,13 +256,24 @@ __global__ void __launch_bounds__(256) k_axis_fin(const __grid_constant__ FinPar
     sEc[tid] = P.tot_x[n3 + R1 + j * R1 + tid];
   }
   __syncthreads();
-  if (tid < R1) {  // prefix over keys for site s = tid
-    long long a = 0, b = 0;
-    for (int k = 0; k < m; ++k) {
-      a += pc[k * R1 + tid];
-      b += pd[k * R1 + tid];
-      pc[k * R1 + tid] = a;
-      pd[k * R1 + tid] = b;
+  {  // prefix over keys, one warp per site s (shuffle scans, 32 keys per step)
+    const int lane = tid & 31;
+    for (int srow = tid >> 5; srow < R1; srow += blockDim.x >> 5) {
+      long long ca = 0, cd = 0;
+      for (int k0 = 0; k0 < m; k0 += 32) {
+        const int k = k0 + lane;
+        long long a = k < m ? pc[k * R1 + srow] : 0, b = k < m ? pd[k * R1 + srow] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
+          if (lane >= o) a += ya, b += yb;
+        }
+        a += ca;
+        b += cd;
+        if (k < m) pc[k * R1 + srow] = a, pd[k * R1 + srow] = b;
+        ca = __shfl_sync(0xffffffffu, a, 31);
+        cd = __shfl_sync(0xffffffffu, b, 31);
+      }
     }
   }
   __syncthreads();

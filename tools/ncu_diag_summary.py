@@ -2,15 +2,18 @@
 time, DRAM bytes, issue activity, shared-memory wavefronts/conflicts, stall
 reasons, op mix and the hottest SASS lines. With --traffic also rewrites
 profiles/ncu_traffic.json (DRAM bytes per launch, read by bench.py).
-Usage: ncu_diag_summary.py report.ncu-rep [--traffic]"""
+Usage: ncu_diag_summary.py report.ncu-rep [--traffic] [--kernel REGEX]"""
 import csv, io, json, os, subprocess, sys
 from collections import Counter
 
 rep = sys.argv[1]
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+import re
+kre = re.compile(sys.argv[sys.argv.index("--kernel") + 1]) if "--kernel" in sys.argv else None
 run = lambda *a: subprocess.run(["ncu", "-i", rep, *a], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(run("--page", "raw", "--csv"))))
-h, units, r = rows[0], rows[1], rows[2]
+h, units = rows[0], rows[1]
+r = next(x for x in rows[2:] if kre is None or kre.search(x[h.index("Kernel Name")]))
 d = dict(zip(h, r))
 u = dict(zip(h, units))
 num = lambda k: float(d[k].replace(",", ""))
@@ -31,7 +34,18 @@ st = sorted(((num(k), k.replace("smsp__pcsamp_warps_issue_stalled_", "")) for k 
              and d[k].replace(",", "").replace(".", "").isdigit()), reverse=True)
 out.append("   stalls (pc samples): " + ", ".join(f"{k}={int(v)}" for v, k in st[:8] if v > 0))
 src = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "sass"))))
-sh, sd = src[1], src[2:]
+sections, cur = [], None
+for row in src:  # one section per kernel: ["Kernel Name", name], header, rows
+    if row and row[0] == "Kernel Name":
+        cur = [row[1] if len(row) > 1 else "", None, []]
+        sections.append(cur)
+    elif cur is not None and cur[1] is None:
+        cur[1] = row
+    elif cur is not None:
+        cur[2].append(row)
+sec = next(x for x in sections if kre is None or kre.search(x[0]))
+sh = sec[1]
+sd = [row for row in sec[2] if len(row) == len(sh)]
 ix = {k: i for i, k in enumerate(sh)}
 f = lambda row, k: float(row[ix[k]].replace(",", "") or 0) if k in ix and row[ix[k]] else 0.0
 ops, wf, ex = Counter(), Counter(), Counter()
