@@ -529,6 +529,8 @@ struct ee_workspace {
   std::vector<Stager> stagers;
   long long* d_diag_acc = nullptr;
   bool diag_acc_dirty = true;
+  void* h_tune = nullptr;  // ee_tune results: mapped pinned memory the kernel writes
+  size_t tune_host_cap = 0;
   // axis-family sweep: per-CTA partial cells and their 64-bit totals
   uint32_t* d_axis_part = nullptr;
   size_t axis_part_cap = 0;
@@ -719,6 +721,7 @@ int ee_workspace_destroy(ee_workspace* ws) {
   if (ws->d_buf) cudaFree(ws->d_buf);
   if (ws->d_diag_acc) cudaFree(ws->d_diag_acc);
   if (ws->d_axis_part) cudaFree(ws->d_axis_part);
+  if (ws->h_tune) cudaFreeHost(ws->h_tune);
   if (ws->d_axis_tot) cudaFree(ws->d_axis_tot);
   if (ws->d_in) cudaFree(ws->d_in);
   for (auto& m : ws->marks) cudaEventDestroy(m.a), cudaEventDestroy(m.b);
@@ -1902,44 +1905,52 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
   if (trace_cap < 0 || (trace_cap > 0 && !h_trace)) return fail(EE_ERR_ARG, "bad trace buffer");
   std::lock_guard<std::mutex> lock(ws->mu);
   auto st = (cudaStream_t)stream;
-  const size_t serve_b = align_up((size_t)(r + 1) * 8, 256);
+  // results land in mapped pinned memory the kernel writes directly: one launch,
+  // one stream sync, no staging copies (the serve table travels in the parameters)
   const size_t out_b = align_up((size_t)(r + 2) * 8 + 4 * 4, 256);
   const size_t trace_b = align_up((size_t)std::max(trace_cap, 1) * r * 8, 256);
-  const size_t sites_b = align_up((size_t)(r + 1) * ((n + 7) & ~7), 256);
-  int rc = ws_reserve(ws, serve_b + out_b + trace_b + sites_b, serve_b);
+  if (out_b + trace_b > ws->tune_host_cap) {
+    if (ws->h_tune) EE_CUDA(cudaFreeHost(ws->h_tune));
+    ws->h_tune = nullptr;
+    EE_CUDA(cudaHostAlloc(&ws->h_tune, out_b + trace_b, cudaHostAllocMapped));
+    ws->tune_host_cap = out_b + trace_b;
+  }
+  unsigned char* hd = nullptr;
+  EE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hd), ws->h_tune, 0));
+  const size_t vals_b = align_up((size_t)(r + 1) * ((n + 7) & ~7) * 8, 256);
+  int rc = ws_reserve(ws, vals_b, 0);
   if (rc) return rc;
-  auto* d0 = static_cast<unsigned char*>(ws->d_buf);
-  std::memcpy(ws->h_stage, h_serve, (size_t)(r + 1) * 8);
-  EE_CUDA(cudaMemcpyAsync(d0, ws->h_stage, serve_b, cudaMemcpyHostToDevice, st));
-  EE_CUDA(cudaEventRecord(ws->staged, st));
-  double* d_out = reinterpret_cast<double*>(d0 + serve_b);
-  int* d_info = reinterpret_cast<int*>(d0 + serve_b + (size_t)(r + 2) * 8);
-  double* d_trace = reinterpret_cast<double*>(d0 + serve_b + out_b);
-  unsigned char* d_sites = d0 + serve_b + out_b + trace_b;
-  tunedev::Params p{acc_loss_budget, init_step, min_step, max_rounds, trace_cap};
+  double* d_vals = static_cast<double*>(ws->d_buf);
+  double* d_out = reinterpret_cast<double*>(hd);
+  int* d_info = reinterpret_cast<int*>(hd + (size_t)(r + 2) * 8);
+  double* d_trace = reinterpret_cast<double*>(hd + out_b);
+  tunedev::Params p{acc_loss_budget, init_step, min_step, max_rounds, trace_cap, {}};
+  for (int j = 0; j <= r; ++j) p.serve[j] = h_serve[j];
   const size_t n8 = (size_t)((n + 7) & ~7);
-  const size_t rows_b = n8 * 4 + (size_t)(r + 1) * n8;
+  const size_t rows_b = n8 * 4 + (size_t)(r + 1) * n8 * 8;
   const size_t win_b = (size_t)n * r * 8;
   const int rows_in = rows_b <= 120 * 1024;
   const int in_smem = rows_in && rows_b + win_b <= 200 * 1024;
   const size_t smem = rows_in ? rows_b + (in_smem ? win_b : 0) : 0;
-  if (smem)
+  static size_t smem_set = 48 * 1024;  // the attribute is raised once, to the largest need
+  if (smem > smem_set) {
     EE_CUDA(cudaFuncSetAttribute(tunedev::k_tune, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
+    smem_set = smem;
+  }
   {
     ProfScope ps(ws, st, "k_tune");
-    tunedev::k_tune<<<1, tunedev::THREADS, smem, st>>>(d_scores, d_bits, (int)n, r,
-                                                        reinterpret_cast<const double*>(d0),
-                                                        vanilla, p, d_sites, d_out, d_info,
-                                                        d_trace, in_smem, rows_in);
+    tunedev::k_tune<<<1, tunedev::THREADS, smem, st>>>(d_scores, d_bits, (int)n, r, vanilla, p,
+                                                        d_vals, d_out, d_info, d_trace, in_smem,
+                                                        rows_in);
   }
   EE_LAUNCH_CHECK();
-  EE_CUDA(cudaMemcpyAsync(h_out, d_out, (size_t)(r + 2) * 8, cudaMemcpyDeviceToHost, st));
-  EE_CUDA(cudaMemcpyAsync(h_info, d_info, 4 * 4, cudaMemcpyDeviceToHost, st));
   EE_CUDA(cudaStreamSynchronize(st));
+  const auto* hs = static_cast<const unsigned char*>(ws->h_tune);
+  std::memcpy(h_out, hs, (size_t)(r + 2) * 8);
+  std::memcpy(h_info, hs + (size_t)(r + 2) * 8, 4 * 4);
   const int rows = std::min(h_info[2], trace_cap);
-  if (rows > 0)
-    EE_CUDA(cudaMemcpy(h_trace, d_trace, (size_t)rows * r * 8, cudaMemcpyDeviceToHost));
+  if (rows > 0) std::memcpy(h_trace, hs + out_b, (size_t)rows * r * 8);
   return EE_OK;
 }
 

@@ -17,6 +17,7 @@ struct Params {
   double budget, init_step, min_step;
   int max_rounds;  // reference raises after 200000
   int trace_cap;   // rows of `trace` available (r doubles each)
+  double serve[MAXR + 1];  // serve table (by value: no staging copy)
 };
 
 // out_d: [0, r) thresholds, r: savings, r+1: accuracy
@@ -24,22 +25,22 @@ struct Params {
 //        2 did not terminate)
 __global__ void __launch_bounds__(THREADS, 1)
     k_tune(const double* __restrict__ s, const uint32_t* __restrict__ bits, int n, int r,
-           const double* __restrict__ serve, double vanilla, Params p,
-           unsigned char* __restrict__ sites, double* __restrict__ out_d, int* __restrict__ out_i,
+           double vanilla, const __grid_constant__ Params p,
+           double* __restrict__ vals, double* __restrict__ out_d, int* __restrict__ out_i,
            double* __restrict__ trace, int window_in_smem, int rows_in_smem) {
-  // Every round re-scans the window and folds the site rows sequentially, so
-  // both live in shared memory when they fit: [bits u32 n][sites (r+1) x n8][window]
+  // Every round re-scans the window and folds the addend rows sequentially, so
+  // both live in shared memory when they fit: [addends f64 (r+1) x n8][bits u32 n][window]
   extern __shared__ __align__(16) unsigned char sdyn[];
   const int n8s = (n + 7) & ~7;
   const double* win = s;
   const uint32_t* wbits = bits;
   if (rows_in_smem) {
-    uint32_t* sb = reinterpret_cast<uint32_t*>(sdyn);
+    vals = reinterpret_cast<double*>(sdyn);
+    uint32_t* sb = reinterpret_cast<uint32_t*>(sdyn + (size_t)(r + 1) * n8s * 8);
     for (int k = threadIdx.x; k < n; k += THREADS) sb[k] = bits[k];
     wbits = sb;
-    sites = sdyn + (size_t)n8s * 4;
     if (window_in_smem) {
-      double* sw = reinterpret_cast<double*>(sdyn + (size_t)n8s * 4 + (size_t)(r + 1) * n8s);
+      double* sw = reinterpret_cast<double*>(sdyn + (size_t)(r + 1) * n8s * 8 + (size_t)n8s * 4);
       for (int64_t k = threadIdx.x; k < (int64_t)n * r; k += THREADS) sw[k] = s[k];
       win = sw;
     }
@@ -48,54 +49,65 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ double sserve[MAXR + 1];
   __shared__ int elig[MAXR], nelig, done;
   __shared__ double acc_cur, sav_cur;
+  __shared__ int n_evals, n_rows, status;
   const int tid = threadIdx.x;
-  for (int j = tid; j <= r; j += THREADS) sserve[j] = serve[j];
+  for (int j = tid; j <= r; j += THREADS) sserve[j] = p.serve[j];
   if (tid < r) {
     th[tid] = 0.0;
     steps[tid] = p.init_step;
   }
   __syncthreads();
 
-  // exact evaluation of rows cand[0..nc): sites in parallel, then one thread per
-  // candidate folds samples in index order (same order as _exitcore.pyx:43-53)
-  // per-candidate site rows, padded to 8 samples so the fold reads 8 at a time
+  // exact evaluation of rows cand[0..nc): every sample's first exit in parallel,
+  // written as its serve value (the fold's addend) while the correct counts are
+  // summed with ballots (integer sums are order-free); then one thread per
+  // candidate folds the addends in index order (same order as
+  // _exitcore.pyx:43-53), a chain of n dependent adds with the next 8 addends
+  // always loaded ahead of it.
   const int n8 = (n + 7) & ~7;
+  __shared__ unsigned long long okc[MAXR + 1];
   auto evaluate = [&](int nc) {
+    if (tid <= MAXR) okc[tid] = 0;
+    __syncthreads();
+    const int lane = tid & 31;
     for (int c = 0; c < nc; ++c) {
-      for (int i = tid; i < n; i += THREADS) {
-        const double* row = win + (int64_t)i * r;
-        int site = r;
-        for (int j = r - 1; j >= 0; --j)  // branch-free: every score is read, earliest hit wins
-          if (row[j] < cand[c][j]) site = j;
-        sites[(int64_t)c * n8 + i] = (unsigned char)site;
+      for (int i0 = 0; i0 < n; i0 += THREADS) {  // warp-uniform trip count for the ballot
+        const int i = i0 + tid;
+        unsigned hit = 0;
+        if (i < n) {
+          const double* row = win + (int64_t)i * r;
+          int site = r;
+          for (int j = r - 1; j >= 0; --j)  // branch-free: every score is read, earliest hit wins
+            if (row[j] < cand[c][j]) site = j;
+          vals[(int64_t)c * n8 + i] = sserve[site];
+          hit = (wbits[i] >> site) & 1u;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0 && b) atomicAdd(&okc[c], (unsigned long long)__popc(b));
       }
     }
     __syncthreads();
     if (tid < nc) {
-      const unsigned char* st = sites + (int64_t)tid * n8;
-      long long ok = 0;
+      const double* vr = vals + (int64_t)tid * n8;
       double ms = 0.0;
       const int nfull = n & ~7;
+      double cur[8], nxt[8];
+      if (nfull > 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cur[q] = vr[q];
+      }
       for (int i0 = 0; i0 < nfull; i0 += 8) {
-        // 8 independent shared loads per step; only the fp64 adds form a chain
-        const uint2 sw = *reinterpret_cast<const uint2*>(st + i0);
-        double add[8];
+        const int i1 = i0 + 8 < nfull ? i0 + 8 : i0;  // loads ahead of the dependent adds
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int site = ((q < 4 ? sw.x : sw.y) >> (8 * (q & 3))) & 0xFF;
-          ok += (wbits[i0 + q] >> site) & 1u;
-          add[q] = sserve[site];
-        }
+        for (int q = 0; q < 8; ++q) nxt[q] = vr[i1 + q];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) ms = __dadd_rn(ms, add[q]);
+        for (int q = 0; q < 8; ++q) ms = __dadd_rn(ms, cur[q]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
       }
-      for (int i = nfull; i < n; ++i) {
-        const int site = st[i];
-        ok += (wbits[i] >> site) & 1u;
-        ms = __dadd_rn(ms, sserve[site]);
-      }
+      for (int i = nfull; i < n; ++i) ms = __dadd_rn(ms, vr[i]);
       const double dn = (double)n;
-      accs[tid] = __ddiv_rn((double)ok, dn);
+      accs[tid] = __ddiv_rn((double)okc[tid], dn);
       savs[tid] = __dsub_rn(vanilla, __ddiv_rn(ms, dn));
     }
     __syncthreads();
@@ -110,13 +122,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     acc_cur = accs[0];
     sav_cur = savs[0];
     done = 0;
-    out_i[0] = 0;
-    out_i[1] = 1;
-    out_i[2] = 0;
-    out_i[3] = 0;
+    // counters live in shared memory; out_i / trace may be mapped host memory
+    // (ee_tune), which the kernel only ever writes
+    n_evals = 1;
+    n_rows = 0;
+    status = 0;
     if (p.trace_cap > 0) {
       for (int j = 0; j < r; ++j) trace[j] = steps[j];
-      out_i[2] = 1;
+      n_rows = 1;
     }
   }
   __syncthreads();
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (nelig == 0) break;
     evaluate(nelig);
     if (tid == 0) {
-      out_i[1] += nelig;
+      n_evals += nelig;
       int best = -1;
       // key: (1, dsav, -i) when the increment loses no accuracy, else
       // (0, dsav / dloss, dsav, -i); lexicographic max (tuner.py:141-153)
@@ -205,13 +218,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             const double h = __ddiv_rn(steps[i], 2.0);
             steps[i] = p.min_step > h ? p.min_step : h;  // Python max(min_step, h)
           }
-        if (out_i[2] < p.trace_cap) {
-          for (int j = 0; j < r; ++j) trace[out_i[2] * r + j] = steps[j];
-          out_i[2] += 1;
+        if (n_rows < p.trace_cap) {
+          for (int j = 0; j < r; ++j) trace[n_rows * r + j] = steps[j];
+          n_rows += 1;
         }
         if (rounds > p.max_rounds) {
           done = 1;
-          out_i[3] = 2;
+          status = 2;
         }
       }
     }
@@ -219,11 +232,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (done) break;
   }
   if (tid == 0) {
+    if (status == 0 && acc_cur < __dsub_rn(floor, 1e-9)) status = 1;
     out_i[0] = rounds;
+    out_i[1] = n_evals;
+    out_i[2] = n_rows;
+    out_i[3] = status;
     for (int j = 0; j < r; ++j) out_d[j] = th[j];
     out_d[r] = sav_cur;
     out_d[r + 1] = acc_cur;
-    if (out_i[3] == 0 && acc_cur < __dsub_rn(floor, 1e-9)) out_i[3] = 1;
   }
 }
 
