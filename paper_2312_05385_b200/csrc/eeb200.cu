@@ -1023,29 +1023,30 @@ static int eval_diag(ee_workspace* ws, const double* d_scores, const uint32_t* d
 // Grid of the diagonal sweeps: one 1024-thread CTA per SM. Resident windows
 // leave one SM to the previous sweep's finalising CTA, so a stream of sweeps
 // overlaps each tail with the next sweep's loop.
-static unsigned diag_grid(const ee_workspace* ws, int64_t n) {
+static unsigned diag_grid(const ee_workspace* ws, int64_t n, int per_sm = 1, int warps = diag2::WARPS) {
   const int64_t nchunks = ceil_div(n, 32);
-  const int sms = ws->resident ? std::max(1, sm_count() - 1) : sm_count();
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(nchunks, diag2::WARPS)));
+  const int slots = sm_count() * per_sm;
+  const int ctas = ws->resident ? std::max(1, slots - 1) : slots;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, ceil_div(nchunks, warps)));
 }
 template <class K>
 static cudaError_t launch_diag_kernel(K k, const char* name, int smem, bool& attr_set,
                                       const diag2::Params& p, int64_t n, cudaStream_t st,
-                                      ee_workspace* ws) {
+                                      ee_workspace* ws, int threads = diag2::THREADS) {
   if (!attr_set) {  // once per instantiation (a driver call)
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const unsigned grid = diag_grid(ws, n);
+  const unsigned grid = diag_grid(ws, n, 1024 / threads, threads / 32);
   ProfScope ps(ws, st, name);  // events bracket the launch itself
   if (!ws->resident) {
-    k<<<grid, diag2::THREADS, smem, st>>>(p);
+    k<<<grid, threads, smem, st>>>(p);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(diag2::THREADS);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1065,11 +1066,14 @@ static cudaError_t launch_diag2(const diag2::Params& p, int64_t n, int upd, cuda
                                        attr_set[0], p, n, st, ws);
 }
 template <int R>
-static cudaError_t launch_diag3(const diag2::Params& p, int64_t n, cudaStream_t st,
+static cudaError_t launch_diag3(const diag2::Params& p, int64_t n, bool pair, cudaStream_t st,
                                 ee_workspace* ws) {
-  static bool attr_set = false;
-  return launch_diag_kernel(diag3::k_diag3<R>, "k_diag3", diag3::smem_bytes<R>(), attr_set, p, n,
-                            st, ws);
+  static bool attr_set[2] = {false, false};
+  if (pair)
+    return launch_diag_kernel(diag3::k_diag3<R, 512, 16>, "k_diag3",
+                              diag3::Pair::smem_bytes<R>(), attr_set[1], p, n, st, ws, 512);
+  return launch_diag_kernel(diag3::k_diag3<R, 1024, 32>, "k_diag3", diag3::Big::smem_bytes<R>(),
+                            attr_set[0], p, n, st, ws, 1024);
 }
 extern "C" {
 
@@ -1166,18 +1170,20 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
   cudaError_t e;
   const int upd = ws->diag_version == 3 ? 0 : 1;
   // k_diag3 (lane-private cumulative counters) where its envelope holds
+  const bool pair = ws->diag_version == 5;  // two 512-thread CTAs per SM
   const bool v3 = ws->diag_version >= 4 && m <= diag3::MAX_M &&
-                  ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n)) <= diag3::MAX_CTA_CHUNKS;
+                  ceil_div(ceil_div(n, 32), (int64_t)(pair ? diag_grid(ws, n, 2, 16) : diag_grid(ws, n))) <=
+                      (pair ? diag3::Pair::MAX_CTA_CHUNKS : diag3::Big::MAX_CTA_CHUNKS);
   if (v3) {
     switch (r) {
-      case 2: e = launch_diag3<2>(p, n, st, ws); break;
-      case 4: e = launch_diag3<4>(p, n, st, ws); break;
-      case 6: e = launch_diag3<6>(p, n, st, ws); break;
-      case 8: e = launch_diag3<8>(p, n, st, ws); break;
-      case 10: e = launch_diag3<10>(p, n, st, ws); break;
-      case 12: e = launch_diag3<12>(p, n, st, ws); break;
-      case 14: e = launch_diag3<14>(p, n, st, ws); break;
-      default: e = launch_diag3<16>(p, n, st, ws); break;
+      case 2: e = launch_diag3<2>(p, n, pair, st, ws); break;
+      case 4: e = launch_diag3<4>(p, n, pair, st, ws); break;
+      case 6: e = launch_diag3<6>(p, n, pair, st, ws); break;
+      case 8: e = launch_diag3<8>(p, n, pair, st, ws); break;
+      case 10: e = launch_diag3<10>(p, n, pair, st, ws); break;
+      case 12: e = launch_diag3<12>(p, n, pair, st, ws); break;
+      case 14: e = launch_diag3<14>(p, n, pair, st, ws); break;
+      default: e = launch_diag3<16>(p, n, pair, st, ws); break;
     }
   } else {
     switch (r) {
@@ -1822,7 +1828,7 @@ int ee_workspace_set_special(ee_workspace* ws, int32_t on) {
 
 int ee_workspace_set_diag_version(ee_workspace* ws, int32_t version) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
-  if (version < 1 || version > 4) return fail(EE_ERR_ARG, "diagonal kernel version must be 1..4");
+  if (version < 1 || version > 5) return fail(EE_ERR_ARG, "diagonal kernel version must be 1..5");
   std::lock_guard<std::mutex> lock(ws->mu);
   ws->diag_version = version;
   return EE_OK;

@@ -27,33 +27,44 @@
 namespace diag3 {
 
 using diag2::Params;
-constexpr int THREADS = diag2::THREADS;
-constexpr int WARPS = diag2::WARPS;
 constexpr int MAX_M = 64;
-constexpr int CELLS = MAX_M + 1;          // positions 0..m (m = sink)
-constexpr int ROWC = CELLS * 32 * 4;      // bytes per ramp: [cell][lane] u32
-constexpr int MAX_CTA_CHUNKS = 32767;     // chunks per CTA: updates per lane copy of a cell < 2^15
-constexpr int OFF_TAB = diag2::OFF_TAB;
-constexpr int OFF_SU = diag2::OFF_SU;
-constexpr int OFF_KEY = diag2::OFF_KEY;
-template <int R>
-__host__ __device__ constexpr int off_c() { return OFF_KEY + WARPS * 32 * R; }
-template <int R>
-__host__ __device__ constexpr int smem_bytes() { return off_c<R>() + R * ROWC; }
-// after the loop: per-CTA F [R][64] (i32) in the key buffer
-// last CTA: finalisation scratch over the cell rows
-template <int R>
-__host__ __device__ constexpr int fin_bytes() {
-  return 3 * (R + 1) * CELLS * 8 + 3 * CELLS * 8;
-}
+constexpr int CELLS = MAX_M + 1;  // positions 0..m (m = sink)
 
-template <int R>
-__global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Params P) {
+// Shape of one variant: NT threads per CTA; CP copies of every cell and of the
+// bin table (lane l uses copy l % CP). CP = 32 makes every update and table
+// read conflict-free; CP = 16 halves that shared memory (lanes l and l + 16
+// share a copy, at most 2-way conflicts) so two 512-thread CTAs fit one SM and
+// one CTA's prologue / fold overlaps the other's streaming.
+template <int NT, int CP>
+struct Cfg {
+  static constexpr int THREADS = NT;
+  static constexpr int WARPS = NT / 32;
+  static constexpr int OFF_TAB = 0;                                   // u32 [NB][CP]
+  static constexpr int OFF_SU = OFF_TAB + diag2::NB * CP * 4;         // f64 [128][SU_REP]
+  static constexpr int OFF_KEY = OFF_SU + (diag2::MAX_M + 1) * diag2::SU_STRIDE;  // u8 [WARPS][32 R]
+  static constexpr int ROWC = CELLS * CP * 4;                         // bytes per ramp: [cell][copy]
+  // updates per copy of a cell: 32 / CP lanes x one per chunk, kept < 2^15
+  static constexpr int MAX_CTA_CHUNKS = 32767 / (32 / CP);
+  template <int R>
+  __host__ __device__ static constexpr int off_c() { return OFF_KEY + WARPS * 32 * R; }
+  template <int R>
+  __host__ __device__ static constexpr int smem_bytes() { return off_c<R>() + R * ROWC; }
+  template <int R>  // last CTA: finalisation scratch over the cell rows
+  __host__ __device__ static constexpr int fin_bytes() { return 3 * (R + 1) * CELLS * 8 + 3 * CELLS * 8; }
+};
+using Big = Cfg<1024, 32>;   // one CTA per SM
+using Pair = Cfg<512, 16>;   // two CTAs per SM
+
+template <int R, int NT, int CP>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_diag3(const __grid_constant__ Params P) {
+  using C = Cfg<NT, CP>;
+  constexpr int THREADS = C::THREADS, WARPS = C::WARPS, ROWC = C::ROWC;
+  constexpr int OFF_TAB = C::OFF_TAB, OFF_SU = C::OFF_SU, OFF_KEY = C::OFF_KEY;
   static_assert(R % 2 == 0 && R >= 2 && R <= diag2::RMAX, "even R only");
-  static_assert(fin_bytes<R>() <= R * ROWC, "finalisation scratch fits the cell rows");
+  static_assert(C::template fin_bytes<R>() <= R * ROWC, "finalisation scratch fits the cell rows");
   static_assert(R * MAX_M * 4 <= WARPS * 32 * R, "per-CTA sums fit the key buffer");
   constexpr int NW = (R + 3) / 4;
-  constexpr int OFF_C = off_c<R>();
+  constexpr int OFF_C = C::template off_c<R>();
   using diag2::lds_f64;
   using diag2::lds_u32;
   using diag2::Unroll;
@@ -101,37 +112,46 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 0] = diag2::gtimer();
   // Parameter reads first: a constant-bank miss issued after the window's
   // loads queues behind them (measured: a 2 us prologue).
-  static_assert(diag2::NB * 8 == 2 * THREADS && (diag2::MAX_M + 1) * diag2::SU_REP / 2 == THREADS,
-                "one table pair and one threshold pair per thread");
-  const uint32_t te0 = P.tab[tid >> 3], te1 = P.tab[(tid + THREADS) >> 3];
-  const int tu = tid / (diag2::SU_REP / 2);
-  const double ue = tu < m ? P.u[tu] : __longlong_as_double(0x7ff8000000000000LL);
+  constexpr int TQ = diag2::NB * CP / 4 / THREADS;                        // table uint4 per thread
+  constexpr int SQ = (diag2::MAX_M + 1) * diag2::SU_REP / 2 / THREADS;    // threshold pairs per thread
+  static_assert(TQ * THREADS * 4 == diag2::NB * CP && SQ * THREADS * 2 == (diag2::MAX_M + 1) * diag2::SU_REP,
+                "whole table / threshold pairs per thread");
+  uint32_t te[TQ];
+  double ue[SQ];
+#pragma unroll
+  for (int i = 0; i < TQ; ++i) te[i] = P.tab[(tid + i * THREADS) / (CP / 4)];
+#pragma unroll
+  for (int i = 0; i < SQ; ++i) {
+    const int tu = (tid + i * THREADS) / (diag2::SU_REP / 2);
+    ue[i] = tu < m ? P.u[tu] : __longlong_as_double(0x7ff8000000000000LL);
+  }
   load(ch);  // first HBM round trip overlaps the prologue
 
   // ---- prologue (vector stores): zeroed cells, replicated bin table and thresholds
   {
     uint4* c4 = reinterpret_cast<uint4*>(cells);
-    const int per_ramp = (m + 1) * 8;  // uint4 per ramp row in use (cells 0..m)
+    const int per_ramp = (m + 1) * CP / 4;  // uint4 per ramp row in use (cells 0..m)
     for (int q = tid; q < R * per_ramp; q += THREADS) {
       const int j = q / per_ramp;
-      c4[j * CELLS * 8 + (q - j * per_ramp)] = make_uint4(0u, 0u, 0u, 0u);
+      c4[j * CELLS * CP / 4 + (q - j * per_ramp)] = make_uint4(0u, 0u, 0u, 0u);
     }
     if (tid < MAX_M) s_osum[tid] = 0;
     if (tid == 0) s_corr = 0;
-    uint4* t4 = reinterpret_cast<uint4*>(stab);  // 8 uint4 per bin (32 copies)
-    t4[tid] = make_uint4(te0, te0, te0, te0);
-    t4[tid + THREADS] = make_uint4(te1, te1, te1, te1);
-    reinterpret_cast<double2*>(su)[tid] = make_double2(ue, ue);
+    uint4* t4 = reinterpret_cast<uint4*>(stab);  // CP / 4 uint4 per bin
+#pragma unroll
+    for (int i = 0; i < TQ; ++i) t4[tid + i * THREADS] = make_uint4(te[i], te[i], te[i], te[i]);
+#pragma unroll
+    for (int i = 0; i < SQ; ++i) reinterpret_cast<double2*>(su)[tid + i * THREADS] = make_double2(ue[i], ue[i]);
   }
   __syncthreads();
 
   const double pa = P.a, pc0 = P.c0;
   const uint32_t smb = (uint32_t)__cvta_generic_to_shared(sm);
-  const uint32_t tb = smb + OFF_TAB + (uint32_t)lane * 4;
+  const uint32_t tb = smb + OFF_TAB + (uint32_t)(lane % CP) * 4;
   const uint32_t sub = smb + OFF_SU + (uint32_t)(lane % diag2::SU_REP) * 8;
-  const uint32_t cB = smb + OFF_C + (uint32_t)lane * 4;  // this lane's copy of every cell
+  const uint32_t cB = smb + OFF_C + (uint32_t)(lane % CP) * 4;  // this lane's copy of every cell
   auto keyof = [&](double x) -> uint32_t {
-    uint32_t e = lds_u32(tb + diag2::bin_of(x, pa, pc0) * 128u);
+    uint32_t e = lds_u32(tb + diag2::bin_of(x, pa, pc0) * (CP * 4u));
     const double t = lds_f64(sub + (e >> 16));
     asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
         : "+r"(e)
@@ -196,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
       const uint32_t kj = __byte_perm(kw[j >> 2], 0, 0x4440 | (j & 3));
       prev = kj < prev ? kj : prev;
       const uint32_t val = 1u + ((cbc << (16 - j)) & 0x10000u) - ((cbc << (15 - j)) & 0x10000u);
-      diag2::red_shared<j * ROWC>(cB + prev * 128u, (int)val);
+      diag2::red_shared<j * ROWC>(cB + prev * (CP * 4u), (int)val);
     });
     corr += (cbc >> R) & 1u;
   }
@@ -217,11 +237,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_diag3(const __grid_constant__ Pa
   int* cF = reinterpret_cast<int*>(skey);  // F [R][MAX_M] raw per-position counts
   for (int q = tid; q < R * m; q += THREADS) {
     const int j = q / m, p = q - j * m;
-    const uint32_t* cell = cells + (j * CELLS + p) * 32;
+    const uint32_t* cell = cells + (j * CELLS + p) * CP;
     int lo = 0, hi = 0;
 #pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const uint32_t w = cell[(k + lane) & 31];
+    for (int k = 0; k < CP; ++k) {
+      const uint32_t w = cell[(k + lane) % CP];
       lo += (int)(w & 0xffffu);
       hi += (int)(short)(w >> 16);  // each copy's high half is its exact signed sum mod 2^16
     }
