@@ -198,6 +198,11 @@ int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float
  * [b, c] (round to nearest even): the A operand of a large ramp head. */
 int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t hw, void* d_out,
                  void* stream);
+/* The same pool for a channels_last (NHWC) map [B, HW, C]: C contiguous, so a
+ * CTA reads 64-channel rows and its 16 thread rows split the spatial extent
+ * (no NCHW copy first). c must be a multiple of 4, d_x 8-byte aligned. */
+int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t hw,
+                      void* d_out, void* stream);
 
 /* Gathers rows d_keep[0 .. *d_nkeep) of d_src (row_bytes each, multiple of
  * 16) into the dense d_dst (capacity max_rows rows): downstream blocks then

@@ -2046,8 +2046,12 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
   } else {
     ProfScope ps(ws, st, "k_exit_logits");
     const int rows_per = exitc::THREADS / 32;
-    exitc::k_exit_logits<<<(unsigned)ceil_div(b, rows_per), exitc::THREADS, 0, st>>>(
-        d_logits_in, b, k, conf, threshold, d_threshold, d_alive, o);
+    const unsigned grid = (unsigned)ceil_div(b, rows_per);
+    auto kern = k <= 64 ? exitc::k_exit_logits<2>
+                : k <= 256 ? exitc::k_exit_logits<8>
+                : k <= 1024 ? exitc::k_exit_logits<32>
+                            : exitc::k_exit_logits<64>;
+    kern<<<grid, exitc::THREADS, 0, st>>>(d_logits_in, b, k, conf, threshold, d_threshold, d_alive, o);
   }
   EE_LAUNCH_CHECK();
   return EE_OK;
@@ -2173,6 +2177,23 @@ int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t 
   else
     gemmtc::k_pool_bf16<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         static_cast<const float*>(d_x), bc, hw, static_cast<uint16_t*>(d_out));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t hw,
+                      void* d_out, void* stream) {
+  if (b < 1 || c < 1 || hw < 1 || b > 65535) return fail(EE_ERR_ARG, "bad shape");
+  if (c % 4) return fail(EE_ERR_ARG, "channels must be a multiple of 4");
+  if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
+  if (reinterpret_cast<uintptr_t>(d_x) % (x_bf16 ? 8 : 16)) return fail(EE_ERR_ARG, "misaligned map");
+  const dim3 grid((unsigned)ceil_div(c, 64), (unsigned)b);
+  if (x_bf16)
+    gemmtc::k_pool_nhwc<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const uint16_t*>(d_x), c, hw, static_cast<uint16_t*>(d_out));
+  else
+    gemmtc::k_pool_nhwc<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const float*>(d_x), c, hw, static_cast<uint16_t*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

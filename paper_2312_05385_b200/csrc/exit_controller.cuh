@@ -163,7 +163,44 @@ __global__ void __launch_bounds__(THREADS)
   const int64_t row = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const float inv = 1.f / (float)HW;
-  if (nhwc || HW == 1) {
+  if ((nhwc || HW == 1) && C % 4 == 0 && C <= 4 * THREADS &&
+      (reinterpret_cast<uintptr_t>(feat) & (4 * sizeof(TF) - 1)) == 0) {
+    // channels contiguous: a thread owns 4 channels (one 8/16-byte load per
+    // position) and the CTA's threads split the positions into THREADS / (C/4)
+    // slices, so every thread keeps loads in flight; slices meet in shared memory
+    __shared__ float4 part[THREADS];
+    const int G = C / 4, S = THREADS / G;
+    const int g = threadIdx.x % G, sl = threadIdx.x / G;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sl < S) {
+      const TF* base = feat + row * (int64_t)HW * C + 4 * g;
+#pragma unroll 4
+      for (int p = sl; p < HW; p += S) {
+        const TF* q = base + (int64_t)p * C;
+        if constexpr (sizeof(TF) == 2) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(q));
+          acc.x += __uint_as_float(v.x << 16);
+          acc.y += __uint_as_float(v.x & 0xffff0000u);
+          acc.z += __uint_as_float(v.y << 16);
+          acc.w += __uint_as_float(v.y & 0xffff0000u);
+        } else {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(q));
+          acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+        }
+      }
+    }
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += THREADS) {
+      const int gc = c / 4, k = c % 4;
+      float t = 0.f;
+      for (int q = 0; q < S; ++q) {
+        const float4 v = part[q * G + gc];
+        t += k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+      }
+      pooled[c] = t * inv;
+    }
+  } else if (nhwc || HW == 1) {
     // channels contiguous: threads over channels, loop over positions
     const TF* base = feat + row * (int64_t)HW * C;
     for (int c = threadIdx.x; c < C; c += THREADS) {
@@ -217,7 +254,66 @@ __global__ void __launch_bounds__(THREADS)
   if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
 }
 
-// confidence + compare + compaction from precomputed logits [B, K] (fp32)
+// confidence() with the row held in registers (NPL values per lane, K <= 32
+// NPL): every load is issued before the first compare, instead of one L2 round
+// trip per 32 logits per pass. Same per-lane order and reductions, so the same
+// bits as confidence().
+template <int NPL>
+__device__ __forceinline__ void confidence_reg(const float* __restrict__ l, int K, int conf,
+                                               float* err_out, int* label_out) {
+  const int lane = threadIdx.x & 31;
+  float v[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int k = lane + 32 * i;
+    v[i] = k < K ? __ldg(l + k) : 0.f;
+  }
+  float mx = -INFINITY;
+  int arg = 0x7fffffff;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int k = lane + 32 * i;
+    if (k < K && (v[i] > mx || (v[i] == mx && k < arg))) {
+      mx = v[i];
+      arg = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const int a2 = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (m2 > mx || (m2 == mx && a2 < arg)) {
+      mx = m2;
+      arg = a2;
+    }
+  }
+  float se = 0.f, sle = 0.f;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    if (lane + 32 * i < K) {
+      const float d = v[i] - mx;
+      const float e = expf(d);
+      se += e;
+      sle += d * e;
+    }
+  }
+  se = warp_sum(se);
+  sle = warp_sum(sle);
+  float err;
+  if (conf == 0) {
+    err = 1.f - 1.f / se;
+  } else {
+    const float H = logf(se) - sle / se;
+    err = K > 1 ? H / logf((float)K) : 0.f;
+  }
+  err = fminf(fmaxf(err, 0.f), 1.f);
+  *err_out = err;
+  *label_out = arg;
+}
+
+// confidence + compare + compaction from precomputed logits [B, K] (fp32);
+// NPL > 0: the row is held in registers (K <= 32 NPL)
+template <int NPL>
 __global__ void __launch_bounds__(THREADS)
     k_exit_logits(const float* __restrict__ logits_in, int64_t B, int K, int conf,
                   double threshold, const double* __restrict__ d_threshold,
@@ -228,7 +324,10 @@ __global__ void __launch_bounds__(THREADS)
   if (row < B) {
     float err;
     int label;
-    confidence(logits_in + row * K, K, conf, &err, &label);
+    if constexpr (NPL > 0)
+      confidence_reg<NPL>(logits_in + row * K, K, conf, &err, &label);
+    else
+      confidence(logits_in + row * K, K, conf, &err, &label);
     if (lane == 0) {
       const bool alive = alive_in ? alive_in[row] != 0 : true;
       const bool ex = alive && (double)err < threshold;

@@ -244,4 +244,46 @@ __global__ void k_pool_bf16(const T* __restrict__ x, int64_t BC, int HW,
   }
 }
 
+// global average pool of a channels_last map [B, HW, C] -> bf16 [B, C]:
+// CTA (b, 64-channel block); 16 x 16 threads, thread (ty, tx) sums channels
+// 4 tx .. 4 tx + 3 over positions ty, ty + 16, ...; rows meet in shared memory.
+template <typename T>
+__global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ x, int C, int HW,
+                                                   uint16_t* __restrict__ out) {
+  __shared__ float part[16][64 + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int b = blockIdx.y, c0 = blockIdx.x * 64 + 4 * tx;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (c0 < C) {
+    const T* base = x + ((int64_t)b * HW) * C + c0;
+    int p = ty;
+#pragma unroll 4
+    for (; p < HW; p += 16) {
+      if constexpr (sizeof(T) == 2) {
+        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(base + (int64_t)p * C));
+        a0 += __uint_as_float(v.x << 16);
+        a1 += __uint_as_float(v.x & 0xffff0000u);
+        a2 += __uint_as_float(v.y << 16);
+        a3 += __uint_as_float(v.y & 0xffff0000u);
+      } else {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(base + (int64_t)p * C));
+        a0 += v.x, a1 += v.y, a2 += v.z, a3 += v.w;
+      }
+    }
+  }
+  part[ty][4 * tx] = a0;
+  part[ty][4 * tx + 1] = a1;
+  part[ty][4 * tx + 2] = a2;
+  part[ty][4 * tx + 3] = a3;
+  __syncthreads();
+  if (threadIdx.x < 64 && blockIdx.x * 64 + (int)threadIdx.x < C) {
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc += part[r][threadIdx.x];
+    uint32_t u = __float_as_uint(acc / (float)HW);
+    u += 0x7FFF + ((u >> 16) & 1);  // round to nearest even bf16
+    out[(int64_t)b * C + blockIdx.x * 64 + threadIdx.x] = (uint16_t)(u >> 16);
+  }
+}
+
 }  // namespace gemmtc

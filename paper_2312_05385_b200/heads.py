@@ -194,13 +194,21 @@ def linear_tc(x, weight, bias=None, *, splits: int = 0, out_bf16: bool = False):
 
 
 def pool_bf16(x):
-    """Global average pool of an NCHW fp32/bf16 map to a bf16 [B, C] GEMM operand."""
+    """Global average pool of an NCHW or channels_last fp32/bf16 map to a bf16 [B, C]
+    GEMM operand."""
     torch = nat.torch_cuda()
     if x.dtype not in (torch.float32, torch.bfloat16) or x.dim() != 4:
         raise ParameterError("pool_bf16 takes an fp32 or bf16 [B, C, H, W] tensor")
-    x = x.contiguous()
     b, c, h, w = x.shape
     out = torch.empty((b, c), dtype=torch.bfloat16, device="cuda")
+    if (x.is_contiguous(memory_format=torch.channels_last) and not x.is_contiguous()
+            and c % 4 == 0 and b <= 65535):
+        # channels_last map: pooled in place, no NCHW copy
+        nat.check(nat.load_library().ee_pool_nhwc_bf16(
+            x.data_ptr(), int(x.dtype == torch.bfloat16), b, c, h * w, out.data_ptr(),
+            nat.stream_handle(torch)))
+        return out
+    x = x.contiguous()
     nat.check(nat.load_library().ee_pool_bf16(x.data_ptr(), int(x.dtype == torch.bfloat16), b, c,
                                               h * w, out.data_ptr(), nat.stream_handle(torch)))
     return out

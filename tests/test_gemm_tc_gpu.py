@@ -55,6 +55,21 @@ def test_large_ramp_head_end_to_end(cuda):
     assert torch.allclose(res.err.cpu().double(), err_ref, atol=2e-5, rtol=0)
 
 
+@pytest.mark.parametrize("b,c,h,w,dtype", [(256, 256, 56, 56, torch.bfloat16), (3, 2048, 7, 7, torch.bfloat16),
+                                           (5, 68, 9, 11, torch.float32), (2, 1024, 14, 14, torch.float32)])
+def test_pool_channels_last_matches_nchw(cuda, b, c, h, w, dtype):
+    """channels_last maps are pooled in place (k_pool_nhwc, no NCHW copy): each
+    mean within one bf16 rounding of the fp64 mean; the NCHW path agrees the same way."""
+    g = torch.Generator(device="cuda").manual_seed(b + c + h)
+    x = torch.randn(b, c, h, w, generator=g, device="cuda").to(dtype)
+    xl = x.contiguous(memory_format=torch.channels_last)
+    assert not xl.is_contiguous()
+    ref = x.double().mean(dim=(2, 3))
+    for got in (pool_bf16(xl), pool_bf16(x)):
+        tol = ref.abs().to(torch.float64) * 2.0 ** -8 + 1e-6  # one bf16 ulp (8-bit mantissa)
+        assert ((got.double() - ref).abs() <= tol).all(), (got.double() - ref).abs().max()
+
+
 @pytest.mark.parametrize("m,n,k", [(32, 3072, 1024), (32, 50257, 1024), (160, 4096, 1024),
                                    (1000, 700, 136), (8192, 2304, 768), (8192, 768, 3072)])
 def test_gemm_bf16_out_and_backbone_shapes(cuda, m, n, k):

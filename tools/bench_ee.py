@@ -4,8 +4,9 @@ For each config: thresholds from per-ramp err quantiles of a calibration
 batch, then timed batches (CUDA events) in feedback mode (Apparate:
 every input runs to completion, results released early) and compaction mode.
 Reports samples/s, p50 batch latency, p50 per-request release latency, exit
-rate, and the same model without ramps (vanilla) for context. bf16 autocast
-for the backbone; ramp heads take bf16 activations."""
+rate, and the same model without ramps (vanilla, eager and as one CUDA graph)
+for context. Backbones run in bf16 (see DTYPE_NOTE); ramp heads take the bf16
+activations."""
 import json
 import os
 import sys
@@ -78,27 +79,84 @@ def bench(name, pipe, make_input, batch, iters, warmup=5):
             ev1.synchronize()
             ts.append(ev0.elapsed_time(ev1))
     out["vanilla"] = {"samples_per_s": batch / (np.mean(ts) / 1e3), "p50_batch_ms": float(np.percentile(ts, 50))}
+    # vanilla captured as one CUDA graph too (the fair partner of feedback_graph)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.no_grad(), torch.cuda.stream(s):
+        for _ in range(2):
+            h = x
+            for st in pipe.stages:
+                h = st(h)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.no_grad(), torch.cuda.graph(g):
+        h = x
+        for st in pipe.stages:
+            h = st(h)
+    ts = []
+    for _ in range(warmup):
+        g.replay()
+    for _ in range(iters):
+        ev0.record()
+        g.replay()
+        ev1.record()
+        ev1.synchronize()
+        ts.append(ev0.elapsed_time(ev1))
+    out["vanilla_graph"] = {"samples_per_s": batch / (np.mean(ts) / 1e3),
+                            "p50_batch_ms": float(np.percentile(ts, 50))}
+    out["dtype"] = DTYPE_NOTE
     return out
 
 
+# Backbones in bf16 weights and activations (ResNets channels_last, the layout
+# cuDNN's tensor-core convolutions want); EE_BENCH_AUTOCAST=1 restores the
+# earlier fp32-weights + bf16-autocast setup for comparison.
+AUTOCAST = os.environ.get("EE_BENCH_AUTOCAST") == "1"
+DTYPE_NOTE = ("bf16 autocast over fp32 weights" if AUTOCAST
+              else "bf16 weights/activations, channels_last convolutions")
+
+
+def _native_bf16(model, channels_last):
+    if AUTOCAST:
+        return
+    if channels_last:
+        model.to(memory_format=torch.channels_last)
+    model.to(torch.bfloat16)
+
+
+def _image(g, channels_last):
+    def make(b, shape):
+        x = torch.randn(b, *shape, generator=g, device="cuda")
+        if AUTOCAST:
+            return x
+        return x.to(torch.bfloat16).contiguous(memory_format=torch.channels_last if channels_last
+                                               else torch.contiguous_format)
+    return make
+
+
 def main():
+    import contextlib
+
     torch.backends.cudnn.benchmark = True
     which = sys.argv[1:] or ["1", "2", "3"]
     g = torch.Generator(device="cuda").manual_seed(0)
+    img = _image(g, True)
     res = []
-    with torch.autocast("cuda", dtype=torch.bfloat16):
+    ctx = torch.autocast("cuda", dtype=torch.bfloat16) if AUTOCAST else contextlib.nullcontext()
+    with ctx:
         if "1" in which:
-            pipe, _ = ee_infer.resnet18_cifar()
-            res.append(bench("resnet18_cifar_6ramps", pipe,
-                             lambda b: torch.randn(b, 3, 32, 32, generator=g, device="cuda"), 32, 50))
+            pipe, m = ee_infer.resnet18_cifar()
+            _native_bf16(m, True)
+            res.append(bench("resnet18_cifar_6ramps", pipe, lambda b: img(b, (3, 32, 32)), 32, 50))
         if "2" in which:
-            pipe, _ = ee_infer.bert_base()
+            pipe, m = ee_infer.bert_base()
+            _native_bf16(m, False)
             res.append(bench("bert_base_12ramps_seq128_entropy", pipe,
                              lambda b: torch.randint(0, 30522, (b, 128), generator=g, device="cuda"), 64, 20))
         if "3" in which:
-            pipe, _ = ee_infer.resnet50_imagenet()
-            res.append(bench("resnet50_imagenet_16ramps", pipe,
-                             lambda b: torch.randn(b, 3, 224, 224, generator=g, device="cuda"), 256, 10))
+            pipe, m = ee_infer.resnet50_imagenet()
+            _native_bf16(m, True)
+            res.append(bench("resnet50_imagenet_16ramps", pipe, lambda b: img(b, (3, 224, 224)), 256, 10))
     for r in res:
         print(json.dumps(r))
 
