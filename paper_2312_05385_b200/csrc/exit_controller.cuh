@@ -174,20 +174,27 @@ __global__ void __launch_bounds__(THREADS)
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sl < S) {
       const TF* base = feat + row * (int64_t)HW * C + 4 * g;
-#pragma unroll 4
-      for (int p = sl; p < HW; p += S) {
-        const TF* q = base + (int64_t)p * C;
+      using V = typename std::conditional<sizeof(TF) == 2, uint2, float4>::type;
+      auto add = [&](const V& v) {
         if constexpr (sizeof(TF) == 2) {
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(q));
           acc.x += __uint_as_float(v.x << 16);
           acc.y += __uint_as_float(v.x & 0xffff0000u);
           acc.z += __uint_as_float(v.y << 16);
           acc.w += __uint_as_float(v.y & 0xffff0000u);
         } else {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(q));
           acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
         }
+      };
+      constexpr int DEPTH = 8;  // loads issued before any is consumed
+      int p = sl;
+      for (; p + (DEPTH - 1) * S < HW; p += DEPTH * S) {
+        V v[DEPTH];
+#pragma unroll
+        for (int i = 0; i < DEPTH; ++i) v[i] = __ldg(reinterpret_cast<const V*>(base + (int64_t)(p + i * S) * C));
+#pragma unroll
+        for (int i = 0; i < DEPTH; ++i) add(v[i]);
       }
+      for (; p < HW; p += S) add(__ldg(reinterpret_cast<const V*>(base + (int64_t)p * C)));
     }
     part[threadIdx.x] = acc;
     __syncthreads();

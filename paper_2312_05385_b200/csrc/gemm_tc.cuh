@@ -256,20 +256,27 @@ __global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ x, int 
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   if (c0 < C) {
     const T* base = x + ((int64_t)b * HW) * C + c0;
-    int p = ty;
-#pragma unroll 4
-    for (; p < HW; p += 16) {
+    using V = typename std::conditional<sizeof(T) == 2, uint2, float4>::type;
+    auto add = [&](const V& v) {
       if constexpr (sizeof(T) == 2) {
-        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(base + (int64_t)p * C));
         a0 += __uint_as_float(v.x << 16);
         a1 += __uint_as_float(v.x & 0xffff0000u);
         a2 += __uint_as_float(v.y << 16);
         a3 += __uint_as_float(v.y & 0xffff0000u);
       } else {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(base + (int64_t)p * C));
         a0 += v.x, a1 += v.y, a2 += v.z, a3 += v.w;
       }
+    };
+    constexpr int DEPTH = 8;  // loads issued before any is consumed
+    int p = ty;
+    for (; p + (DEPTH - 1) * 16 < HW; p += DEPTH * 16) {
+      V v[DEPTH];
+#pragma unroll
+      for (int i = 0; i < DEPTH; ++i) v[i] = __ldcs(reinterpret_cast<const V*>(base + (int64_t)(p + 16 * i) * C));
+#pragma unroll
+      for (int i = 0; i < DEPTH; ++i) add(v[i]);
     }
+    for (; p < HW; p += 16) add(__ldcs(reinterpret_cast<const V*>(base + (int64_t)p * C)));
   }
   part[ty][4 * tx] = a0;
   part[ty][4 * tx + 1] = a1;
