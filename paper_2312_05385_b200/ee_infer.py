@@ -184,6 +184,39 @@ class GraphRunner:
 
 
 # ---------------------------------------------------------------- model builders
+def fold_batchnorm(model):
+    """Fold every eval-mode BatchNorm2d of a torchvision ResNet into the conv
+    before it (w' = w * g / sqrt(v + eps) per output channel, b' = beta - mu * g /
+    sqrt(v + eps)) and turn the BatchNorm into an identity, in place. The
+    pipeline stages hold the same module objects, so they see the folded
+    convolutions: one conv (+ bias) kernel instead of conv + BN kernels.
+    (Model preparation only: it runs wherever the weights live.)"""
+    import torch
+
+    def fold(conv, bn):
+        with torch.no_grad():
+            scale = bn.weight.float() / torch.sqrt(bn.running_var.float() + bn.eps)
+            conv.weight.mul_(scale.view(-1, 1, 1, 1).to(conv.weight.dtype))
+            bias = bn.bias.float() - bn.running_mean.float() * scale
+            if conv.bias is None:
+                conv.bias = torch.nn.Parameter(bias.to(conv.weight.dtype))
+            else:
+                conv.bias.copy_(conv.bias.float() * scale + bias)
+        bn.forward = lambda x: x  # the instance now passes activations through
+
+    model.eval()
+    fold(model.conv1, model.bn1)
+    for layer in (model.layer1, model.layer2, model.layer3, model.layer4):
+        for blk in layer:
+            for i in (1, 2, 3):
+                conv, bn = getattr(blk, f"conv{i}", None), getattr(blk, f"bn{i}", None)
+                if conv is not None and bn is not None:
+                    fold(conv, bn)
+            if blk.downsample is not None:
+                fold(blk.downsample[0], blk.downsample[1])
+    return model
+
+
 def _calibrate_bn(model, shape, batches: int = 4, seed: int = 0):
     """Seeded train-mode passes so random-init BatchNorm statistics are sane."""
     torch = nat.torch_cuda()

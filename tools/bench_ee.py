@@ -113,13 +113,14 @@ def bench(name, pipe, make_input, batch, iters, warmup=5):
 # earlier fp32-weights + bf16-autocast setup for comparison.
 AUTOCAST = os.environ.get("EE_BENCH_AUTOCAST") == "1"
 DTYPE_NOTE = ("bf16 autocast over fp32 weights" if AUTOCAST
-              else "bf16 weights/activations, channels_last convolutions")
+              else "bf16 weights/activations; CNNs channels_last with BatchNorm folded into the convolutions")
 
 
 def _native_bf16(model, channels_last):
     if AUTOCAST:
         return
-    if channels_last:
+    if channels_last:  # CNNs: BatchNorm folded into the convolutions (inference form)
+        ee_infer.fold_batchnorm(model)
         model.to(memory_format=torch.channels_last)
     model.to(torch.bfloat16)
 
