@@ -9,10 +9,19 @@ from paper_2312_05385_b200 import ee_infer
 from paper_2312_05385_b200.serve_live import LiveParams, profile_pipeline, serve_live
 from paper_2312_05385_b200.tuner import TunerParams
 
-pipe, _ = ee_infer.resnet18_cifar()
+torch.backends.cudnn.benchmark = True  # every batch shape 1..32 is autotuned in the warm-up below
+pipe, m = ee_infer.resnet18_cifar()
+# same backbone form as tools/bench_ee.py: BatchNorm folded, bf16, channels_last
+ee_infer.fold_batchnorm(m)
+m.to(memory_format=torch.channels_last).to(torch.bfloat16)
 n = int(os.environ.get("N", 2048))
 g = torch.Generator(device="cuda").manual_seed(0)
-x = torch.randn(n, 3, 32, 32, generator=g, device="cuda")
+x = torch.randn(n, 3, 32, 32, generator=g, device="cuda").to(torch.bfloat16).contiguous(
+    memory_format=torch.channels_last)
+for bsz in range(1, 33):  # warm every batch shape the server can form (cuDNN picks its kernels once)
+    for _ in range(2):
+        pipe.run(x[:bsz], [0.0] * pipe.n_ramps)
+torch.cuda.synchronize()
 prof = profile_pipeline(pipe, x[:32])
 probe = pipe.run(x[:256], [0.0] * pipe.n_ramps)
 err = probe.ramp_err.float().cpu().numpy()
@@ -26,7 +35,8 @@ rep = serve_live(pipe, x, arr, prof, th0, params)
 wall = time.perf_counter() - t0
 vanilla_ms = prof.model_latency(32)
 print(json.dumps({
-    "config": f"config1 closed loop: ResNet-18 CIFAR 6 ramps, {n} requests, Poisson {rate}/ms, max batch 32",
+    "config": f"config1 closed loop: ResNet-18 CIFAR 6 ramps (bf16, channels_last, BN folded), {n} requests, "
+              f"Poisson {rate}/ms, max batch 32",
     "p50_ms": rep.p50_ms, "throughput_rps": rep.throughput_rps, "accuracy_vs_final": rep.accuracy,
     "exit_rate": float(np.mean([r.exit_site is not None for r in rep.rows])),
     "batches": len(rep.batches), "retunes": len(rep.tunes),
