@@ -258,8 +258,16 @@ def run_ours(args):
     # Resident window copies, rotated step by step: each step streams a window
     # last touched WINDOW_COPIES - 1 steps ago (>= 300 MB of other traffic in
     # between, L2 is 126 MB), so no flush is needed between timed steps.
-    sweeps = [ShardedSweep(arrays, sites, prof, rank=rank, world=world, n_total=args.n)
+    # N > 1: each sweep's all-reduce + finalisation runs on one side stream, so
+    # sweep k+1 streams its shard while sweep k's counts are exchanged
+    comm = torch.cuda.Stream() if world > 1 else None
+    sweeps = [ShardedSweep(arrays, sites, prof, rank=rank, world=world, n_total=args.n,
+                           overlap_comm=world > 1, comm_stream=comm)
               for _ in range(args.copies)]
+
+    def join():
+        if comm is not None:
+            torch.cuda.current_stream().wait_stream(comm)
     sweep = sweeps[0]
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
 
@@ -268,6 +276,7 @@ def run_ours(args):
 
     for i in range(args.warmup):
         step(i)
+    join()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -282,6 +291,7 @@ def run_ours(args):
         with torch.cuda.graph(graph):
             for i in range(args.steps):
                 step(i)
+            join()
         graph.replay()
         torch.cuda.synchronize()
     except Exception:  # noqa: BLE001 - fall back to eager stream launches
@@ -299,6 +309,7 @@ def run_ours(args):
         else:
             for i in range(args.steps):
                 step(i)
+            join()
         t1.record()
         torch.cuda.synchronize()
         if world > 1:
@@ -323,6 +334,7 @@ def run_ours(args):
         flush.zero_()
         ls[i].record()
         step()
+        join()
         le[i].record()
     torch.cuda.synchronize()
     nat.profile_enable(False)
@@ -346,6 +358,7 @@ def run_ours(args):
         flush.zero_()
         gs[i].record()
         step()
+        join()
         ge[i].record()
     torch.cuda.synchronize()
     nat.set_special(True)

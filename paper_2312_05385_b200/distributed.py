@@ -61,7 +61,13 @@ class ShardedSweep:
 
     def __init__(self, arrays: WindowArrays, sites: Sequence[RampSite], profile: ModelProfile,
                  *, rank: int = 0, world: int = 1, n_total: int | None = None, group=None,
-                 already_sharded: bool = False):
+                 already_sharded: bool = False, overlap_comm: bool = False, comm_stream=None):
+        """overlap_comm: the all-reduce and finalisation of each sweep run on a
+        side stream, so a stream of sweeps overlaps sweep k+1 with the exchange
+        of sweep k. Results are then ready once `self.ready` (an event) has
+        completed; `join()` makes the current stream wait for all of them.
+        Sweeps sharing a process group must share `comm_stream` (collectives
+        on one communicator stay in one order)."""
         self.n_total = int(n_total if n_total is not None else arrays.n)
         if not already_sharded:
             lo, hi = shard_range(arrays.n, rank, world)
@@ -69,6 +75,9 @@ class ShardedSweep:
         self.group = group
         self.local = WindowEvaluator.from_arrays(arrays, sites, profile, mode="hist")
         self.r = len(sites)
+        self.overlap_comm = overlap_comm
+        self.comm = comm_stream
+        self.ready = None
 
     def counts(self, thresholds: np.ndarray):
         """Global (hist [C, R+1], ok [C]) as int64 device tensors."""
@@ -88,7 +97,39 @@ class ShardedSweep:
             th = np.ascontiguousarray(thresholds, dtype=np.float64)
             acc, sav, _, _ = self.local._eval_device(th, mode_code=nat.MODE_HIST)
             return (acc.cpu().numpy(), sav.cpu().numpy()) if to_host else (acc, sav)
-        hist, ok = self.counts(thresholds)
+        if not self.overlap_comm:
+            hist, ok = self.counts(thresholds)
+            acc, sav = self._finalize(torch, hist, ok)
+        else:
+            th = np.ascontiguousarray(thresholds, dtype=np.float64)
+            _, _, ok, hist = self.local._eval_device(th, want_hist=True, mode_code=nat.MODE_HIST,
+                                                     counts_only=True)
+            if self.comm is None:
+                self.comm = torch.cuda.Stream()
+            swept = torch.cuda.Event()
+            swept.record()
+            with torch.cuda.stream(self.comm):
+                self.comm.wait_event(swept)
+                hist, ok = reduce_counts(hist, ok, self.group)
+                acc, sav = self._finalize(torch, hist, ok)
+            for t in (hist, ok, acc, sav):  # in use on the side stream: no early reuse
+                t.record_stream(self.comm)
+            self.ready = torch.cuda.Event()
+            self.ready.record(self.comm)
+            if to_host:
+                self.ready.synchronize()
+        if to_host:
+            return acc.cpu().numpy(), sav.cpu().numpy()
+        return acc, sav
+
+    def join(self) -> None:
+        """Make the current stream wait for every overlapped exchange issued so far."""
+        import torch
+
+        if self.comm is not None:
+            torch.cuda.current_stream().wait_stream(self.comm)
+
+    def _finalize(self, torch, hist, ok):
         c = hist.shape[0]
         acc = torch.empty(c, dtype=torch.float64, device="cuda")
         sav = torch.empty(c, dtype=torch.float64, device="cuda")
@@ -97,8 +138,6 @@ class ShardedSweep:
             nat.workspace(), hist.data_ptr(), ok.data_ptr(), c, self.r, self.n_total,
             ev.serve.ctypes.data, float(ev.vanilla_ms), acc.data_ptr(), sav.data_ptr(),
             nat.stream_handle(torch)))
-        if to_host:
-            return acc.cpu().numpy(), sav.cpu().numpy()
         return acc, sav
 
 

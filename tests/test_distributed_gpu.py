@@ -3,7 +3,7 @@ cuda:0, gloo standing in for NCCL) each run the counts-only sweep on their
 sample shard, all-reduce the single histogram+correct-count buffer in place,
 and finalise on device (ee_finalize_hist). acc/sav must be bit-identical to
 one GPU evaluating the whole window, for the diagonal kernel and the generic
-path."""
+path, with the exchange in line and on a side stream (overlap_comm)."""
 
 from __future__ import annotations
 
@@ -42,6 +42,13 @@ def _worker(rank, world, port, q):
         rnd = (np.arange(64) / 63.0)[np.random.default_rng(3).integers(0, 64, size=(50, 12))]
         sw = ShardedSweep(arrays, sites, prof, rank=rank, world=world)
         res = [sw.evaluate_many(th) for th in (diag, rnd)]
+        # exchange on a side stream (overlap_comm), results read after join()
+        comm = torch.cuda.Stream()
+        ov = ShardedSweep(arrays, sites, prof, rank=rank, world=world, overlap_comm=True,
+                          comm_stream=comm)
+        dev = [ov.evaluate_many(th, to_host=False) for th in (diag, rnd, diag)]
+        ov.join()
+        res += [(a.cpu().numpy(), s.cpu().numpy()) for a, s in dev]
         q.put((rank, [(a.tolist(), s.tolist()) for a, s in res]))
     finally:
         dist.destroy_process_group()
@@ -60,6 +67,7 @@ def test_two_rank_sweep_matches_one_gpu(cuda):
     diag = np.repeat((np.arange(64) / 63.0)[:, None], 12, axis=1)
     rnd = (np.arange(64) / 63.0)[np.random.default_rng(3).integers(0, 64, size=(50, 12))]
     one = [ShardedSweep(arrays, sites, prof).evaluate_many(th) for th in (diag, rnd)]
+    one += one + one[:1]  # the overlapped exchange: diag, rnd, diag
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -45,5 +45,23 @@ try:
     out["graph_matches_eager"] = all(np.array_equal(x.cpu().numpy(), ref[0]) and np.array_equal(y.cpu().numpy(), ref[1]) for x, y in res)
 except Exception as e:  # noqa: BLE001
     out["graph_error"] = f"{type(e).__name__}: {e}"[:300]
+# the same with the exchange on a side stream (overlap_comm): sweep k+1 runs
+# while sweep k is all-reduced and finalised
+sw2 = D.ShardedSweep(arrays, sites, prof, overlap_comm=True)
+sw2._single = lambda: False
+assert all(np.array_equal(a, b) for a, b in zip(sw2.evaluate_many(th), ref))
+for _ in range(3): sw2.evaluate_many(th, to_host=False)
+sw2.join(); torch.cuda.synchronize()
+try:
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2):
+        res2 = [sw2.evaluate_many(th, to_host=False) for _ in range(K)]
+        sw2.join()
+    g2.replay(); torch.cuda.synchronize()
+    a.record(); g2.replay(); b.record(); torch.cuda.synchronize()
+    out["overlap_graph_us_per_step"] = a.elapsed_time(b) / K * 1e3
+    out["overlap_graph_matches_eager"] = all(np.array_equal(x.cpu().numpy(), ref[0]) and np.array_equal(y.cpu().numpy(), ref[1]) for x, y in res2)
+except Exception as e:  # noqa: BLE001
+    out["overlap_graph_error"] = f"{type(e).__name__}: {e}"[:300]
 print(json.dumps(out))
 dist.destroy_process_group()
