@@ -70,21 +70,24 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid <= MAXR) okc[tid] = 0;
     __syncthreads();
     const int lane = tid & 31;
-    for (int c = 0; c < nc; ++c) {
-      for (int i0 = 0; i0 < n; i0 += THREADS) {  // warp-uniform trip count for the ballot
-        const int i = i0 + tid;
-        unsigned hit = 0;
-        if (i < n) {
-          const double* row = win + (int64_t)i * r;
-          int site = r;
-          for (int j = r - 1; j >= 0; --j)  // branch-free: every score is read, earliest hit wins
-            if (row[j] < cand[c][j]) site = j;
-          vals[(int64_t)c * n8 + i] = sserve[site];
-          hit = (wbits[i] >> site) & 1u;
-        }
-        const unsigned b = __ballot_sync(0xffffffffu, hit);
-        if (lane == 0 && b) atomicAdd(&okc[c], (unsigned long long)__popc(b));
+    // (candidate, sample) pairs flattened over all threads: a warp's 32 pairs
+    // share one candidate (samples padded to 32), so small windows use every warp
+    const int n32 = (n + 31) & ~31;
+    const int total = nc * n32;
+    for (int t0 = 0; t0 < total; t0 += THREADS) {  // warp-uniform trip count for the ballot
+      const int t = t0 + tid;
+      const int c = t / n32, i = t - c * n32;
+      unsigned hit = 0;
+      if (c < nc && i < n) {
+        const double* row = win + (int64_t)i * r;
+        int site = r;
+        for (int j = r - 1; j >= 0; --j)  // branch-free: every score is read, earliest hit wins
+          if (row[j] < cand[c][j]) site = j;
+        vals[(int64_t)c * n8 + i] = sserve[site];
+        hit = (wbits[i] >> site) & 1u;
       }
+      const unsigned b = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0 && b) atomicAdd(&okc[c], (unsigned long long)__popc(b));
     }
     __syncthreads();
     if (tid < nc) {
