@@ -529,6 +529,7 @@ struct ee_workspace {
   std::vector<Stager> stagers;
   long long* d_diag_acc = nullptr;
   bool diag_acc_dirty = true;
+  void* d_exit_done = nullptr;  // exit controllers' completion counter (self-resetting)
   void* h_tune = nullptr;  // ee_tune results: mapped pinned memory the kernel writes
   size_t tune_host_cap = 0;
   // axis-family sweep: per-CTA partial cells and their 64-bit totals
@@ -722,6 +723,7 @@ int ee_workspace_destroy(ee_workspace* ws) {
   if (ws->d_diag_acc) cudaFree(ws->d_diag_acc);
   if (ws->d_axis_part) cudaFree(ws->d_axis_part);
   if (ws->h_tune) cudaFreeHost(ws->h_tune);
+  if (ws->d_exit_done) cudaFree(ws->d_exit_done);
   if (ws->d_axis_tot) cudaFree(ws->d_axis_tot);
   if (ws->d_in) cudaFree(ws->d_in);
   for (auto& m : ws->marks) cudaEventDestroy(m.a), cudaEventDestroy(m.b);
@@ -1969,11 +1971,14 @@ static int exit_out(ee_workspace* ws, cudaStream_t st, int64_t b, const int32_t*
   if ((d_slot_label != nullptr) != (d_slot_err != nullptr) ||
       (d_slot_label != nullptr) != (d_slot_site != nullptr))
     return fail(EE_ERR_ARG, "slot scatter targets must be all given or all null");
-  int rc = ws_reserve(ws, 256, 0);
-  if (rc) return rc;
-  EE_CUDA(cudaMemsetAsync(ws->d_buf, 0, 4, st));
+  // the grid-completion counter is the workspace's own word, zeroed once at
+  // allocation and reset by each launch's last CTA (no memset per ramp call)
+  if (!ws->d_exit_done) {
+    EE_CUDA(cudaMalloc(&ws->d_exit_done, 256));
+    EE_CUDA(cudaMemset(ws->d_exit_done, 0, 256));
+  }
   *o = exitc::Out{d_err, d_label, d_exit, d_logits, d_keep, d_nkeep, d_slot, d_slot_label,
-                  d_slot_err, d_slot_site, site, static_cast<unsigned*>(ws->d_buf)};
+                  d_slot_err, d_slot_site, site, static_cast<unsigned*>(ws->d_exit_done)};
   (void)b;
   return EE_OK;
 }

@@ -37,7 +37,7 @@ struct Out {
   float* slot_err;
   int32_t* slot_site;
   int32_t site;
-  unsigned* done;    // grid completion counter (zeroed by the host)
+  unsigned* done;    // grid completion counter (zero on entry; the last CTA leaves it zero)
 };
 
 __device__ __forceinline__ float bf16_to_f32(uint16_t h) {
@@ -136,7 +136,10 @@ __device__ void compact_and_scatter(int64_t B, const uint8_t* alive_in, const Ou
       for (int w = 0; w < THREADS / 32; ++w) base += warp_tot[w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *o.n_keep = base;
+  if (threadIdx.x == 0) {
+    *o.n_keep = base;
+    *o.done = 0u;  // every other CTA has counted: ready for the next launch
+  }
 }
 
 __device__ __forceinline__ bool last_cta(unsigned* done) {
