@@ -97,12 +97,21 @@ class EEPipeline:
         dev_th = hasattr(thresholds, "data_ptr")
         if dev_th:
             thresholds = [thresholds[r : r + 1] for r in range(R)]
-        slots = SlotTable.empty(b)
         alive = torch.ones(b, dtype=torch.uint8, device=dev)
         rows = torch.arange(b, dtype=torch.int32, device=dev)  # request slot of each live row
-        ramp_err = torch.full((R, b), float("nan"), dtype=torch.float32, device=dev)
-        ramp_label = torch.full((R, b), -1, dtype=torch.int32, device=dev)
-        final_label = torch.full((b,), -1, dtype=torch.int32, device=dev)
+        if mode == "feedback":
+            # every row reaches every ramp (each writes err/label for all rows) and
+            # is released exactly once (at a ramp or by the final model), so the
+            # result tables need no fill kernels
+            slots = SlotTable.uninitialized(b)
+            ramp_err = torch.empty((R, b), dtype=torch.float32, device=dev)
+            ramp_label = torch.empty((R, b), dtype=torch.int32, device=dev)
+            final_label = torch.empty((b,), dtype=torch.int32, device=dev)
+        else:
+            slots = SlotTable.empty(b)
+            ramp_err = torch.full((R, b), float("nan"), dtype=torch.float32, device=dev)
+            ramp_label = torch.full((R, b), -1, dtype=torch.int32, device=dev)
+            final_label = torch.full((b,), -1, dtype=torch.int32, device=dev)
         marks = []
         if timed:
             start = torch.cuda.Event(enable_timing=True)

@@ -52,6 +52,14 @@ class SlotTable:
                    torch.full((slots,), float("nan"), dtype=torch.float32, device="cuda"),
                    torch.full((slots,), -1, dtype=torch.int32, device="cuda"))
 
+    @classmethod
+    def uninitialized(cls, slots: int):
+        """For a caller that releases every slot exactly once (a feedback-mode
+        batch: each row exits at a ramp or at the final model): no fill kernels."""
+        torch = nat.torch_cuda()
+        buf = torch.empty((3, slots), dtype=torch.int32, device="cuda")
+        return cls(buf[0], buf[1].view(torch.float32), buf[2])
+
 
 def _outputs(torch, b, k, want_logits, out_err=None, out_label=None, out_exits=None):
     dev = "cuda"
