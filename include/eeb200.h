@@ -116,6 +116,16 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
 /* Host-side packing of correct_ext f64 [n, r1] into u32 bit rows (bit j =
  * column j) on n_threads threads (<= 0: all cores); EE_ERR_NOT_BINARY if any
  * entry is not exactly 0.0 or 1.0. */
+/* Host only (no device work): which sweep family a candidate matrix th [c, r]
+ * belongs to, as eval dispatch sees it: *kind = 1 diagonal (every row repeats
+ * one threshold; *n_values = distinct non-NaN thresholds), 2 single-coordinate
+ * (rows equal a base vector except in at most one column; *n_values = distinct
+ * non-NaN varied values; the base is written to base[r] when base is non-null),
+ * 0 anything else. Replaces no reference function: it documents and tests the
+ * family dispatch in front of _exitcore.eval_thresholds (_exitcore.pyx:27-56). */
+int ee_classify_candidates(const double* h_th, int64_t c, int32_t r, int32_t* kind,
+                           int32_t* n_values, double* base);
+
 int ee_pack_correct_host(const double* h_correct_ext, int64_t n, int32_t r1, uint32_t* h_bits,
                          int32_t n_threads);
 

@@ -828,6 +828,22 @@ static int eval_exact(ee_workspace* ws, const double* d_scores, const uint32_t* 
 }
 
 // Diagonal family: every row repeats one threshold (NaN rows allowed).
+static bool diagonal_rows_any(const double* th, int64_t C, int r, std::vector<double>& distinct) {
+  if (r < 1) return false;
+  distinct.clear();
+  for (int64_t c = 0; c < C; ++c) {
+    const double first = th[c * r];
+    for (int j = 1; j < r; ++j) {
+      const double v = th[c * r + j];
+      if (!(v == first || (v != v && first != first))) return false;
+    }
+    if (first == first) distinct.push_back(canon(first));
+  }
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  return true;
+}
+
 static bool diagonal_rows(const double* th, int64_t C, int r, std::vector<double>& distinct) {
   if (r < 1) return false;
   distinct.clear();
@@ -2183,6 +2199,34 @@ int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t 
     gemmtc::k_pool_bf16<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         static_cast<const float*>(d_x), bc, hw, static_cast<uint16_t*>(d_out));
   EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_classify_candidates(const double* h_th, int64_t c, int32_t r, int32_t* kind,
+                           int32_t* n_values, double* base) {
+  if (c < 0 || r < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (!kind || !n_values || (c > 0 && r > 0 && !h_th)) return fail(EE_ERR_ARG, "null pointer");
+  *kind = 0;
+  *n_values = 0;
+  if (c == 0 || r == 0) return EE_OK;
+  std::vector<double> u;
+  if (diagonal_rows_any(h_th, c, r, u)) {
+    *kind = 1;
+    *n_values = (int32_t)u.size();
+    return EE_OK;
+  }
+  std::vector<double> bv, val;
+  std::vector<int> col;
+  if (c <= axis::MAX_C && axis_rows(h_th, c, r, bv, col, val)) {
+    for (int64_t i = 0; i < c; ++i)
+      if (val[i] == val[i]) u.push_back(canon(val[i]));
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    *kind = 2;
+    *n_values = (int32_t)u.size();
+    if (base)
+      for (int j = 0; j < r; ++j) base[j] = bv[j];
+  }
   return EE_OK;
 }
 

@@ -205,3 +205,26 @@ def install_into(module) -> None:
     module.eval_thresholds = eval_thresholds
     module.exit_sites = exit_sites
     module.BACKEND = BACKEND
+
+
+def classify_candidates(thresholds):
+    """Which sweep family a (C, R) candidate matrix belongs to, as the native
+    dispatch sees it (host only, no device work): ("diagonal", m, None),
+    ("axis", m, base vector) or ("generic", 0, None); m = distinct values."""
+    th = np.ascontiguousarray(thresholds, dtype=np.float64)
+    if th.ndim != 2:
+        raise ParameterError(f"thresholds must be 2-D, got {th.shape}")
+    c, r = th.shape
+    import ctypes
+
+    kind = ctypes.c_int32()
+    m = ctypes.c_int32()
+    base = np.empty(max(r, 1))
+    nat.check(nat.load_library().ee_classify_candidates(
+        th.ctypes.data if th.size else None, c, r, ctypes.byref(kind), ctypes.byref(m),
+        base.ctypes.data))
+    if kind.value == 1:
+        return "diagonal", m.value, None
+    if kind.value == 2:
+        return "axis", m.value, base[:r].copy()
+    return "generic", 0, None

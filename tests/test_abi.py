@@ -125,3 +125,31 @@ def test_host_pack_correct_matches_numpy_and_rejects_non_binary():
     bad[7777, 2] = np.nan
     with pytest.raises(ValueError):
         kernels.pack_correct_host(bad)
+
+
+def test_candidate_family_classification_on_the_host():
+    """ee_classify_candidates (host only) sees the families the sweep dispatch
+    specialises: diagonal rows, a base vector with one swept ramp (SURVEY 8d's
+    C = 768 axis family, NaN base entries and rows equal to the base included),
+    and everything else as generic."""
+    r = 12
+    diag = np.repeat((np.arange(64) / 63.0)[:, None], r, axis=1)
+    assert kernels.classify_candidates(diag) == ("diagonal", 64, None)
+    diag_nan = np.vstack([diag, np.full((1, r), np.nan)])
+    assert kernels.classify_candidates(diag_nan)[:2] == ("diagonal", 64)
+    axis = np.full((768, r), 0.3)
+    for j in range(r):
+        axis[j * 64:(j + 1) * 64, j] = np.arange(64) / 63.0
+    kind, m, base = kernels.classify_candidates(axis)
+    assert kind == "axis" and m == 64 and np.array_equal(base, np.full(r, 0.3))
+    axis2 = axis.copy()
+    axis2[:, 5] = np.where(np.arange(768) // 64 == 5, axis2[:, 5], np.nan)  # NaN base entry
+    axis2 = np.vstack([axis2, axis2[0:1] * 0 + np.where(np.arange(r) == 5, np.nan, 0.3)])
+    kind, m, base = kernels.classify_candidates(axis2)
+    assert kind == "axis" and np.isnan(base[5]) and base[0] == 0.3
+    rnd = (np.arange(64) / 63.0)[np.random.default_rng(1).integers(0, 64, size=(64, r))]
+    assert kernels.classify_candidates(rnd) == ("generic", 0, None)
+    two = np.full((4, r), 0.3)
+    two[1, 0] = two[1, 1] = 0.9  # two columns changed in one row
+    assert kernels.classify_candidates(two)[0] == "generic"
+    assert kernels.classify_candidates(np.empty((0, r)))[0] == "generic"
