@@ -92,9 +92,11 @@ class GPT2Decoder:
         self.lnf_w = torch.ones(d, device="cuda", dtype=bf)
         self.lnf_b = torch.zeros(d, device="cuda", dtype=bf)
         H, Dh = spec.n_head, spec.head_dim
-        self.k_cache = [torch.zeros(batch, H, max_tokens + 1, Dh, device="cuda", dtype=bf)
-                        for _ in range(spec.n_layer)]
-        self.v_cache = [torch.zeros_like(k) for k in self.k_cache]
+        # K and V of a layer in one tensor [2, B, H, T+1, Dh]: one scatter writes both
+        self.kv_cache = [torch.zeros(2, batch, H, max_tokens + 1, Dh, device="cuda", dtype=bf)
+                         for _ in range(spec.n_layer)]
+        self.k_cache = [kv[0] for kv in self.kv_cache]
+        self.v_cache = [kv[1] for kv in self.kv_cache]
         self.rows = torch.arange(batch, device="cuda")
         self.key_idx = torch.arange(max_tokens + 1, device="cuda")
 
@@ -111,6 +113,7 @@ class GPT2Decoder:
         # one scatter index per pass, shared by every layer: cache viewed as
         # [B*H, T+1, Dh], rows b*H + h, slot wpos[b, i]
         sidx = wpos[:, None, :, None].expand(B, H, q, Dh).reshape(B * H, q, Dh)
+        sidx2 = sidx.repeat(2, 1, 1)  # K rows then V rows of the [2*B*H, T+1, Dh] view
         # key j visible to query (b, i) iff j <= pos[b, i]; padding queries see key 0 only
         qpos = torch.where(valid, pos, torch.zeros_like(pos))
         mask = (self.key_idx[None, None, :] <= qpos[:, :, None]) & (self.key_idx[None, None, :] < T)
@@ -120,13 +123,14 @@ class GPT2Decoder:
             x = F.layer_norm(h, (d,), w["ln1_w"], w["ln1_b"], eps=1e-5)
             qkv = F.linear(x, w["qkv_w"], w["qkv_b"]).view(B, q, 3, H, Dh).permute(2, 0, 3, 1, 4)
             qh = qkv[0]
-            self.k_cache[l].view(B * H, T + 1, Dh).scatter_(1, sidx, qkv[1].reshape(B * H, q, Dh))
-            self.v_cache[l].view(B * H, T + 1, Dh).scatter_(1, sidx, qkv[2].reshape(B * H, q, Dh))
+            self.kv_cache[l].view(2 * B * H, T + 1, Dh).scatter_(
+                1, sidx2, qkv[1:3].reshape(2 * B * H, q, Dh))
             att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l], attn_mask=mask)
             h = h + F.linear(att.transpose(1, 2).reshape(B, q, d), w["o_w"], w["o_b"])
             x = F.layer_norm(h, (d,), w["ln2_w"], w["ln2_b"], eps=1e-5)
-            h = h + F.linear(F.gelu(F.linear(x, w["fc_w"], w["fc_b"]), approximate="tanh"),
-                             w["pr_w"], w["pr_b"])
+            # bias + tanh-GELU in the GEMM epilogue (cuBLASLt), then the projection
+            t = torch._addmm_activation(w["fc_b"], x.reshape(B * q, d), w["fc_w"].t(), use_gelu=True)
+            h = h + F.linear(t.view(B, q, -1), w["pr_w"], w["pr_b"])
         return h
 
     def embed(self, tokens, pos):
@@ -139,9 +143,8 @@ class GPT2Decoder:
         return linear_tc(x.to(self.torch.bfloat16).contiguous(), self.wte)
 
     def reset(self):
-        for k, v in zip(self.k_cache, self.v_cache):
-            k.zero_()
-            v.zero_()
+        for kv in self.kv_cache:
+            kv.zero_()
 
     def full_forward(self, tokens):
         """Teacher-forced causal forward of [B, T'] tokens through every layer
