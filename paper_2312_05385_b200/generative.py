@@ -117,7 +117,10 @@ class GPT2Decoder:
         # key j visible to query (b, i) iff j <= pos[b, i]; padding queries see key 0 only
         qpos = torch.where(valid, pos, torch.zeros_like(pos))
         mask = (self.key_idx[None, None, :] <= qpos[:, :, None]) & (self.key_idx[None, None, :] < T)
-        mask = mask[:, None, :, :]
+        # additive bf16 mask built once per pass (a boolean mask is converted by
+        # the attention backend in every layer: three extra kernels per layer)
+        mask = torch.zeros(mask.shape, dtype=h.dtype, device=h.device).masked_fill_(
+            ~mask, float("-inf"))[:, None, :, :]
         for l in range(l0, l1):
             w = self.layers[l]
             x = F.layer_norm(h, (d,), w["ln1_w"], w["ln1_b"], eps=1e-5)
