@@ -217,6 +217,14 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
 /* Gathers rows d_keep[0 .. *d_nkeep) of d_src (row_bytes each, multiple of
  * 16) into the dense d_dst (capacity max_rows rows): downstream blocks then
  * run only on the non-exited samples (compaction mode). */
+/* KV-cache append for the token-level decoder (config 5, the reference's KV
+ * fill for skipped layers, generative.py:170-273): qkv bf16 [b, q, 3, h, dh]
+ * (a fused QKV projection), pos i64 [b, q] with 0 <= pos < t1; writes K and V
+ * of every (b, i) into kv bf16 [2, b, h, t1, dh] at slot pos[b, i]. A warp per
+ * (b, i, K|V, head) row; dh must be a multiple of 2 and at most 256. */
+int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_t q, int32_t h,
+                      int32_t dh, int64_t t1, void* d_kv, void* stream);
+
 int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
                     const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream);
 

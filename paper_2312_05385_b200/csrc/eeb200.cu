@@ -2247,6 +2247,40 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
   return EE_OK;
 }
 
+}  // extern "C"
+// KV append: warp w -> row (b, i, s, head); lanes copy dh bf16 (u32 pairs)
+__global__ void k_kv_append(const uint32_t* __restrict__ qkv, const int64_t* __restrict__ pos,
+                            int64_t b, int q, int h, int dh2, int64_t t1,
+                            uint32_t* __restrict__ kv) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = b * q * 2 * h;
+  if (w >= rows) return;
+  const int hh = (int)(w % h);
+  const int s = (int)((w / h) % 2);
+  const int64_t bi = w / (2 * h);  // b * q + i
+  const int64_t bb = bi / q;
+  const int64_t slot = __ldg(pos + bi);
+  const uint32_t* src = qkv + ((bi * 3 + 1 + s) * h + hh) * dh2;
+  uint32_t* dst = kv + (((s * b + bb) * h + hh) * t1 + slot) * dh2;
+  for (int k = lane; k < dh2; k += 32) dst[k] = __ldg(src + k);
+}
+extern "C" {
+
+int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_t q, int32_t h,
+                      int32_t dh, int64_t t1, void* d_kv, void* stream) {
+  if (b < 1 || q < 1 || h < 1 || dh < 2 || dh % 2 || dh > 256 || t1 < 1)
+    return fail(EE_ERR_ARG, "bad KV shape");
+  if (!d_qkv || !d_pos || !d_kv) return fail(EE_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(d_qkv) | reinterpret_cast<uintptr_t>(d_kv)) % 4)
+    return fail(EE_ERR_ARG, "misaligned bf16 pairs");
+  const int64_t rows = b * q * 2 * h;
+  k_kv_append<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint32_t*>(d_qkv), d_pos, b, q, h, dh / 2, t1, static_cast<uint32_t*>(d_kv));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
 int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
                     const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream) {
   if (row_bytes <= 0 || row_bytes % 16) return fail(EE_ERR_ARG, "row_bytes must be a positive multiple of 16");

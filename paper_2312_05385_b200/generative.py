@@ -110,10 +110,10 @@ class GPT2Decoder:
         H, Dh, T = self.spec.n_head, self.spec.head_dim, self.T
         valid = pos >= 0
         wpos = torch.where(valid, pos, torch.full_like(pos, T))  # padding -> sink slot T
-        # one scatter index per pass, shared by every layer: cache viewed as
-        # [B*H, T+1, Dh], rows b*H + h, slot wpos[b, i]
-        sidx = wpos[:, None, :, None].expand(B, H, q, Dh).reshape(B * H, q, Dh)
-        sidx2 = sidx.repeat(2, 1, 1)  # K rows then V rows of the [2*B*H, T+1, Dh] view
+        # every layer appends K/V of token (b, i) at slot wpos[b, i] (ee_kv_append_bf16)
+        wpos = wpos.to(torch.int64).contiguous()
+        lib = nat.load_library()
+        st = nat.stream_handle(torch)
         # key j visible to query (b, i) iff j <= pos[b, i]; padding queries see key 0 only
         qpos = torch.where(valid, pos, torch.zeros_like(pos))
         mask = (self.key_idx[None, None, :] <= qpos[:, :, None]) & (self.key_idx[None, None, :] < T)
@@ -124,10 +124,11 @@ class GPT2Decoder:
         for l in range(l0, l1):
             w = self.layers[l]
             x = F.layer_norm(h, (d,), w["ln1_w"], w["ln1_b"], eps=1e-5)
-            qkv = F.linear(x, w["qkv_w"], w["qkv_b"]).view(B, q, 3, H, Dh).permute(2, 0, 3, 1, 4)
-            qh = qkv[0]
-            self.kv_cache[l].view(2 * B * H, T + 1, Dh).scatter_(
-                1, sidx2, qkv[1:3].reshape(2 * B * H, q, Dh))
+            qkv = F.linear(x, w["qkv_w"], w["qkv_b"])  # [B, q, 3d] contiguous
+            # K and V rows straight from the projection into their cache slots (one kernel)
+            nat.check(lib.ee_kv_append_bf16(qkv.data_ptr(), wpos.data_ptr(), B, q, H, Dh, T + 1,
+                                            self.kv_cache[l].data_ptr(), st))
+            qh = qkv.view(B, q, 3, H, Dh)[:, :, 0].transpose(1, 2)
             att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l], attn_mask=mask)
             h = h + F.linear(att.transpose(1, 2).reshape(B, q, d), w["o_w"], w["o_b"])
             x = F.layer_norm(h, (d,), w["ln2_w"], w["ln2_b"], eps=1e-5)

@@ -105,3 +105,25 @@ def test_forced_cap_carry_end_flushes(cuda):
         assert kinds[2] == []
         assert kinds[3] == [(2, "end")]
         _kv_check(torch, model, rep, prompt, first.cpu().numpy(), n_new)
+
+
+def test_kv_append_matches_scatter(cuda):
+    """ee_kv_append_bf16 writes exactly the K/V rows a scatter into the cache
+    would (padding rows to the sink slot), and nothing else."""
+    import torch
+
+    from paper_2312_05385_b200 import _native as nat
+
+    B, q, H, Dh, T1 = 5, 3, 4, 64, 11
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = torch.randn(B, q, 3, H, Dh, generator=g, device="cuda").to(torch.bfloat16)
+    pos = torch.tensor([[0, 1, 2], [4, 5, 10], [7, 10, 8], [3, 2, 1], [9, 8, 6]], device="cuda")
+    kv = torch.randn(2, B, H, T1, Dh, generator=g, device="cuda").to(torch.bfloat16)
+    ref = kv.clone()
+    for b in range(B):
+        for i in range(q):
+            ref[0, b, :, pos[b, i]] = qkv[b, i, 1]
+            ref[1, b, :, pos[b, i]] = qkv[b, i, 2]
+    nat.check(nat.load_library().ee_kv_append_bf16(qkv.data_ptr(), pos.data_ptr(), B, q, H, Dh, T1,
+                                                    kv.data_ptr(), nat.stream_handle(torch)))
+    assert torch.equal(kv, ref)
