@@ -225,6 +225,13 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
 int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_t q, int32_t h,
                       int32_t dh, int64_t t1, void* d_kv, void* stream);
 
+/* Fused residual add + LayerNorm for the decoder (config 5): h[r] += y[r]
+ * (bf16, rounded like torch's add), then x[r] = LayerNorm(h[r]) * gamma + beta
+ * (fp32 statistics, two-pass), bf16 throughout; y may be null (LayerNorm only).
+ * One CTA of d / 8 threads per row; d a multiple of 8, at most 8192. */
+int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const void* d_beta,
+                          double eps, int64_t rows, int32_t d, void* d_x, void* stream);
+
 int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
                     const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream);
 

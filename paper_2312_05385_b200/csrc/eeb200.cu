@@ -2248,6 +2248,72 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
 }
 
 }  // extern "C"
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t bf_round(float f) {  // fp32 -> bf16 bits, nearest even
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7f800000u) == 0x7f800000u) return (u >> 16) | ((u & 0xffffu) ? 0x40u : 0u);  // inf/NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return u >> 16;
+}
+// residual add + LayerNorm, one CTA (d / 8 threads) per row, 8 bf16 per thread
+__global__ void k_add_layernorm(uint16_t* __restrict__ h, const uint16_t* __restrict__ y,
+                                const uint16_t* __restrict__ gamma, const uint16_t* __restrict__ beta,
+                                float eps, int d, uint16_t* __restrict__ x) {
+  __shared__ float red[32];
+  const int64_t row = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  const bool act = t < d / 8;  // the CTA is rounded up to whole warps
+  uint4 hv = act ? reinterpret_cast<const uint4*>(h + row * d)[t] : make_uint4(0, 0, 0, 0);
+  float v[8];
+  {
+    const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[2 * k] = bf_lo(hw[k]), v[2 * k + 1] = bf_hi(hw[k]);
+  }
+  if (y && act) {
+    const uint4 yv = reinterpret_cast<const uint4*>(y + row * d)[t];
+    const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t a = bf_round(v[2 * k] + bf_lo(yw[k])), b = bf_round(v[2 * k + 1] + bf_hi(yw[k]));
+      o[k] = a | (b << 16);
+      v[2 * k] = bf_lo(o[k]);
+      v[2 * k + 1] = bf_hi(o[k]);
+    }
+    reinterpret_cast<uint4*>(h + row * d)[t] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  auto block_sum = [&](float s) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __syncthreads();
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    float tot = 0.f;
+    for (int w = 0; w < nw; ++w) tot += red[w];
+    return tot;
+  };
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += v[k];
+  const float mean = block_sum(s) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) q += act ? (v[k] - mean) * (v[k] - mean) : 0.f;
+  const float rstd = rsqrtf(block_sum(q) / (float)d + eps);
+  if (!act) return;
+  const uint4 gv = reinterpret_cast<const uint4*>(gamma)[t], bv = reinterpret_cast<const uint4*>(beta)[t];
+  const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float a = (v[2 * k] - mean) * rstd * bf_lo(gw[k]) + bf_lo(bw[k]);
+    const float b = (v[2 * k + 1] - mean) * rstd * bf_hi(gw[k]) + bf_hi(bw[k]);
+    o[k] = bf_round(a) | (bf_round(b) << 16);
+  }
+  reinterpret_cast<uint4*>(x + row * d)[t] = make_uint4(o[0], o[1], o[2], o[3]);
+}
 // KV append: warp w -> row (b, i, s, head); lanes copy dh bf16 (u32 pairs)
 __global__ void k_kv_append(const uint32_t* __restrict__ qkv, const int64_t* __restrict__ pos,
                             int64_t b, int q, int h, int dh2, int64_t t1,
@@ -2277,6 +2343,22 @@ int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_
   const int64_t rows = b * q * 2 * h;
   k_kv_append<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(
       static_cast<const uint32_t*>(d_qkv), d_pos, b, q, h, dh / 2, t1, static_cast<uint32_t*>(d_kv));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const void* d_beta,
+                          double eps, int64_t rows, int32_t d, void* d_x, void* stream) {
+  if (rows < 1 || d < 8 || d % 8 || d > 8192 || rows > 0x7fffffff) return fail(EE_ERR_ARG, "bad shape");
+  if (!d_h || !d_gamma || !d_beta || !d_x) return fail(EE_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(d_h) | reinterpret_cast<uintptr_t>(d_y) |
+       reinterpret_cast<uintptr_t>(d_gamma) | reinterpret_cast<uintptr_t>(d_beta) |
+       reinterpret_cast<uintptr_t>(d_x)) % 16)
+    return fail(EE_ERR_ARG, "misaligned rows");
+  k_add_layernorm<<<(unsigned)rows, (unsigned)((d / 8 + 31) / 32 * 32), 0, (cudaStream_t)stream>>>(
+      static_cast<uint16_t*>(d_h), static_cast<const uint16_t*>(d_y),
+      static_cast<const uint16_t*>(d_gamma), static_cast<const uint16_t*>(d_beta), (float)eps, d,
+      static_cast<uint16_t*>(d_x));
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

@@ -121,20 +121,36 @@ class GPT2Decoder:
         # the attention backend in every layer: three extra kernels per layer)
         mask = torch.zeros(mask.shape, dtype=h.dtype, device=h.device).masked_fill_(
             ~mask, float("-inf"))[:, None, :, :]
+        if l1 <= l0:
+            return h
+        # the residual stream is owned here and updated in place by the fused
+        # add + LayerNorm kernel (ee_add_layernorm_bf16): h += y; x = LN(h)
+        h = h.contiguous().clone()
+        x = torch.empty_like(h)
+
+        def add_ln(y, gamma, beta):
+            nat.check(lib.ee_add_layernorm_bf16(h.data_ptr(), None if y is None else y.data_ptr(),
+                                                gamma.data_ptr(), beta.data_ptr(), 1e-5, B * q, d,
+                                                x.data_ptr(), st))
+
+        add_ln(None, self.layers[l0]["ln1_w"], self.layers[l0]["ln1_b"])
         for l in range(l0, l1):
             w = self.layers[l]
-            x = F.layer_norm(h, (d,), w["ln1_w"], w["ln1_b"], eps=1e-5)
             qkv = F.linear(x, w["qkv_w"], w["qkv_b"])  # [B, q, 3d] contiguous
             # K and V rows straight from the projection into their cache slots (one kernel)
             nat.check(lib.ee_kv_append_bf16(qkv.data_ptr(), wpos.data_ptr(), B, q, H, Dh, T + 1,
                                             self.kv_cache[l].data_ptr(), st))
             qh = qkv.view(B, q, 3, H, Dh)[:, :, 0].transpose(1, 2)
             att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l], attn_mask=mask)
-            h = h + F.linear(att.transpose(1, 2).reshape(B, q, d), w["o_w"], w["o_b"])
-            x = F.layer_norm(h, (d,), w["ln2_w"], w["ln2_b"], eps=1e-5)
+            add_ln(F.linear(att.transpose(1, 2).reshape(B, q, d), w["o_w"], w["o_b"]),
+                   w["ln2_w"], w["ln2_b"])
             # bias + tanh-GELU in the GEMM epilogue (cuBLASLt), then the projection
             t = torch._addmm_activation(w["fc_b"], x.reshape(B * q, d), w["fc_w"].t(), use_gelu=True)
-            h = h + F.linear(t.view(B, q, -1), w["pr_w"], w["pr_b"])
+            y = F.linear(t.view(B, q, -1), w["pr_w"], w["pr_b"])
+            if l + 1 < l1:
+                add_ln(y, self.layers[l + 1]["ln1_w"], self.layers[l + 1]["ln1_b"])
+            else:
+                h += y
         return h
 
     def embed(self, tokens, pos):

@@ -127,3 +127,26 @@ def test_kv_append_matches_scatter(cuda):
     nat.check(nat.load_library().ee_kv_append_bf16(qkv.data_ptr(), pos.data_ptr(), B, q, H, Dh, T1,
                                                     kv.data_ptr(), nat.stream_handle(torch)))
     assert torch.equal(kv, ref)
+
+
+def test_add_layernorm_matches_torch(cuda):
+    """ee_add_layernorm_bf16: h += y rounded exactly like torch's bf16 add; x
+    within bf16 rounding of torch's LayerNorm of that h."""
+    import torch
+
+    from paper_2312_05385_b200 import _native as nat
+
+    g = torch.Generator(device="cuda").manual_seed(4)
+    for rows, d in ((32, 1024), (7, 64), (160, 1024)):
+        h = torch.randn(rows, d, generator=g, device="cuda").to(torch.bfloat16)
+        y = torch.randn(rows, d, generator=g, device="cuda").to(torch.bfloat16)
+        gamma = (1 + 0.1 * torch.randn(d, generator=g, device="cuda")).to(torch.bfloat16)
+        beta = (0.1 * torch.randn(d, generator=g, device="cuda")).to(torch.bfloat16)
+        h_ref = h + y
+        x_ref = torch.nn.functional.layer_norm(h_ref.float(), (d,), gamma.float(), beta.float(), eps=1e-5)
+        x = torch.empty_like(h)
+        nat.check(nat.load_library().ee_add_layernorm_bf16(
+            h.data_ptr(), y.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5, rows, d,
+            x.data_ptr(), nat.stream_handle(torch)))
+        assert torch.equal(h, h_ref)
+        assert torch.allclose(x.float(), x_ref, rtol=2 ** -7, atol=2 ** -7)
