@@ -232,6 +232,16 @@ int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_
 int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const void* d_beta,
                           double eps, int64_t rows, int32_t d, void* d_x, void* stream);
 
+/* Length-aware decode attention for the token-level decoder (config 5): for
+ * each (b, head) and each of q <= 8 queries (the fused QKV projection qkv bf16
+ * [b, q, 3, h, dh]), softmax(q k^T / sqrt(dh)) v over keys 0 .. qpos[b, i] of
+ * the layer's cache kv bf16 [2, b, h, t1, dh]: only the visible part of the
+ * cache is read. Writes out bf16 [b, q, h, dh] (the o-projection's input).
+ * dh = 64, q * t1 <= 51200. */
+int ee_decode_attention_bf16(const void* d_qkv, const void* d_kv, const int64_t* d_qpos, int64_t b,
+                             int32_t q, int32_t h, int32_t dh, int64_t t1, void* d_out,
+                             void* stream);
+
 int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
                     const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream);
 

@@ -2314,6 +2314,114 @@ __global__ void k_add_layernorm(uint16_t* __restrict__ h, const uint16_t* __rest
   }
   reinterpret_cast<uint4*>(x + row * d)[t] = make_uint4(o[0], o[1], o[2], o[3]);
 }
+// Decode attention, CTA per (b, head), 128 threads, dh = 64. HBM-bound on the
+// visible K/V rows, so every phase keeps whole 16-byte loads in flight:
+//  scores: a lane per key (its 128-byte K row as 8 uint4 loads), q in shared
+//          memory (broadcast reads), one score per (query, key);
+//  softmax per query over its visible keys (a warp per query);
+//  P V:    thread (key group kg of 16, 8-dim chunk dc), 4 keys in flight per
+//          thread, partial sums reduced over the key groups in shared memory.
+constexpr int DA_QMAX = 8;
+constexpr int DA_THREADS = 128;
+__device__ __forceinline__ void bf8_to_f32(const uint4 w, float* f) {
+  f[0] = bf_lo(w.x), f[1] = bf_hi(w.x), f[2] = bf_lo(w.y), f[3] = bf_hi(w.y);
+  f[4] = bf_lo(w.z), f[5] = bf_hi(w.z), f[6] = bf_lo(w.w), f[7] = bf_hi(w.w);
+}
+__global__ void __launch_bounds__(DA_THREADS) k_decode_attn(
+    const uint16_t* __restrict__ qkv, const uint16_t* __restrict__ kv,
+    const int64_t* __restrict__ qpos, int64_t B, int q, int H, int64_t T1,
+    uint16_t* __restrict__ out) {
+  extern __shared__ float sc[];  // [q][T1] scores, then probabilities
+  __shared__ float qs[DA_QMAX][64];
+  __shared__ float part[16][64];
+  __shared__ float rsum[DA_QMAX];
+  __shared__ int vis[DA_QMAX];
+  const int bh = blockIdx.x;
+  const int64_t b = bh / H;
+  const int hh = bh % H;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t < q) vis[t] = (int)__ldg(qpos + b * q + t) + 1;
+  for (int e = t; e < q * 64; e += DA_THREADS) {
+    const int i = e / 64, k = e % 64;
+    qs[i][k] = __uint_as_float((uint32_t)__ldg(qkv + ((b * q + i) * 3 * H + hh) * 64 + k) << 16) * 0.125f;
+  }
+  __syncthreads();
+  int nvis = 1;
+  for (int i = 0; i < q; ++i) nvis = vis[i] > nvis ? vis[i] : nvis;
+  const uint4* K = reinterpret_cast<const uint4*>(kv + ((0 * B + b) * H + hh) * T1 * 64);
+  const uint4* V = reinterpret_cast<const uint4*>(kv + ((1 * B + b) * H + hh) * T1 * 64);
+  for (int j = t; j < nvis; j += DA_THREADS) {  // a lane per key
+    uint4 kw[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) kw[c] = __ldg(K + (int64_t)j * 8 + c);
+    for (int i = 0; i < q; ++i) {
+      float d = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float kf[8];
+        bf8_to_f32(kw[c], kf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d += qs[i][8 * c + e] * kf[e];
+      }
+      sc[i * T1 + j] = d;
+    }
+  }
+  __syncthreads();
+  for (int i = warp; i < q; i += DA_THREADS / 32) {  // softmax of query i over its visible keys
+    const int vi = vis[i];
+    float mx = -INFINITY;
+    for (int j = lane; j < vi; j += 32) mx = fmaxf(mx, sc[i * T1 + j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (int j = lane; j < nvis; j += 32) {
+      const float e = j < vi ? __expf(sc[i * T1 + j] - mx) : 0.f;
+      sc[i * T1 + j] = e;
+      sum += e;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) rsum[i] = 1.f / sum;
+  }
+  __syncthreads();
+  const int dc = t & 7, kg = t >> 3;  // 8 dims x 16 key groups
+  for (int i = 0; i < q; ++i) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int vi = vis[i];
+    int j = kg;
+    for (; j + 48 < vi; j += 64) {  // 4 V rows in flight
+      uint4 vw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) vw[u] = __ldg(V + (int64_t)(j + 16 * u) * 8 + dc);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float vf[8];
+        bf8_to_f32(vw[u], vf);
+        const float p = sc[i * T1 + j + 16 * u];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += p * vf[e];
+      }
+    }
+    for (; j < vi; j += 16) {
+      float vf[8];
+      bf8_to_f32(__ldg(V + (int64_t)j * 8 + dc), vf);
+      const float p = sc[i * T1 + j];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += p * vf[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) part[kg][8 * dc + e] = acc[e];
+    __syncthreads();
+    if (t < 64) {
+      float s = 0.f;
+#pragma unroll
+      for (int g = 0; g < 16; ++g) s += part[g][t];
+      out[((b * q + i) * H + hh) * 64 + t] = (uint16_t)bf_round(s * rsum[i]);
+    }
+    __syncthreads();
+  }
+}
+
 // KV append: warp w -> row (b, i, s, head); lanes copy dh bf16 (u32 pairs)
 __global__ void k_kv_append(const uint32_t* __restrict__ qkv, const int64_t* __restrict__ pos,
                             int64_t b, int q, int h, int dh2, int64_t t1,
@@ -2343,6 +2451,26 @@ int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_
   const int64_t rows = b * q * 2 * h;
   k_kv_append<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(
       static_cast<const uint32_t*>(d_qkv), d_pos, b, q, h, dh / 2, t1, static_cast<uint32_t*>(d_kv));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_decode_attention_bf16(const void* d_qkv, const void* d_kv, const int64_t* d_qpos, int64_t b,
+                             int32_t q, int32_t h, int32_t dh, int64_t t1, void* d_out,
+                             void* stream) {
+  if (b < 1 || q < 1 || q > DA_QMAX || h < 1 || dh != 64 || t1 < 1 || (int64_t)q * t1 > 51200)
+    return fail(EE_ERR_ARG, "decode attention: q <= 8, dh = 64, q * t1 <= 51200");
+  if (!d_qkv || !d_kv || !d_qpos || !d_out) return fail(EE_ERR_ARG, "null pointer");
+  if (reinterpret_cast<uintptr_t>(d_kv) % 16) return fail(EE_ERR_ARG, "misaligned cache");
+  const size_t smem = (size_t)q * t1 * 4;
+  static size_t smem_set = 48 * 1024;
+  if (smem > smem_set) {
+    EE_CUDA(cudaFuncSetAttribute(k_decode_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  k_decode_attn<<<(unsigned)(b * h), DA_THREADS, smem, (cudaStream_t)stream>>>(
+      static_cast<const uint16_t*>(d_qkv), static_cast<const uint16_t*>(d_kv), d_qpos, b, q, h, t1,
+      static_cast<uint16_t*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

@@ -116,11 +116,15 @@ class GPT2Decoder:
         st = nat.stream_handle(torch)
         # key j visible to query (b, i) iff j <= pos[b, i]; padding queries see key 0 only
         qpos = torch.where(valid, pos, torch.zeros_like(pos))
-        mask = (self.key_idx[None, None, :] <= qpos[:, :, None]) & (self.key_idx[None, None, :] < T)
-        # additive bf16 mask built once per pass (a boolean mask is converted by
-        # the attention backend in every layer: three extra kernels per layer)
-        mask = torch.zeros(mask.shape, dtype=h.dtype, device=h.device).masked_fill_(
-            ~mask, float("-inf"))[:, None, :, :]
+        # short passes (decode, flushes: q <= 8 tokens) attend with the length-aware
+        # kernel (ee_decode_attention_bf16), which reads only keys 0 .. qpos; longer
+        # chunks use SDPA with an additive bf16 mask built once per pass
+        short = q <= 8 and Dh == 64 and q * (T + 1) <= 51200
+        qpos_c = qpos.to(torch.int64).contiguous()
+        if not short:
+            vis = (self.key_idx[None, None, :] <= qpos[:, :, None]) & (self.key_idx[None, None, :] < T)
+            mask = torch.zeros(vis.shape, dtype=h.dtype, device=h.device).masked_fill_(
+                ~vis, float("-inf"))[:, None, :, :]
         if l1 <= l0:
             return h
         # the residual stream is owned here and updated in place by the fused
@@ -140,10 +144,16 @@ class GPT2Decoder:
             # K and V rows straight from the projection into their cache slots (one kernel)
             nat.check(lib.ee_kv_append_bf16(qkv.data_ptr(), wpos.data_ptr(), B, q, H, Dh, T + 1,
                                             self.kv_cache[l].data_ptr(), st))
-            qh = qkv.view(B, q, 3, H, Dh)[:, :, 0].transpose(1, 2)
-            att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l], attn_mask=mask)
-            add_ln(F.linear(att.transpose(1, 2).reshape(B, q, d), w["o_w"], w["o_b"]),
-                   w["ln2_w"], w["ln2_b"])
+            if short:  # decode / flush passes: length-aware kernel, output already [B, q, d]
+                att = torch.empty(B, q, d, dtype=h.dtype, device=h.device)
+                nat.check(lib.ee_decode_attention_bf16(qkv.data_ptr(), self.kv_cache[l].data_ptr(),
+                                                       qpos_c.data_ptr(), B, q, H, Dh, T + 1,
+                                                       att.data_ptr(), st))
+            else:
+                qh = qkv.view(B, q, 3, H, Dh)[:, :, 0].transpose(1, 2)
+                att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l],
+                                                     attn_mask=mask).transpose(1, 2).reshape(B, q, d)
+            add_ln(F.linear(att, w["o_w"], w["o_b"]), w["ln2_w"], w["ln2_b"])
             # bias + tanh-GELU in the GEMM epilogue (cuBLASLt), then the projection
             t = torch._addmm_activation(w["fc_b"], x.reshape(B * q, d), w["fc_w"].t(), use_gelu=True)
             y = F.linear(t.view(B, q, -1), w["pr_w"], w["pr_b"])

@@ -150,3 +150,32 @@ def test_add_layernorm_matches_torch(cuda):
             x.data_ptr(), nat.stream_handle(torch)))
         assert torch.equal(h, h_ref)
         assert torch.allclose(x.float(), x_ref, rtol=2 ** -7, atol=2 ** -7)
+
+
+def test_decode_attention_matches_sdpa(cuda):
+    """ee_decode_attention_bf16 (length-aware, q <= 8 queries per sequence)
+    against torch SDPA with the equivalent mask, fp32 reference on the same
+    bf16 operands; padding queries (qpos 0) see key 0 only."""
+    import torch
+
+    from paper_2312_05385_b200 import _native as nat
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    B, H, Dh, T1 = 6, 4, 64, 197
+    for q in (1, 3, 8):
+        qkv = torch.randn(B, q, 3, H, Dh, generator=g, device="cuda").to(torch.bfloat16)
+        kv = torch.randn(2, B, H, T1, Dh, generator=g, device="cuda").to(torch.bfloat16)
+        qpos = torch.randint(0, T1 - 1, (B, q), generator=g, device="cuda")
+        qpos[0, -1] = 0
+        qpos[1, 0] = T1 - 2
+        out = torch.empty(B, q, H * Dh, dtype=torch.bfloat16, device="cuda")
+        nat.check(nat.load_library().ee_decode_attention_bf16(
+            qkv.data_ptr(), kv.data_ptr(), qpos.data_ptr(), B, q, H, Dh, T1, out.data_ptr(),
+            nat.stream_handle(torch)))
+        qh = qkv[:, :, 0].transpose(1, 2).float()
+        keys = torch.arange(T1, device="cuda")
+        vis = (keys[None, None, :] <= qpos[:, :, None]) & (keys[None, None, :] < T1 - 1)
+        ref = torch.nn.functional.scaled_dot_product_attention(
+            qh, kv[0].float(), kv[1].float(), attn_mask=vis[:, None])
+        ref = ref.transpose(1, 2).reshape(B, q, H * Dh)
+        assert torch.allclose(out.float(), ref, rtol=2e-2, atol=2e-2), (out.float() - ref).abs().max()
