@@ -167,9 +167,11 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
  * are cleared), so chaining ramps needs no extra launch. Outputs per row: d_err f32, d_label i32,
  * d_exit u8, optional d_logits f32 [b, k]. Then, in the same launch, the
  * surviving (alive, non-exiting) rows are compacted in ascending row order
- * into d_keep with their count in *d_nkeep, and each exiting row's (label,
- * err, site) is scattered to its request slot d_slot[row] (NULL = row index)
- * in d_slot_label / d_slot_err / d_slot_site (all NULL = no scatter). */
+ * into d_keep with their count in *d_nkeep (both NULL: no compaction, e.g. a
+ * feedback-mode batch that keeps every row, and no cross-CTA step at all), and
+ * each exiting row's (label, err, site) is scattered to its request slot
+ * d_slot[row] (NULL = row index) in d_slot_label / d_slot_err / d_slot_site
+ * (all NULL = no scatter). */
 int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, int64_t b,
                        int32_t c, int32_t hw, int32_t nhwc, const void* d_w, int32_t w_bf16,
                        const float* d_bias, int32_t k, int32_t conf, double threshold,

@@ -1982,8 +1982,9 @@ static int exit_out(ee_workspace* ws, cudaStream_t st, int64_t b, const int32_t*
                     int32_t site, float* d_err, int32_t* d_label, uint8_t* d_exit,
                     float* d_logits, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
                     float* d_slot_err, int32_t* d_slot_site, exitc::Out* o) {
-  if (!d_err || !d_label || !d_exit || !d_keep || !d_nkeep)
-    return fail(EE_ERR_ARG, "null output pointer");
+  if (!d_err || !d_label || !d_exit) return fail(EE_ERR_ARG, "null output pointer");
+  if ((d_keep == nullptr) != (d_nkeep == nullptr))
+    return fail(EE_ERR_ARG, "keep and n_keep must both be given (compaction) or both be null");
   if ((d_slot_label != nullptr) != (d_slot_err != nullptr) ||
       (d_slot_label != nullptr) != (d_slot_site != nullptr))
     return fail(EE_ERR_ARG, "slot scatter targets must be all given or all null");

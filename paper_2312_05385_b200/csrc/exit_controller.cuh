@@ -105,7 +105,8 @@ __device__ __forceinline__ void confidence(const float* l, int K, int conf, floa
   *label_out = arg;
 }
 
-// last CTA: stable compaction of the survivors + scatter of exiting rows
+// last CTA: stable compaction of the survivors (the exiting rows were already
+// scattered to their request slots by the CTA or warp that owns the row)
 __device__ void compact_and_scatter(int64_t B, const uint8_t* alive_in, const Out& o) {
   // alive_in already has this launch's exits cleared (keep = alive after the ramp)
   __shared__ int warp_tot[THREADS / 32];
@@ -125,12 +126,6 @@ __device__ void compact_and_scatter(int64_t B, const uint8_t* alive_in, const Ou
     int off = base;
     for (int w = 0; w < wid; ++w) off += warp_tot[w];
     if (keep) o.keep[off + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
-    if (valid && ex && o.slot_label) {
-      const int32_t s = o.slot ? o.slot[row] : (int32_t)row;
-      o.slot_label[s] = __ldcg(o.label + row);
-      o.slot_err[s] = __ldcg(o.err + row);
-      o.slot_site[s] = o.site;
-    }
     __syncthreads();
     if (threadIdx.x == 0)
       for (int w = 0; w < THREADS / 32; ++w) base += warp_tot[w];
@@ -140,6 +135,15 @@ __device__ void compact_and_scatter(int64_t B, const uint8_t* alive_in, const Ou
     *o.n_keep = base;
     *o.done = 0u;  // every other CTA has counted: ready for the next launch
   }
+}
+
+// an exiting row's (label, err, site) -> its request slot
+__device__ __forceinline__ void scatter_row(const Out& o, int64_t row, int32_t label, float err) {
+  if (!o.slot_label) return;
+  const int32_t s = o.slot ? o.slot[row] : (int32_t)row;
+  o.slot_label[s] = label;
+  o.slot_err[s] = err;
+  o.slot_site[s] = o.site;
 }
 
 __device__ __forceinline__ bool last_cta(unsigned* done) {
@@ -259,9 +263,10 @@ __global__ void __launch_bounds__(THREADS)
       o.label[row] = label;
       o.exits[row] = ex ? 1 : 0;
       if (ex && alive_in) alive_in[row] = 0;  // exited rows stop being alive
+      if (ex) scatter_row(o, row, label, err);
     }
   }
-  if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
+  if (o.keep && last_cta(o.done)) compact_and_scatter(B, alive_in, o);
 }
 
 // confidence() with the row held in registers (NPL values per lane, K <= 32
@@ -345,9 +350,10 @@ __global__ void __launch_bounds__(THREADS)
       o.label[row] = label;
       o.exits[row] = ex ? 1 : 0;
       if (ex && alive_in) alive_in[row] = 0;
+      if (ex) scatter_row(o, row, label, err);
     }
   }
-  if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
+  if (o.keep && last_cta(o.done)) compact_and_scatter(B, alive_in, o);
 }
 
 // Wide heads (an LM-head ramp: K = 50257): one CTA per row, block-wide
@@ -415,8 +421,9 @@ __global__ void __launch_bounds__(ROW_THREADS)
     o.label[row] = arg;
     o.exits[row] = ex ? 1 : 0;
     if (ex && alive_in) alive_in[row] = 0;
+    if (ex) scatter_row(o, row, arg, err);
   }
-  if (last_cta(o.done)) compact_and_scatter(B, alive_in, o);
+  if (o.keep && last_cta(o.done)) compact_and_scatter(B, alive_in, o);
 }
 
 // gather surviving rows into a dense buffer (downstream blocks skip exited rows)

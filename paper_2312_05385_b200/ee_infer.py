@@ -129,7 +129,7 @@ class EEPipeline:
                 th = thresholds[r] if dev_th else float(thresholds[r])
                 if mode == "feedback":  # rows are the identity: write signals in place
                     res = head(h, th, alive=alive, slot=rows, slots=slots,
-                               out_err=ramp_err[r], out_label=ramp_label[r])
+                               out_err=ramp_err[r], out_label=ramp_label[r], compact=False)
                 else:
                     res = head(h, th, alive=alive, slot=rows, slots=slots)
                     ramp_err[r].index_copy_(0, rows.long(), res.err)
@@ -149,7 +149,7 @@ class EEPipeline:
                 final_label.index_copy_(0, rows.long(), torch.argmax(logits, dim=1).to(torch.int32))
                 # every still-alive row is released with the final model's label
                 exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=R, alive=alive,
-                                 slot=rows, slots=slots)
+                                 slot=rows, slots=slots, compact=(mode != "feedback"))
         out = BatchResult(slots.label, slots.site, slots.err, ramp_err, ramp_label, final_label)
         if timed:
             end = torch.cuda.Event(enable_timing=True)

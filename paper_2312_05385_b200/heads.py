@@ -61,14 +61,14 @@ class SlotTable:
         return cls(buf[0], buf[1].view(torch.float32), buf[2])
 
 
-def _outputs(torch, b, k, want_logits, out_err=None, out_label=None, out_exits=None):
+def _outputs(torch, b, k, want_logits, out_err=None, out_label=None, out_exits=None, compact=True):
     dev = "cuda"
     return (out_err if out_err is not None else torch.empty(b, dtype=torch.float32, device=dev),
             out_label if out_label is not None else torch.empty(b, dtype=torch.int32, device=dev),
             out_exits if out_exits is not None else torch.empty(b, dtype=torch.uint8, device=dev),
             torch.empty((b, k), dtype=torch.float32, device=dev) if want_logits else None,
-            torch.empty(b, dtype=torch.int32, device=dev),
-            torch.empty(1, dtype=torch.int32, device=dev))
+            torch.empty(b, dtype=torch.int32, device=dev) if compact else None,
+            torch.empty(1, dtype=torch.int32, device=dev) if compact else None)
 
 
 def _check_aux(torch, b, alive, slot):
@@ -97,10 +97,11 @@ class ExitController:
 
     def __call__(self, feat, threshold, *, alive=None, slot=None,
                  slots: SlotTable | None = None, want_logits: bool = False,
-                 out_err=None, out_label=None) -> ExitResult:
+                 out_err=None, out_label=None, compact: bool = True) -> ExitResult:
         """feat: [B, C, H, W] / [B, C] (NCHW) or channels-last memory format; fp32 or bf16.
         `threshold` is a float or a one-element CUDA f64 tensor (graph-capture friendly);
-        out_err / out_label let the caller supply the per-row output buffers."""
+        out_err / out_label let the caller supply the per-row output buffers.
+        compact=False: no survivor list (feedback mode keeps every row)."""
         torch = nat.torch_cuda()
         if feat.dtype not in (torch.float32, torch.bfloat16) or not feat.is_cuda:
             raise ParameterError("feat must be a CUDA fp32 or bf16 tensor")
@@ -120,14 +121,14 @@ class ExitController:
             raise ParameterError(f"feat has {c} channels, head expects {self.c}")
         _check_aux(torch, b, alive, slot)
         err, label, exits, logits, keep, n_keep = _outputs(torch, b, self.k, want_logits,
-                                                           out_err, out_label)
+                                                           out_err, out_label, compact=compact)
         th_val, th_ptr = _threshold_args(torch, threshold)
         nat.check(nat.load_library().ee_exit_controller(
             nat.workspace(), feat.data_ptr(), int(feat.dtype == torch.bfloat16), b, c, hw, nhwc,
             self.weight.data_ptr(), int(self.weight.dtype == torch.bfloat16), nat.ptr(self.bias),
             self.k, CONF[self.conf], th_val, th_ptr, nat.ptr(alive), nat.ptr(slot), self.site,
             err.data_ptr(), label.data_ptr(), exits.data_ptr(), nat.ptr(logits),
-            keep.data_ptr(), n_keep.data_ptr(),
+            nat.ptr(keep), nat.ptr(n_keep),
             nat.ptr(slots.label if slots else None), nat.ptr(slots.err if slots else None),
             nat.ptr(slots.site if slots else None), nat.stream_handle(torch)))
         return ExitResult(err, label, exits, keep, n_keep, logits)
@@ -144,7 +145,8 @@ def _threshold_args(torch, threshold):
 
 def exit_from_logits(logits, threshold, *, conf: str = "maxprob", site: int = 0,
                      alive=None, slot=None, slots: SlotTable | None = None,
-                     out_err=None, out_label=None, out_exits=None) -> ExitResult:
+                     out_err=None, out_label=None, out_exits=None,
+                     compact: bool = True) -> ExitResult:
     """Confidence + compare + compaction + scatter over precomputed fp32 logits [B, K]."""
     torch = nat.torch_cuda()
     if logits.dtype != torch.float32 or logits.dim() != 2 or not logits.is_cuda:
@@ -152,12 +154,13 @@ def exit_from_logits(logits, threshold, *, conf: str = "maxprob", site: int = 0,
     logits = logits.contiguous()
     b, k = logits.shape
     _check_aux(torch, b, alive, slot)
-    err, label, exits, _, keep, n_keep = _outputs(torch, b, k, False, out_err, out_label, out_exits)
+    err, label, exits, _, keep, n_keep = _outputs(torch, b, k, False, out_err, out_label, out_exits,
+                                                  compact=compact)
     th_val, th_ptr = _threshold_args(torch, threshold)
     nat.check(nat.load_library().ee_exit_from_logits(
         nat.workspace(), logits.data_ptr(), b, k, CONF[conf], th_val, th_ptr, nat.ptr(alive),
         nat.ptr(slot), site, err.data_ptr(), label.data_ptr(), exits.data_ptr(),
-        keep.data_ptr(), n_keep.data_ptr(),
+        nat.ptr(keep), nat.ptr(n_keep),
         nat.ptr(slots.label if slots else None), nat.ptr(slots.err if slots else None),
         nat.ptr(slots.site if slots else None), nat.stream_handle(torch)))
     return ExitResult(err, label, exits, keep, n_keep, None)
@@ -235,12 +238,13 @@ class LargeRampHead:
 
     def __call__(self, feat, threshold, *, alive=None, slot=None,
                  slots: SlotTable | None = None, want_logits: bool = False,
-                 out_err=None, out_label=None) -> ExitResult:
+                 out_err=None, out_label=None, compact: bool = True) -> ExitResult:
         torch = nat.torch_cuda()
         x = pool_bf16(feat) if feat.dim() == 4 else feat.to(torch.bfloat16)
         logits = linear_tc(x, self.weight, self.bias)
         res = exit_from_logits(logits, threshold, conf=self.conf, site=self.site, alive=alive,
-                               slot=slot, slots=slots, out_err=out_err, out_label=out_label)
+                               slot=slot, slots=slots, out_err=out_err, out_label=out_label,
+                               compact=compact)
         if want_logits:
             res.logits = logits
         return res
