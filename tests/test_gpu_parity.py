@@ -357,6 +357,36 @@ def test_axis_family_path_matches_generic_and_oracle(cuda, r, n, nan_base):
     assert np.array_equal(hist2, hist_a) and np.array_equal(ok2, ok_a)
 
 
+@pytest.mark.parametrize("r,n", [(5, 3001), (12, 1), (12, 31), (4, 64)])
+def test_axis_family_edges_and_fallback(cuda, r, n):
+    """Single-coordinate rows outside k_axis's envelope (odd R) take the generic
+    path; tiny windows (n < one chunk per CTA) run k_axis; all exact vs the oracle."""
+    from paper_2312_05385_b200 import _native
+
+    rng = np.random.default_rng(8800 + r + n)
+    scores, cext, serve, vanilla, _ = random_window(rng, n, r, 1, nan_frac=0.02)
+    th = np.full((1 + r * 20, r), 0.45)
+    for j in range(r):
+        th[1 + j * 20:1 + (j + 1) * 20, j] = np.arange(20) / 19.0
+    arrays = WindowArrays(scores, cext.astype(np.uint8))
+    prof = make_chain(r + 1)
+    ev = WindowEvaluator.from_arrays(arrays, find_feasible_sites(prof)[:r], prof, mode="hist")
+    _native.profile_read()
+    _native.profile_enable(True)
+    try:
+        hist, ok = ev.histograms(th)
+        acc, sav = ev.evaluate_many(th)
+    finally:
+        _native.profile_enable(False)
+    launched = _native.profile_read()
+    assert ("k_axis" in launched) == (r % 2 == 0), launched
+    hist_o, ok_o = O.eval_hist(scores, cext, th)
+    assert np.array_equal(hist, hist_o) and np.array_equal(ok, ok_o)
+    acc_o, sav_o = O.eval_thresholds(scores, cext, ev.serve, ev.vanilla_ms, th)
+    assert np.array_equal(acc, acc_o)
+    np.testing.assert_allclose(sav, sav_o, rtol=SAV_RTOL, atol=1e-12)
+
+
 @pytest.mark.parametrize("r,n,m,c_rep", [(2, 1, 5, 1), (4, 31, 17, 1), (6, 33, 64, 1),
                                          (10, 4099, 127, 1), (12, 70001, 64, 1), (12, 2500, 40, 20),
                                          (14, 9000, 100, 1), (16, 12345, 126, 2)])
