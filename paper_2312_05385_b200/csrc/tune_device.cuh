@@ -139,69 +139,90 @@ __global__ void __launch_bounds__(THREADS, 1)
   int rounds = 0;
   while (true) {
     ++rounds;
-    if (tid == 0) {
-      int k = 0;
-      for (int i = 0; i < r; ++i)
-        if (th[i] < 1.0) elig[k++] = i;
-      nelig = k;
-      for (int pos = 0; pos < k; ++pos) {
-        for (int j = 0; j < r; ++j) cand[pos][j] = th[j];
-        const int i = elig[pos];
-        const double up = __dadd_rn(th[i], steps[i]);
-        cand[pos][i] = up < 1.0 ? up : 1.0;
-      }
+    if (tid < 32) {  // eligible ramps in index order (r <= 31: one warp)
+      const bool e = tid < r && th[tid] < 1.0;
+      const unsigned m = __ballot_sync(0xffffffffu, e);
+      if (e) elig[__popc(m & ((1u << tid) - 1))] = tid;
+      if (tid == 0) nelig = __popc(m);
     }
     __syncthreads();
     if (nelig == 0) break;
+    for (int q = tid; q < nelig * r; q += THREADS) {  // candidate rows, all entries in parallel
+      const int pos = q / r, j = q - pos * r;
+      const int i = elig[pos];
+      double v = th[j];
+      if (j == i) {
+        const double up = __dadd_rn(th[i], steps[i]);
+        v = up < 1.0 ? up : 1.0;
+      }
+      cand[pos][j] = v;
+    }
+    __syncthreads();
     evaluate(nelig);
-    if (tid == 0) {
-      n_evals += nelig;
-      int best = -1;
-      // key: (1, dsav, -i) when the increment loses no accuracy, else
-      // (0, dsav / dloss, dsav, -i); lexicographic max (tuner.py:141-153)
-      int bk0 = 0;
-      double bk1 = 0.0, bk2 = 0.0;
-      int bk3 = 0;
-      unsigned viol = 0;
-      for (int pos = 0; pos < nelig; ++pos) {
-        const int i = elig[pos];
-        if (accs[pos] < floor_eps) {
-          viol |= 1u << i;
-          continue;
-        }
+    __shared__ int s_best;
+    __shared__ unsigned s_viol;
+    __shared__ bool s_allmin;
+    if (tid < 32) {
+      // every eligible increment scored by its own lane; key (1, dsav, -i) when
+      // it loses no accuracy, else (0, dsav / dloss, dsav, -i); the warp keeps
+      // the lexicographic max (tuner.py:141-153). -i makes the max unique, so
+      // the reduction picks what the reference's in-order scan picks.
+      const int pos = tid;
+      const bool valid = pos < nelig;
+      const int i = valid ? elig[pos] : 0;
+      const bool viol_me = valid && accs[pos] < floor_eps;
+      bool ok = valid && !viol_me;
+      int k0 = 0, k3 = -i;
+      double k1 = 0.0, k2 = 0.0;
+      if (ok) {
         const double dsav = __dsub_rn(savs[pos], sav_cur);
         const double dloss = __dsub_rn(acc_cur, accs[pos]);
-        int k0;
-        double k1, k2;
         if (dloss <= ACC_EPS) {
           k0 = 1;
           k1 = dsav;
-          k2 = 0.0;
         } else {
-          k0 = 0;
           k1 = __ddiv_rn(dsav, dloss);
           k2 = dsav;
         }
-        const int k3 = -i;
-        bool better;
-        if (best < 0)
-          better = true;
-        else if (k0 != bk0)
-          better = k0 > bk0;
-        else if (k1 != bk1)
-          better = k1 > bk1;
-        else if (k0 == 0 && k2 != bk2)
-          better = k2 > bk2;
-        else
-          better = k3 > bk3;
-        if (better) {
-          best = pos;
-          bk0 = k0;
-          bk1 = k1;
-          bk2 = k2;
-          bk3 = k3;
-        }
       }
+      int best = ok ? pos : -1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const bool ok2 = __shfl_xor_sync(0xffffffffu, ok, o);
+        const int a0 = __shfl_xor_sync(0xffffffffu, k0, o), a3 = __shfl_xor_sync(0xffffffffu, k3, o);
+        const double a1 = __shfl_xor_sync(0xffffffffu, k1, o), a2 = __shfl_xor_sync(0xffffffffu, k2, o);
+        const int b2 = __shfl_xor_sync(0xffffffffu, best, o);
+        bool take;
+        if (!ok2)
+          take = false;
+        else if (!ok)
+          take = true;
+        else if (a0 != k0)
+          take = a0 > k0;
+        else if (a1 != k1)
+          take = a1 > k1;
+        else if (k0 == 0 && a2 != k2)
+          take = a2 > k2;
+        else
+          take = a3 > k3;
+        if (take) ok = true, k0 = a0, k1 = a1, k2 = a2, k3 = a3, best = b2;
+      }
+      unsigned vm = viol_me ? 1u << i : 0u;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) vm |= __shfl_xor_sync(0xffffffffu, vm, o);
+      const bool at_min = !valid || steps[i] <= __dadd_rn(p.min_step, ACC_EPS);
+      const bool all_min = __all_sync(0xffffffffu, at_min);
+      if (tid == 0) {
+        s_best = best;
+        s_viol = vm;
+        s_allmin = all_min;
+      }
+    }
+    __syncwarp();
+    if (tid == 0) {
+      n_evals += nelig;
+      const int best = s_best;
+      const unsigned viol = s_viol;
       if (best >= 0) {
         const int i = elig[best];
         const double up = __dadd_rn(th[i], steps[i]);
@@ -209,11 +230,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         acc_cur = accs[best];
         sav_cur = savs[best];
         steps[i] = __dmul_rn(steps[i], 2.0);
-      } else {
-        bool all_min = true;
-        for (int pos = 0; pos < nelig; ++pos)
-          if (!(steps[elig[pos]] <= __dadd_rn(p.min_step, ACC_EPS))) all_min = false;
-        if (all_min) done = 1;
+      } else if (s_allmin) {
+        done = 1;
       }
       if (!done) {
         for (int i = 0; i < r; ++i)
