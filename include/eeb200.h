@@ -101,6 +101,18 @@ int ee_eval_thresholds(ee_workspace* ws, const double* d_scores, const uint32_t*
                        const double* h_th, int64_t c, int32_t mode, int64_t* d_hist,
                        int64_t* d_ok, double* d_acc, double* d_sav, void* stream);
 
+/* The same HIST-mode evaluation over nwin windows at once (same n, r and
+ * candidate rows; d_scores_list / d_bits_list are DEVICE arrays of nwin device
+ * pointers, each window laid out as for ee_eval_thresholds): one persistent
+ * sweep launch that builds its tables once and streams the windows back to
+ * back, then one finalisation launch. acc/sav are [nwin, c]. Diagonal
+ * candidate rows only (every row repeats one threshold; <= 64 distinct
+ * values, c <= 512, even r <= 16); anything else returns EE_ERR_ARG. */
+int ee_eval_thresholds_windows(ee_workspace* ws, const double* const* d_scores_list,
+                               const uint32_t* const* d_bits_list, int32_t nwin, int64_t n,
+                               int32_t r, const double* h_serve, double vanilla, const double* h_th,
+                               int64_t c, double* d_acc, double* d_sav, void* stream);
+
 /* The same evaluation from HOST buffers (the reference's own calling
  * convention: numpy arrays in, numpy arrays out, engine.py:165-170):
  * h_scores f64 [n, r], h_correct_ext f64 [n, r+1] (0.0/1.0, else

@@ -530,6 +530,8 @@ struct ee_workspace {
   long long* d_diag_acc = nullptr;
   bool diag_acc_dirty = true;
   void* d_exit_done = nullptr;  // exit controllers' completion counter (self-resetting)
+  void* d_accw = nullptr;       // per-window accumulators of ee_eval_thresholds_windows
+  size_t accw_cap = 0;
   void* h_tune = nullptr;  // ee_tune results: mapped pinned memory the kernel writes
   size_t tune_host_cap = 0;
   // axis-family sweep: per-CTA partial cells and their 64-bit totals
@@ -724,6 +726,7 @@ int ee_workspace_destroy(ee_workspace* ws) {
   if (ws->d_axis_part) cudaFree(ws->d_axis_part);
   if (ws->h_tune) cudaFreeHost(ws->h_tune);
   if (ws->d_exit_done) cudaFree(ws->d_exit_done);
+  if (ws->d_accw) cudaFree(ws->d_accw);
   if (ws->d_axis_tot) cudaFree(ws->d_axis_tot);
   if (ws->d_in) cudaFree(ws->d_in);
   for (auto& m : ws->marks) cudaEventDestroy(m.a), cudaEventDestroy(m.b);
@@ -1388,6 +1391,83 @@ static int eval_axis(ee_workspace* ws, const double* d_scores, const uint32_t* d
 #undef EE_AXIS_CASE
   }
   if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_axis_fin: ") + cudaGetErrorString(e));
+  return EE_OK;
+}
+
+}  // extern "C"
+template <int R>
+static cudaError_t launch_windows(const diag2::Params& p, const double* const* sl,
+                                 const uint32_t* const* bl, int nwin, long long* accw,
+                                 double* acc, double* sav, cudaStream_t st, ee_workspace* ws) {
+  static bool attr_set = false;
+  constexpr int smem = diag3::Big::smem_bytes<R>();
+  constexpr int fsmem = diag3::Big::fin_bytes<R>();
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(diag3::k_diag3_windows<R>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const unsigned grid = diag_grid(ws, p.n);
+  {
+    ProfScope ps(ws, st, "k_diag3_windows");
+    diag3::k_diag3_windows<R><<<grid, 1024, smem, st>>>(p, sl, bl, nwin, accw);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ProfScope ps(ws, st, "k_diag3_windows_fin");
+  diag3::k_diag3_windows_fin<R><<<(unsigned)nwin, 1024, fsmem, st>>>(p, accw, acc, sav);
+  return cudaGetLastError();
+}
+extern "C" {
+
+int ee_eval_thresholds_windows(ee_workspace* ws, const double* const* d_scores_list,
+                               const uint32_t* const* d_bits_list, int32_t nwin, int64_t n,
+                               int32_t r, const double* h_serve, double vanilla, const double* h_th,
+                               int64_t c, double* d_acc, double* d_sav, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (nwin < 1 || n < 1 || c < 1 || c > diag2::MAX_POS || r < 2 || r > diag2::RMAX || (r & 1))
+    return fail(EE_ERR_ARG, "windows: nwin, n, c >= 1, c <= 512, even r <= 16");
+  if (!d_scores_list || !d_bits_list || !h_serve || !h_th || !d_acc || !d_sav)
+    return fail(EE_ERR_ARG, "null pointer");
+  std::vector<double> u;
+  if (!diagonal_rows(h_th, c, r, u) || u.empty() || (int)u.size() > diag3::MAX_M)
+    return fail(EE_ERR_ARG, "windows: candidate rows must be diagonal with <= 64 distinct values");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  ws->resident = false;
+  if (ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n)) > diag3::Big::MAX_CTA_CHUNKS)
+    return fail(EE_ERR_ARG, "windows: window too large for the packed cell counters");
+  diag2::Params p{};
+  if (!plan_bins(u, &p.a, &p.c0, p.tab)) return fail(EE_ERR_ARG, "windows: thresholds do not fit the bin grid");
+  const int m = (int)u.size();
+  p.n = n;
+  p.m = m;
+  p.C = c;
+  p.vanilla = vanilla;
+  for (int j = 0; j <= r; ++j) p.serve[j] = h_serve[j];
+  for (int i = 0; i < m; ++i) p.u[i] = u[i];
+  for (int64_t k = 0; k < c; ++k) {
+    const double v = h_th[k * r];
+    p.pos[k] = v == v ? (unsigned char)(std::lower_bound(u.begin(), u.end(), canon(v)) - u.begin())
+                      : (unsigned char)255;
+  }
+  const size_t acc_b = (size_t)nwin * diag2::ACC_WORDS * 8;
+  if (acc_b > ws->accw_cap) {
+    if (ws->d_accw) EE_CUDA(cudaFree(ws->d_accw));
+    ws->d_accw = nullptr;
+    EE_CUDA(cudaMalloc(&ws->d_accw, acc_b));
+    ws->accw_cap = acc_b;
+  }
+  EE_CUDA(cudaMemsetAsync(ws->d_accw, 0, acc_b, st));
+  cudaError_t e;
+  switch (r) {
+#define EE_WIN_CASE(K) case K: e = launch_windows<K>(p, d_scores_list, d_bits_list, nwin, static_cast<long long*>(ws->d_accw), d_acc, d_sav, st, ws); break;
+    EE_WIN_CASE(2) EE_WIN_CASE(4) EE_WIN_CASE(6) EE_WIN_CASE(8) EE_WIN_CASE(10) EE_WIN_CASE(12)
+    EE_WIN_CASE(14) default: e = launch_windows<16>(p, d_scores_list, d_bits_list, nwin, static_cast<long long*>(ws->d_accw), d_acc, d_sav, st, ws); break;
+#undef EE_WIN_CASE
+  }
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_diag3_windows: ") + cudaGetErrorString(e));
   return EE_OK;
 }
 

@@ -55,6 +55,122 @@ struct Cfg {
 using Big = Cfg<1024, 32>;   // one CTA per SM
 using Pair = Cfg<512, 16>;   // two CTAs per SM
 
+// Finalise one window from its merged per-position totals gD (+ this CTA's own
+// unmerged sums cF / osum / own_corr when given): prefix over positions, exact
+// histograms and correct counts, the k_finalize TwoSum chain, outputs per
+// candidate. zero_acc leaves gD and the completion counters zeroed.
+template <int R, int THREADS>
+__device__ void finalize_window(const Params& P, unsigned char* scratch, long long* gD, const int* cF,
+                                const int* osum, unsigned long long own_corr, bool zero_acc,
+                                int64_t n, int64_t* hist_out, int64_t* ok_out, double* acc_out,
+                                double* sav_out) {
+  constexpr int WARPS = THREADS / 32;
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = P.m;
+  const int M1 = m + 1;
+  long long* hst = reinterpret_cast<long long*>(scratch);  // [R+1][M1] (F_j first)
+  long long* okp = hst + (R + 1) * M1;
+  double* prs = reinterpret_cast<double*>(okp + M1);
+  double* pes = prs + (R + 1) * M1;
+  double* accp = pes + (R + 1) * M1;
+  double* savp = accp + M1;
+  __shared__ long long s_corr_all;
+  if (tid == 0) {
+    s_corr_all = (long long)(__ldcg(gD + diag2::CORR_IDX) + own_corr);
+    if (zero_acc) {
+      gD[diag2::CORR_IDX] = 0;
+      P.done[0] = 0u;
+      P.done[1] = 0u;
+    }
+  }
+  for (int q = tid; q < (R + 1) * m; q += THREADS) {  // global + own (+ zero for the next launch)
+    const int j = q / m, p = q - j * m;
+    const long long g = __ldcg(gD + j * diag2::W + p);
+    if (zero_acc) gD[j * diag2::W + p] = 0;
+    const long long own = !cF ? 0 : j < R ? (long long)cF[j * MAX_M + p] : (long long)osum[p];
+    hst[j * M1 + p] = g + own;
+  }
+  __syncthreads();
+  for (int row = warp; row <= R; row += WARPS) {  // inclusive prefix over p < m: F_j(p), O(p)
+    long long* a = hst + row * M1;
+    long long carry = 0;
+    for (int p0 = 0; p0 < m; p0 += 32) {
+      const int p = p0 + lane;
+      long long x = p < m ? a[p] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      x += carry;
+      if (p < m) a[p] = x;
+      carry = __shfl_sync(FULL, x, 31);
+    }
+  }
+  __syncthreads();
+  const long long corrR = s_corr_all;
+  for (int p = tid; p < M1; p += THREADS) {  // F -> histograms, O -> correct counts
+    if (p == m) {  // NaN threshold row: nothing exits
+      for (int j = 0; j < R; ++j) hst[j * M1 + p] = 0;
+      hst[R * M1 + p] = n;
+      okp[p] = corrR;
+      continue;
+    }
+    okp[p] = corrR + hst[R * M1 + p];
+    long long fprev = 0;
+    for (int j = 0; j < R; ++j) {
+      const long long f = hst[j * M1 + p];
+      hst[j * M1 + p] = f - fprev;
+      fprev = f;
+    }
+    hst[R * M1 + p] = n - fprev;
+  }
+  __syncthreads();
+  for (int i = tid; i < (R + 1) * M1; i += THREADS) {  // error-free products
+    const int site = i / M1;
+    const double x = (double)hst[i];
+    const double pr = __dmul_rn(x, P.serve[site]);
+    prs[i] = pr;
+    pes[i] = __fma_rn(x, P.serve[site], -pr);
+  }
+  __syncthreads();
+  for (int p = tid; p < M1; p += THREADS) {  // the ordered TwoSum chain of k_finalize
+    double hi = 0.0, lo = 0.0;
+#pragma unroll
+    for (int site = 0; site <= R; ++site) {
+      double s2, e;
+      two_sum(hi, prs[site * M1 + p], s2, e);
+      hi = s2;
+      lo = __dadd_rn(lo, __dadd_rn(e, pes[site * M1 + p]));
+    }
+    double tot2, e;
+    two_sum(hi, lo, tot2, e);
+    const double dn = (double)n;
+    accp[p] = __ddiv_rn((double)okp[p], dn);
+    savp[p] = __dsub_rn(P.vanilla, __ddiv_rn(tot2, dn));
+  }
+  __syncthreads();
+  auto posof = [&](int64_t c) -> int {
+    const int q = P.C <= diag2::MAX_POS ? P.pos[c] : P.pos_dev[c];
+    return q == 255 ? m : q;
+  };
+  if (hist_out)
+    for (int64_t i = tid; i < P.C * (R + 1); i += THREADS) {
+      const int64_t c = i / (R + 1);
+      const int site = (int)(i - c * (R + 1));
+      hist_out[i] = hst[site * M1 + posof(c)];
+    }
+  for (int64_t c = tid; c < P.C; c += THREADS) {
+    const int p = posof(c);
+    if (ok_out) ok_out[c] = okp[p];
+    if (acc_out) {
+      acc_out[c] = accp[p];
+      sav_out[c] = savp[p];
+    }
+  }
+}
+
 template <int R, int NT, int CP>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_diag3(const __grid_constant__ Params P) {
   using C = Cfg<NT, CP>;
@@ -275,108 +391,184 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_diag3(const __grid_constant__
   }
   __syncthreads();
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 1] = diag2::gtimer();
-  const int M1 = m + 1;
-  long long* hst = reinterpret_cast<long long*>(sm + OFF_C);  // [R+1][M1] (F_j first)
-  long long* okp = hst + (R + 1) * M1;
-  double* prs = reinterpret_cast<double*>(okp + M1);
-  double* pes = prs + (R + 1) * M1;
-  double* accp = pes + (R + 1) * M1;
-  double* savp = accp + M1;
-  __shared__ long long s_corr_all;
-  if (tid == 0) {
-    s_corr_all = (long long)(__ldcg(gD + diag2::CORR_IDX) + s_corr);
-    gD[diag2::CORR_IDX] = 0;
-    P.done[0] = 0u;
-    P.done[1] = 0u;
-  }
-  for (int q = tid; q < (R + 1) * m; q += THREADS) {  // global + own, zero for the next launch
-    const int j = q / m, p = q - j * m;
-    const long long g = __ldcg(gD + j * diag2::W + p);
-    gD[j * diag2::W + p] = 0;
-    hst[j * M1 + p] = g + (j < R ? (long long)cF[j * MAX_M + p] : (long long)s_osum[p]);
-  }
-  __syncthreads();
-  for (int row = warp; row <= R; row += WARPS) {  // inclusive prefix over p < m: F_j(p), O(p)
-    long long* a = hst + row * M1;
-    long long carry = 0;
-    for (int p0 = 0; p0 < m; p0 += 32) {
-      const int p = p0 + lane;
-      long long x = p < m ? a[p] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(FULL, x, o);
-        if (lane >= o) x += y;
-      }
-      x += carry;
-      if (p < m) a[p] = x;
-      carry = __shfl_sync(FULL, x, 31);
-    }
-  }
-  __syncthreads();
-  const long long corrR = s_corr_all;
-  for (int p = tid; p < M1; p += THREADS) {  // F -> histograms, O -> correct counts
-    if (p == m) {  // NaN threshold row: nothing exits
-      for (int j = 0; j < R; ++j) hst[j * M1 + p] = 0;
-      hst[R * M1 + p] = n;
-      okp[p] = corrR;
-      continue;
-    }
-    okp[p] = corrR + hst[R * M1 + p];
-    long long fprev = 0;
-    for (int j = 0; j < R; ++j) {
-      const long long f = hst[j * M1 + p];
-      hst[j * M1 + p] = f - fprev;
-      fprev = f;
-    }
-    hst[R * M1 + p] = n - fprev;
-  }
-  __syncthreads();
-  for (int i = tid; i < (R + 1) * M1; i += THREADS) {  // error-free products
-    const int site = i / M1;
-    const double x = (double)hst[i];
-    const double pr = __dmul_rn(x, P.serve[site]);
-    prs[i] = pr;
-    pes[i] = __fma_rn(x, P.serve[site], -pr);
-  }
-  __syncthreads();
-  for (int p = tid; p < M1; p += THREADS) {  // the ordered TwoSum chain of k_finalize
-    double hi = 0.0, lo = 0.0;
-#pragma unroll
-    for (int site = 0; site <= R; ++site) {
-      double s2, e;
-      two_sum(hi, prs[site * M1 + p], s2, e);
-      hi = s2;
-      lo = __dadd_rn(lo, __dadd_rn(e, pes[site * M1 + p]));
-    }
-    double tot2, e;
-    two_sum(hi, lo, tot2, e);
-    const double dn = (double)n;
-    accp[p] = __ddiv_rn((double)okp[p], dn);
-    savp[p] = __dsub_rn(P.vanilla, __ddiv_rn(tot2, dn));
-  }
-  __syncthreads();
-  auto posof = [&](int64_t c) -> int {
-    const int q = P.C <= diag2::MAX_POS ? P.pos[c] : P.pos_dev[c];
-    return q == 255 ? m : q;
-  };
-  if (P.hist)
-    for (int64_t i = tid; i < P.C * (R + 1); i += THREADS) {
-      const int64_t c = i / (R + 1);
-      const int site = (int)(i - c * (R + 1));
-      P.hist[i] = hst[site * M1 + posof(c)];
-    }
-  for (int64_t c = tid; c < P.C; c += THREADS) {
-    const int p = posof(c);
-    if (P.ok) P.ok[c] = okp[p];
-    if (P.acc) {
-      P.acc[c] = accp[p];
-      P.sav[c] = savp[p];
-    }
-  }
+  finalize_window<R, THREADS>(P, sm + OFF_C, gD, cF, s_osum, s_corr, /*zero_acc=*/true, n, P.hist,
+                              P.ok, P.acc, P.sav);
   if (P.trace) {
     __syncthreads();
     if (tid == 0) P.trace[blockIdx.x * 6 + 4] = diag2::gtimer();
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_diag3_windows: the same sweep over nwin windows (same n, r and candidate
+// rows) in one persistent launch. Tables are built once; per window a CTA
+// zeroes its cells, streams its share, folds and REDs its sums into that
+// window's accumulator, and moves on (the next window's first chunk is already
+// in flight during the fold). No cross-CTA wait: k_diag3_windows_fin then
+// finalises every window from its totals (one CTA per window).
+// ---------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(1024, 1) k_diag3_windows(
+    const __grid_constant__ Params P, const double* const* __restrict__ s_list,
+    const uint32_t* const* __restrict__ b_list, int nwin, long long* __restrict__ accw) {
+  using C = Big;
+  constexpr int THREADS = C::THREADS, WARPS = C::WARPS, ROWC = C::ROWC, CP = 32;
+  constexpr int NW = (R + 3) / 4;
+  constexpr int OFF_C = C::template off_c<R>();
+  using diag2::lds_f64;
+  using diag2::lds_u32;
+  using diag2::Unroll;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int m = P.m;
+  uint32_t* stab = reinterpret_cast<uint32_t*>(sm + C::OFF_TAB);
+  double* su = reinterpret_cast<double*>(sm + C::OFF_SU);
+  unsigned char* skey = sm + C::OFF_KEY;
+  uint32_t* cells = reinterpret_cast<uint32_t*>(sm + OFF_C);
+  __shared__ unsigned long long s_corr;
+  __shared__ int s_osum[MAX_M];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  const int64_t n = P.n;
+  const int64_t nchunks = (n + 31) >> 5;
+  const int64_t c_end = (int64_t)(blockIdx.x + 1) * nchunks / gridDim.x;
+  const int64_t c_begin = (int64_t)blockIdx.x * nchunks / gridDim.x + warp;
+  double2 v[R / 2];
+  uint32_t cb = 0;
+  auto load = [&](const double* S, const uint32_t* BITS, int64_t c) {
+    if (c >= c_end) return;
+    const int64_t s0 = c << 5;
+    const double2* src = reinterpret_cast<const double2*>(S + s0 * R);
+    const int64_t npairs = (n - s0) * (R / 2);
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      const int t = k * 32 + lane;
+      v[k] = t < npairs ? __ldcs(src + t) : make_double2(INF, INF);
+    }
+    cb = s0 + lane < n ? __ldcs(BITS + s0 + lane) : 0u;
+  };
+  load(s_list[0], b_list[0], c_begin);
+  {  // tables once
+    uint4* t4 = reinterpret_cast<uint4*>(stab);
+    for (int q = tid; q < diag2::NB * CP / 4; q += THREADS) {
+      const uint32_t e = P.tab[q / (CP / 4)];
+      t4[q] = make_uint4(e, e, e, e);
+    }
+    for (int q = tid; q < (diag2::MAX_M + 1) * diag2::SU_REP / 2; q += THREADS) {
+      const int tu = q / (diag2::SU_REP / 2);
+      const double x = tu < m ? P.u[tu] : __longlong_as_double(0x7ff8000000000000LL);
+      reinterpret_cast<double2*>(su)[q] = make_double2(x, x);
+    }
+  }
+  const double pa = P.a, pc0 = P.c0;
+  const uint32_t smb = (uint32_t)__cvta_generic_to_shared(sm);
+  const uint32_t tb = smb + C::OFF_TAB + (uint32_t)lane * 4;
+  const uint32_t sub = smb + C::OFF_SU + (uint32_t)(lane % diag2::SU_REP) * 8;
+  const uint32_t cB = smb + OFF_C + (uint32_t)lane * 4;
+  auto keyof = [&](double x) -> uint32_t {
+    uint32_t e = lds_u32(tb + diag2::bin_of(x, pa, pc0) * (CP * 4u));
+    const double t = lds_f64(sub + (e >> 16));
+    asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+        : "+r"(e)
+        : "d"(t), "d"(x));
+    return e;
+  };
+  unsigned char* kb = skey + warp * 32 * R;
+  for (int w = 0; w < nwin; ++w) {
+    const double* S = s_list[w];
+    const uint32_t* BITS = b_list[w];
+    {  // this window's cells
+      uint4* c4 = reinterpret_cast<uint4*>(cells);
+      const int per_ramp = (m + 1) * CP / 4;
+      for (int q = tid; q < R * per_ramp; q += THREADS) {
+        const int j = q / per_ramp;
+        c4[j * CELLS * CP / 4 + (q - j * per_ramp)] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      if (tid < MAX_M) s_osum[tid] = 0;
+      if (tid == 0) s_corr = 0;
+    }
+    __syncthreads();
+    unsigned corr = 0;
+    for (int64_t ch = c_begin; ch < c_end; ch += WARPS) {
+      __syncwarp();
+      const int64_t nx = ch + WARPS;
+      const int64_t s1 = nx << 5;
+      const double2* src = reinterpret_cast<const double2*>(S + s1 * R);
+      const int64_t npairs = nx < c_end ? (n - s1) * (R / 2) : 0;
+#pragma unroll
+      for (int k = 0; k < R / 2; ++k) {
+        const uint32_t k0 = keyof(v[k].x), k1 = keyof(v[k].y);
+        *reinterpret_cast<unsigned short*>(kb + 2 * (k * 32 + lane)) =
+            (unsigned short)__byte_perm(k0, k1, 0x0040);
+        const int t = k * 32 + lane;
+        if (npairs >= 32 * (R / 2))
+          v[k] = __ldcs(src + t);
+        else if (npairs > 0)
+          v[k] = t < npairs ? __ldcs(src + t) : make_double2(INF, INF);
+      }
+      const uint32_t cbc = cb;
+      if (nx < c_end) cb = s1 + lane < n ? __ldcs(BITS + s1 + lane) : 0u;
+      __syncwarp();
+      uint32_t kw[NW];
+#pragma unroll
+      for (int q = 0; q < NW; ++q) kw[q] = 0;
+#pragma unroll
+      for (int hq = 0; hq < R / 2; ++hq)
+        kw[hq >> 1] |= (uint32_t)reinterpret_cast<const unsigned short*>(kb + lane * R)[hq]
+                       << (16 * (hq & 1));
+      uint32_t prev = (uint32_t)m;
+      Unroll<R>::run([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        const uint32_t kj = __byte_perm(kw[j >> 2], 0, 0x4440 | (j & 3));
+        prev = kj < prev ? kj : prev;
+        const uint32_t val = 1u + ((cbc << (16 - j)) & 0x10000u) - ((cbc << (15 - j)) & 0x10000u);
+        diag2::red_shared<j * ROWC>(cB + prev * (CP * 4u), (int)val);
+      });
+      corr += (cbc >> R) & 1u;
+    }
+    if (w + 1 < nwin) load(s_list[w + 1], b_list[w + 1], c_begin);  // in flight during the fold
+#pragma unroll
+    for (int o = 16; o; o >>= 1) corr += __shfl_xor_sync(FULL, corr, o);
+    __syncthreads();
+    if (lane == 0 && corr) atomicAdd(&s_corr, (unsigned long long)corr);
+    int* cF = reinterpret_cast<int*>(skey);
+    for (int q = tid; q < R * m; q += THREADS) {
+      const int j = q / m, p = q - j * m;
+      const uint32_t* cell = cells + (j * CELLS + p) * CP;
+      int lo = 0, hi = 0;
+#pragma unroll 8
+      for (int k = 0; k < CP; ++k) {
+        const uint32_t x = cell[(k + lane) % CP];
+        lo += (int)(x & 0xffffu);
+        hi += (int)(short)(x >> 16);
+      }
+      cF[j * MAX_M + p] = lo;
+      if (hi) atomicAdd(&s_osum[p], hi);
+    }
+    __syncthreads();
+    long long* gD = accw + (int64_t)w * diag2::ACC_WORDS;
+    for (int q = tid; q < (R + 1) * m; q += THREADS) {
+      const int j = q / m, p = q - j * m;
+      const long long x = j < R ? (long long)cF[j * MAX_M + p] : (long long)s_osum[p];
+      if (x) atomicAdd(reinterpret_cast<unsigned long long*>(gD + j * diag2::W + p), (unsigned long long)x);
+    }
+    if (tid == 0 && s_corr)
+      atomicAdd(reinterpret_cast<unsigned long long*>(gD + diag2::CORR_IDX), s_corr);
+    __syncthreads();  // cF (key buffer) and the cells are reused by the next window
+  }
+}
+
+// one CTA per window: finalise from the totals k_diag3_windows left in accw
+template <int R>
+__global__ void __launch_bounds__(1024, 1) k_diag3_windows_fin(const __grid_constant__ Params P,
+                                                              long long* __restrict__ accw,
+                                                              double* __restrict__ acc_out,
+                                                              double* __restrict__ sav_out) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int w = blockIdx.x;
+  finalize_window<R, 1024>(P, sm, accw + (int64_t)w * diag2::ACC_WORDS, nullptr, nullptr, 0ull,
+                           /*zero_acc=*/false, P.n, nullptr, nullptr, acc_out + w * P.C,
+                           sav_out + w * P.C);
+}
 }  // namespace diag3

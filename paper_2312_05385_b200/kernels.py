@@ -228,3 +228,32 @@ def classify_candidates(thresholds):
     if kind.value == 2:
         return "axis", m.value, base[:r].copy()
     return "generic", 0, None
+
+
+def eval_thresholds_windows(evaluators, thresholds, order=None):
+    """acc, sav [len(order), C] (CUDA f64) for diagonal candidate rows over many
+    resident windows at once (ee_eval_thresholds_windows: one persistent sweep
+    launch + one finalisation). `evaluators` are WindowEvaluators with the same
+    n, r, serve table and vanilla latency; `order` lists which evaluator each
+    output row sweeps (default: each once)."""
+    torch = nat.torch_cuda()
+    th = np.ascontiguousarray(thresholds, dtype=np.float64)
+    evs = list(evaluators)
+    if not evs:
+        raise ParameterError("no windows")
+    e0 = evs[0]
+    for e in evs[1:]:
+        if e.n != e0.n or e.r != e0.r or not np.array_equal(e.serve, e0.serve) or e.vanilla_ms != e0.vanilla_ms:
+            raise ParameterError("windows must share n, r, serve table and vanilla latency")
+    order = list(range(len(evs))) if order is None else [int(i) for i in order]
+    sl = torch.tensor([nat.ptr(evs[i].d_scores) for i in order], dtype=torch.int64, device="cuda")
+    bl = torch.tensor([evs[i].d_bits.data_ptr() for i in order], dtype=torch.int64, device="cuda")
+    c = th.shape[0]
+    acc = torch.empty((len(order), c), dtype=torch.float64, device="cuda")
+    sav = torch.empty((len(order), c), dtype=torch.float64, device="cuda")
+    nat.check(nat.load_library().ee_eval_thresholds_windows(
+        nat.workspace(), sl.data_ptr(), bl.data_ptr(), len(order), e0.n, e0.r, e0.serve.ctypes.data,
+        float(e0.vanilla_ms), th.ctypes.data, c, acc.data_ptr(), sav.data_ptr(),
+        nat.stream_handle(torch)))
+    acc._eeb200_keep = (sl, bl)  # pointer lists live until the stream has used them
+    return acc, sav

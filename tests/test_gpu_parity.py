@@ -357,6 +357,35 @@ def test_axis_family_path_matches_generic_and_oracle(cuda, r, n, nan_base):
     assert np.array_equal(hist2, hist_a) and np.array_equal(ok2, ok_a)
 
 
+def test_windows_batch_matches_per_window_sweeps(cuda):
+    """ee_eval_thresholds_windows (one persistent sweep over several resident
+    windows + one finalisation) returns, per window, the bits a per-window
+    sweep returns; windows repeated in the order are independent results."""
+    import torch
+
+    from paper_2312_05385_b200 import kernels as K
+
+    r, n = 12, 40001
+    prof = make_chain(r + 1)
+    sites = find_feasible_sites(prof)[:r]
+    evs = []
+    for w in range(3):
+        rng = np.random.default_rng(6100 + w)
+        scores, cext, *_ = random_window(rng, n, r, 1, nan_frac=0.01)
+        cext[:, r] = (rng.random(n) < 0.8).astype(np.float64)
+        evs.append(WindowEvaluator.from_arrays(WindowArrays(scores, cext.astype(np.uint8)), sites, prof,
+                                               mode="hist"))
+    vals = np.concatenate([np.arange(60) / 59.0, [np.nan, -np.inf]])
+    th = np.repeat(vals[:, None], r, axis=1)
+    order = [0, 1, 2, 1, 0]
+    acc, sav = K.eval_thresholds_windows(evs, th, order)
+    torch.cuda.synchronize()
+    for row, wi in enumerate(order):
+        a1, s1 = evs[wi].evaluate_many(th)
+        assert np.array_equal(acc[row].cpu().numpy(), a1)
+        assert np.array_equal(sav[row].cpu().numpy(), s1)
+
+
 @pytest.mark.parametrize("r,n", [(5, 3001), (12, 1), (12, 31), (4, 64)])
 def test_axis_family_edges_and_fallback(cuda, r, n):
     """Single-coordinate rows outside k_axis's envelope (odd R) take the generic
