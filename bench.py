@@ -297,7 +297,7 @@ def run_ours(args):
     except Exception:  # noqa: BLE001 - fall back to eager stream launches
         graph = None
         torch.cuda.synchronize()
-    launches_per_step = 1 if world == 1 else 2  # k_diag2 (+ k_finalize after the all-reduce)
+    launches_per_step = 1 if world == 1 else 2  # the sweep (+ k_finalize after the all-reduce)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
@@ -324,7 +324,7 @@ def run_ours(args):
     del graph
 
     # single-sweep latency: L2 flushed before each sweep, CUDA events around each
-    # one (the launch itself is bracketed by k_diag2's own profiling events)
+    # one (the launch itself is bracketed by the kernel's own profiling events)
     lat_steps = max(20, min(args.steps, 200))
     nat.profile_read()
     nat.profile_enable(True)
@@ -436,7 +436,7 @@ def run_ours(args):
 
 
 def phase_timeline(sweep, th, flush, *, n_local, r, c):
-    """k_diag2's own %globaltimer stamps (ee_diag_trace) for one launch: prologue,
+    """The diagonal sweep kernel's own %globaltimer stamps (ee_diag_trace) for one launch: prologue,
     the streaming sweep loop (bytes / loop time = in-kernel GB/s), the cross-CTA
     merge and finalise tail. Launch/teardown overhead is what the CUDA events add
     on top (an empty 148 x 1024-thread kernel measures ~8-10 us between events on
