@@ -153,3 +153,20 @@ def test_candidate_family_classification_on_the_host():
     two[1, 0] = two[1, 1] = 0.9  # two columns changed in one row
     assert kernels.classify_candidates(two)[0] == "generic"
     assert kernels.classify_candidates(np.empty((0, r)))[0] == "generic"
+
+
+def test_windows_batch_rejects_non_diagonal_rows_before_device_work():
+    """ee_eval_thresholds_windows validates its envelope on the host first: a
+    non-diagonal candidate matrix (or odd R, or C > 512) is a ParameterError with
+    no device call (the fake device pointers below are never dereferenced)."""
+    lib = _native.load_library()
+    ws = ctypes.c_void_p(1)  # never used before validation fails
+    serve = np.zeros(13)
+    fake = ctypes.c_void_p(16)
+    rnd = np.random.default_rng(0).random((8, 12))
+    for th, r in ((rnd, 12), (np.zeros((8, 5)), 5), (np.zeros((600, 12)), 12)):
+        th = np.ascontiguousarray(th)
+        rc = lib.ee_eval_thresholds_windows(ws, fake, fake, 2, 1000, r, serve.ctypes.data, 10.0,
+                                            th.ctypes.data, th.shape[0], fake, fake, None)
+        with pytest.raises(ParameterError):
+            _native.check(rc)
