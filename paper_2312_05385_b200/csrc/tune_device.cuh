@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // _exitcore.pyx:43-53), a chain of n dependent adds with the next 8 addends
   // always loaded ahead of it.
   const int n8 = (n + 7) & ~7;
-  __shared__ unsigned long long okc[MAXR + 1];
+  __shared__ unsigned okc[MAXR + 1];  // n <= EE_TUNE_N_MAX: 32-bit counts, native shared atomics
   auto evaluate = [&](int nc) {
     if (tid <= MAXR) okc[tid] = 0;
     __syncthreads();
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         hit = (wbits[i] >> site) & 1u;
       }
       const unsigned b = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0 && b) atomicAdd(&okc[c], (unsigned long long)__popc(b));
+      if (lane == 0 && b) atomicAdd(&okc[c], (unsigned)__popc(b));
     }
     __syncthreads();
     if (tid < nc) {
