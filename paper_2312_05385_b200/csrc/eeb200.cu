@@ -2032,7 +2032,7 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
   for (int j = 0; j <= r; ++j) p.serve[j] = h_serve[j];
   const size_t n8 = (size_t)((n + 7) & ~7);
   const size_t rows_b = n8 * 4 + (size_t)(r + 1) * n8 * 8;
-  const size_t win_b = (size_t)n * r * 8;
+  const size_t win_b = n8 * r * 8;  // transposed [r][n8] in shared memory
   const int rows_in = rows_b <= 120 * 1024;
   const int in_smem = rows_in && rows_b + win_b <= 200 * 1024;
   const size_t smem = rows_in ? rows_b + (in_smem ? win_b : 0) : 0;

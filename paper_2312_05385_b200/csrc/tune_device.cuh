@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(16) unsigned char sdyn[];
   const int n8s = (n + 7) & ~7;
   const double* win = s;
+  int64_t wsi = r, wsj = 1;  // score (i, j) at win[i * wsi + j * wsj]
   const uint32_t* wbits = bits;
   if (rows_in_smem) {
     vals = reinterpret_cast<double*>(sdyn);
@@ -41,8 +42,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     wbits = sb;
     if (window_in_smem) {
       double* sw = reinterpret_cast<double*>(sdyn + (size_t)(r + 1) * n8s * 8 + (size_t)n8s * 4);
-      for (int64_t k = threadIdx.x; k < (int64_t)n * r; k += THREADS) sw[k] = s[k];
+      // transposed [r][n8]: a warp's lanes (consecutive samples) read consecutive words
+      for (int64_t k = threadIdx.x; k < (int64_t)n * r; k += THREADS) {
+        const int64_t i = k / r, j = k - i * r;
+        sw[j * n8s + i] = s[k];
+      }
       win = sw;
+      wsi = 1;
+      wsj = n8s;
     }
   }
   __shared__ double th[MAXR], steps[MAXR], cand[MAXR + 1][MAXR], accs[MAXR + 1], savs[MAXR + 1];
@@ -79,10 +86,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int c = t / n32, i = t - c * n32;
       unsigned hit = 0;
       if (c < nc && i < n) {
-        const double* row = win + (int64_t)i * r;
+        const double* row = win + (int64_t)i * wsi;
         int site = r;
         for (int j = r - 1; j >= 0; --j)  // branch-free: every score is read, earliest hit wins
-          if (row[j] < cand[c][j]) site = j;
+          if (row[j * wsj] < cand[c][j]) site = j;
         vals[(int64_t)c * n8 + i] = sserve[site];
         hit = (wbits[i] >> site) & 1u;
       }
