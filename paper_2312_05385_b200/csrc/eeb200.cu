@@ -2036,15 +2036,16 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
   const int rows_in = rows_b <= 120 * 1024;
   const int in_smem = rows_in && rows_b + win_b <= 200 * 1024;
   const size_t smem = rows_in ? rows_b + (in_smem ? win_b : 0) : 0;
-  static size_t smem_set = 48 * 1024;  // the attribute is raised once, to the largest need
-  if (smem > smem_set) {
-    EE_CUDA(cudaFuncSetAttribute(tunedev::k_tune, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    smem_set = smem;
+  auto kern = r <= 8 ? tunedev::k_tune<8> : r <= 16 ? tunedev::k_tune<16> : tunedev::k_tune<32>;
+  static size_t smem_set[3] = {48 * 1024, 48 * 1024, 48 * 1024};  // raised once per variant
+  const int kv = r <= 8 ? 0 : r <= 16 ? 1 : 2;
+  if (smem > smem_set[kv]) {
+    EE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set[kv] = smem;
   }
   {
     ProfScope ps(ws, st, "k_tune");
-    tunedev::k_tune<<<1, tunedev::THREADS, smem, st>>>(d_scores, d_bits, (int)n, r, vanilla, p,
+    kern<<<1, tunedev::THREADS, smem, st>>>(d_scores, d_bits, (int)n, r, vanilla, p,
                                                         d_vals, d_out, d_info, d_trace, in_smem,
                                                         rows_in);
   }

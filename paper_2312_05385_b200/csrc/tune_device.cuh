@@ -23,6 +23,7 @@ struct Params {
 // out_d: [0, r) thresholds, r: savings, r+1: accuracy
 // out_i: 0 rounds, 1 evals, 2 trace rows written, 3 status (0 ok, 1 budget violated,
 //        2 did not terminate)
+template <int RB>  // register slots for one sample's scores (RB >= r)
 __global__ void __launch_bounds__(THREADS, 1)
     k_tune(const double* __restrict__ s, const uint32_t* __restrict__ bits, int n, int r,
            double vanilla, const __grid_constant__ Params p,
@@ -79,6 +80,31 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int lane = tid & 31;
     // (candidate, sample) pairs flattened over all threads: a warp's 32 pairs
     // share one candidate (samples padded to 32), so small windows use every warp
+    if (n >= THREADS) {
+      // large windows: a thread per sample; its scores are read once into registers
+      // (RB >= r, the extra slots predicated off) and scanned for every candidate
+      for (int i0 = 0; i0 < n; i0 += THREADS) {  // warp-uniform trip count for the ballots
+        const int i = i0 + tid;
+        const bool valid = i < n;
+        double x[RB];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) x[j] = (valid && j < r) ? win[(int64_t)i * wsi + j * wsj] : 0.0;
+        const uint32_t wb = valid ? wbits[i] : 0u;
+        for (int c = 0; c < nc; ++c) {
+          int site = r;
+#pragma unroll
+          for (int j = RB - 1; j >= 0; --j)
+            if (j < r && x[j] < cand[c][j]) site = j;
+          unsigned hit = 0;
+          if (valid) {
+            vals[(int64_t)c * n8 + i] = sserve[site];
+            hit = (wb >> site) & 1u;
+          }
+          const unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (lane == 0 && b) atomicAdd(&okc[c], (unsigned)__popc(b));
+        }
+      }
+    } else {
     const int n32 = (n + 31) & ~31;
     const int total = nc * n32;
     for (int t0 = 0; t0 < total; t0 += THREADS) {  // warp-uniform trip count for the ballot
@@ -95,6 +121,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       const unsigned b = __ballot_sync(0xffffffffu, hit);
       if (lane == 0 && b) atomicAdd(&okc[c], (unsigned)__popc(b));
+    }
     }
     __syncthreads();
     if (tid < nc) {
