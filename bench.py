@@ -86,6 +86,21 @@ def window(n: int):
 
 # ---------------------------------------------------------------- CPU reference
 _G = {}
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")
+REF_CACHE = os.environ.get("EEB200_REF_CACHE", "/tmp/eeb200_ref_window")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def _ref_worker(args):
@@ -98,12 +113,62 @@ def _ref_worker(args):
 
 
 def reference_kernel():
+    """The reference's CPU kernel: the installed reference package's own
+    `eesim._kernels` (baseline/_ref, BACKEND "compiled"), else its
+    _exitcore.pyx compiled by oracle/Makefile (oracle/_ref), else the C port."""
+    if os.path.isdir(os.path.join(REF_PKG, "eesim")):
+        if REF_PKG not in sys.path:
+            sys.path.insert(0, REF_PKG)
+        import eesim._kernels as ek
+
+        if ek.BACKEND == "compiled":
+            return ek, "reference"
     from oracle import oracle as O
 
     ref = O.reference_kernel()
     if ref is not None:
         return ref, "reference"
     return O, "port"
+
+
+def reference_window(n: int):
+    """Config-4 window built ONLY by the reference package (baseline/_ref):
+    eesim.trace.synthesize_workload (trace.py:164-227) packed by
+    eesim.engine.WindowEvaluator (engine.py:135-163), serve table from
+    eesim.engine._serve_table (engine.py:124-132). No repo code or library is
+    touched. The packed arrays are cached under EEB200_REF_CACHE (default
+    /tmp/eeb200_ref_window; generation takes ~1 min per 1M records)."""
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    from eesim.engine import WindowEvaluator, _serve_table
+    from eesim.graph import ModelProfile, find_feasible_sites
+    from eesim.trace import synthesize_workload
+
+    nodes = [f"n{i}" for i in range(13)]  # make_chain(13, layer_ms=1.0, ramp_ms=0.01)
+    prof = ModelProfile(nodes, list(zip(nodes, nodes[1:])), {x: {1: 1.0} for x in nodes},
+                        {x: {1: 0.01} for x in nodes[:-1]}, nodes[-1], name="chain")
+    sites = find_feasible_sites(prof)
+    serve = _serve_table(sites, prof, 1)
+    vanilla = prof.model_latency(1)
+    tag = os.path.join(REF_CACHE, f"config4_n{n}_seed0")
+    try:
+        scores = np.load(tag + "_scores.npy")
+        cext = np.load(tag + "_correct.npy").astype(np.float64)
+        if scores.shape == (n, len(sites)) and cext.shape == (n, len(sites) + 1):
+            return scores, cext, serve, vanilla, len(sites), "cache (reference generator)"
+    except (OSError, ValueError):
+        pass
+    curve = {x.position: 0.5 + (0.95 - 0.5) * i / 11 for i, x in enumerate(sites)}
+    w = synthesize_workload(prof, n, 0.9, curve, seed=0, miscalibration=0.05, n_labels=10)
+    ev = WindowEvaluator(w.records, sites, prof, batch=1)
+    scores, cext = ev.scores, ev.correct_ext
+    try:
+        os.makedirs(REF_CACHE, exist_ok=True)
+        np.save(tag + "_scores.npy", scores)
+        np.save(tag + "_correct.npy", cext.astype(np.uint8))
+    except OSError:
+        pass
+    return scores, cext, serve, vanilla, len(sites), "generated (reference generator)"
 
 
 def cpu_sweep(kernel, scores, cext, serve, vanilla, th, procs, n_sample):
@@ -124,18 +189,14 @@ def cpu_sweep(kernel, scores, cext, serve, vanilla, th, procs, n_sample):
 
 
 def run_reference(args):
+    """The reference arm: the reference package's own window, packing, serve
+    table and compiled kernel on all host cores. Imports nothing from the
+    product package (no libeeb200.so in this process)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2312_05385_b200.engine import serve_table
-
-    prof, sites, arrays = window(args.n)
-    r = len(sites)
+    scores, cext, serve, vanilla, r, source = reference_window(args.n)
     th = candidates(args.family, args.c, r)
-    serve = serve_table(sites, prof, 1)
-    vanilla = prof.model_latency(1)
-    scores = np.ascontiguousarray(arrays.errs)
-    cext = arrays.correct_ext()
     kernel, kind = reference_kernel()
     procs = os.cpu_count() or 1
     # bound each step so warmup + steps stay within ~2 minutes of CPU time
@@ -149,17 +210,22 @@ def run_reference(args):
              for _ in range(args.steps)]
     t_step = float(np.mean(times)) * args.n / n_sample  # full-window equivalent
     value = th.shape[0] / t_step
+    where = (f"baseline/_ref eesim._kernels (BACKEND={kernel.BACKEND})"
+             if hasattr(kernel, "BACKEND") else
+             "oracle/_ref: _exitcore.pyx compiled from /root/reference" if kind == "reference"
+             else "oracle C port")
     sample = (f"{n_sample} of {args.n} samples x {th.shape[0]} candidates per step, scaled to "
               f"the full window; {procs} forked processes each running the reference kernel "
-              f"({'oracle/_ref: _exitcore.pyx compiled from /root/reference' if kind == 'reference' else 'oracle C port'})")
+              f"({where}); window {source}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator eesim.trace.synthesize_workload, seed 0)",
         "config": config_block(args, r, th.shape[0]),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": kind,
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -548,7 +614,7 @@ def cpu_baseline(args, arrays, prof, sites, th, acc_gpu, sav_gpu):
     kernel.eval_thresholds(scores[:ns], cext[:ns], serve, vanilla, th)
     one = (time.perf_counter() - t0) * args.n / ns
     return {"value": th.shape[0] / dt, "unit": UNIT, "cores": procs, "kind": kind,
-            "single_core_value": th.shape[0] / one,
+            "cpu_model": cpu_model(), "single_core_value": th.shape[0] / one,
             "single_core_sample": f"{ns} of {args.n} samples, 1 process, scaled to the full window",
             "sample": f"full workload ({args.n} samples x {th.shape[0]} candidates), one pass, "
                       f"{procs} forked processes over sample shards",

@@ -2,6 +2,7 @@
 
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -9,7 +10,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "eeb200.cu"), os.path.join(HERE, "csrc", "synth.cpp")]
-HEADERS = [os.path.join(ROOT, "include", "eeb200.h")]
+HEADERS = [os.path.join(ROOT, "include", "eeb200.h")] + sorted(
+    glob.glob(os.path.join(HERE, "csrc", "*.cuh")))
 LIB = os.path.join(HERE, "libeeb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

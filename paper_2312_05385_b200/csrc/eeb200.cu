@@ -66,6 +66,34 @@ int sm_count() {
   return g_sms;
 }
 
+// cudaFuncSetAttribute is per (function, device): raised dynamic shared-memory
+// limits are remembered per (function, device) under one process-wide lock, so
+// a second GPU driven from the same process, or two threads racing on a first
+// call, still set the attribute before launching.
+static cudaError_t ensure_smem_fn(const void* fn, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& d : done)
+    if (d.first.first == fn && d.first.second == dev) {
+      if (d.second >= smem) return cudaSuccess;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) d.second = smem;
+      return e;
+    }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done.push_back({{fn, dev}, smem});
+  return e;
+}
+template <class K>
+static cudaError_t ensure_smem(K* fn, size_t smem) {
+  return ensure_smem_fn(reinterpret_cast<const void*>(fn), smem);
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -471,7 +499,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 #include "sweep_axis.cuh"
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
-#include "gemm_tc.cuh"
+#include "pool.cuh"
 #include "gemm_tc2.cuh"
 namespace {
 
@@ -1051,13 +1079,12 @@ static unsigned diag_grid(const ee_workspace* ws, int64_t n, int per_sm = 1, int
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, ceil_div(nchunks, warps)));
 }
 template <class K>
-static cudaError_t launch_diag_kernel(K k, const char* name, int smem, bool& attr_set,
+static cudaError_t launch_diag_kernel(K k, const char* name, int smem,
                                       const diag2::Params& p, int64_t n, cudaStream_t st,
                                       ee_workspace* ws, int threads = diag2::THREADS) {
-  if (!attr_set) {  // once per instantiation (a driver call)
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem(k, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const unsigned grid = diag_grid(ws, n, 1024 / threads, threads / 32);
   ProfScope ps(ws, st, name);  // events bracket the launch itself
@@ -1080,21 +1107,19 @@ static cudaError_t launch_diag_kernel(K k, const char* name, int smem, bool& att
 template <int R>
 static cudaError_t launch_diag2(const diag2::Params& p, int64_t n, int upd, cudaStream_t st,
                                 ee_workspace* ws) {
-  static bool attr_set[2] = {false, false};
   return upd == 1 ? launch_diag_kernel(diag2::k_diag2<R, 1>, "k_diag2", diag2::smem_bytes<R>(),
-                                       attr_set[1], p, n, st, ws)
+                                       p, n, st, ws)
                   : launch_diag_kernel(diag2::k_diag2<R, 0>, "k_diag2", diag2::smem_bytes<R>(),
-                                       attr_set[0], p, n, st, ws);
+                                       p, n, st, ws);
 }
 template <int R>
 static cudaError_t launch_diag3(const diag2::Params& p, int64_t n, bool pair, cudaStream_t st,
                                 ee_workspace* ws) {
-  static bool attr_set[2] = {false, false};
   if (pair)
     return launch_diag_kernel(diag3::k_diag3<R, 512, 16>, "k_diag3",
-                              diag3::Pair::smem_bytes<R>(), attr_set[1], p, n, st, ws, 512);
+                              diag3::Pair::smem_bytes<R>(), p, n, st, ws, 512);
   return launch_diag_kernel(diag3::k_diag3<R, 1024, 32>, "k_diag3", diag3::Big::smem_bytes<R>(),
-                            attr_set[0], p, n, st, ws, 1024);
+                            p, n, st, ws, 1024);
 }
 extern "C" {
 
@@ -1287,13 +1312,11 @@ static bool axis_rows(const double* th, int64_t C, int r, std::vector<double>& b
 template <int R>
 static cudaError_t launch_axis(const axis::Params& p, unsigned grid, bool nanchk, cudaStream_t st,
                                ee_workspace* ws) {
-  static bool attr_set[2] = {false, false};
   constexpr int smem = axis::Layout<R>::SMEM;
   auto k = nanchk ? axis::k_axis<R, true> : axis::k_axis<R, false>;
-  if (!attr_set[nanchk]) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem(k, smem);
     if (e != cudaSuccess) return e;
-    attr_set[nanchk] = true;
   }
   ProfScope ps(ws, st, "k_axis");
   k<<<grid, axis::THREADS, smem, st>>>(p);
@@ -1399,14 +1422,11 @@ template <int R>
 static cudaError_t launch_windows(const diag2::Params& p, const double* const* sl,
                                  const uint32_t* const* bl, int nwin, long long* accw,
                                  double* acc, double* sav, cudaStream_t st, ee_workspace* ws) {
-  static bool attr_set = false;
   constexpr int smem = diag3::Big::smem_bytes<R>();
   constexpr int fsmem = diag3::Big::fin_bytes<R>();
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(diag3::k_diag3_windows<R>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem(diag3::k_diag3_windows<R>, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const unsigned grid = diag_grid(ws, p.n);
   {
@@ -1934,12 +1954,8 @@ int ee_workspace_set_diag_version(ee_workspace* ws, int32_t version) {
 
 int ee_l2_flush(void* d_buf, int64_t bytes, void* stream) {
   if (!d_buf || bytes < 16) return fail(EE_ERR_ARG, "bad flush buffer");
-  static bool attr = false;
-  if (!attr) {
-    EE_CUDA(cudaFuncSetAttribute(k_l2_flush, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared));
-    attr = true;
-  }
+  EE_CUDA(cudaFuncSetAttribute(k_l2_flush, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
   k_l2_flush<<<(unsigned)sm_count() * 2, 1024, 0, (cudaStream_t)stream>>>(
       static_cast<uint4*>(d_buf), bytes / 16);
   EE_LAUNCH_CHECK();
@@ -2037,12 +2053,7 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
   const int in_smem = rows_in && rows_b + win_b <= 200 * 1024;
   const size_t smem = rows_in ? rows_b + (in_smem ? win_b : 0) : 0;
   auto kern = r <= 8 ? tunedev::k_tune<8> : r <= 16 ? tunedev::k_tune<16> : tunedev::k_tune<32>;
-  static size_t smem_set[3] = {48 * 1024, 48 * 1024, 48 * 1024};  // raised once per variant
-  const int kv = r <= 8 ? 0 : r <= 16 ? 1 : 2;
-  if (smem > smem_set[kv]) {
-    EE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set[kv] = smem;
-  }
+  EE_CUDA(ensure_smem(kern, smem));
   {
     ProfScope ps(ws, st, "k_tune");
     kern<<<1, tunedev::THREADS, smem, st>>>(d_scores, d_bits, (int)n, r, vanilla, p,
@@ -2196,11 +2207,9 @@ static cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, co
                                 cudaStream_t st) {
   auto kern = gemm2::k_gemm2<BN, BF>;
   constexpr int smem = gemm2::smem_bytes<BN>();
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem(kern, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   kern<<<grid, gemm2::THREADS, smem, st>>>(ta, tb, bias, c, m, n, k, per, partials);
   return cudaGetLastError();
@@ -2275,10 +2284,10 @@ int ee_pool_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int32_t 
   const int64_t bc = b * c;
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(bc, 8), sm_count() * 16);
   if (x_bf16)
-    gemmtc::k_pool_bf16<uint16_t><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    pool::k_pool_bf16<uint16_t><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         static_cast<const uint16_t*>(d_x), bc, hw, static_cast<uint16_t*>(d_out));
   else
-    gemmtc::k_pool_bf16<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    pool::k_pool_bf16<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         static_cast<const float*>(d_x), bc, hw, static_cast<uint16_t*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;
@@ -2320,10 +2329,10 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
   if (reinterpret_cast<uintptr_t>(d_x) % (x_bf16 ? 8 : 16)) return fail(EE_ERR_ARG, "misaligned map");
   const dim3 grid((unsigned)ceil_div(c, 64), (unsigned)b);
   if (x_bf16)
-    gemmtc::k_pool_nhwc<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+    pool::k_pool_nhwc<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
         static_cast<const uint16_t*>(d_x), c, hw, static_cast<uint16_t*>(d_out));
   else
-    gemmtc::k_pool_nhwc<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
+    pool::k_pool_nhwc<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
         static_cast<const float*>(d_x), c, hw, static_cast<uint16_t*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;
@@ -2545,11 +2554,7 @@ int ee_decode_attention_bf16(const void* d_qkv, const void* d_kv, const int64_t*
   if (!d_qkv || !d_kv || !d_qpos || !d_out) return fail(EE_ERR_ARG, "null pointer");
   if (reinterpret_cast<uintptr_t>(d_kv) % 16) return fail(EE_ERR_ARG, "misaligned cache");
   const size_t smem = (size_t)q * t1 * 4;
-  static size_t smem_set = 48 * 1024;
-  if (smem > smem_set) {
-    EE_CUDA(cudaFuncSetAttribute(k_decode_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
-  }
+  EE_CUDA(ensure_smem(k_decode_attn, smem));
   k_decode_attn<<<(unsigned)(b * h), DA_THREADS, smem, (cudaStream_t)stream>>>(
       static_cast<const uint16_t*>(d_qkv), static_cast<const uint16_t*>(d_kv), d_qpos, b, q, h, t1,
       static_cast<uint16_t*>(d_out));

@@ -32,6 +32,11 @@ from paper_2312_05385_b200 import _native as nat
 from paper_2312_05385_b200.errors import ParameterError
 from paper_2312_05385_b200.heads import ExitController, LargeRampHead, SlotTable, exit_from_logits
 
+# North star: a sample whose confidence lies within 1e-5 of a threshold is a
+# near-tie — its exit decision may legitimately differ from an fp64 CPU oracle,
+# so it is reported rather than counted as a mismatch.
+NEAR_TIE_EPS = 1e-5
+
 
 @dataclass
 class BatchResult:
@@ -43,6 +48,31 @@ class BatchResult:
     final_label: "object"     # i32 [B] (-1 if censored in compaction mode)
     release_ms: np.ndarray | None = None  # per request, from batch start (host, if timed)
     batch_ms: float | None = None
+    thresholds: "object" = None  # the thresholds this batch was decided under (host list or CUDA f64 [R])
+
+    def near_ties(self, thresholds=None, eps: float = NEAR_TIE_EPS):
+        """bool [B] (CUDA): rows with |err_j - t_j| < eps at some active ramp j the
+        row reached (j <= its release site) — the decisions the north star
+        reports instead of requiring them to match an fp64 oracle bit for bit
+        (the strict rule is engine.py:207). NaN (censored) entries never tie."""
+        import torch
+
+        th = self.thresholds if thresholds is None else thresholds
+        if th is None:
+            raise ParameterError("near_ties needs the thresholds the batch ran under")
+        r, b = self.ramp_err.shape
+        if r == 0:
+            return torch.zeros(b, dtype=torch.bool, device=self.ramp_err.device)
+        if not hasattr(th, "data_ptr"):
+            th = torch.tensor([float(t) for t in th], dtype=torch.float64)
+        th = th.to(self.ramp_err.device, torch.float64).view(r, 1)
+        close = (self.ramp_err.double() - th).abs() < eps
+        reached = torch.arange(r, device=self.ramp_err.device).view(r, 1) <= \
+            self.released_site.view(1, b).long()
+        return (close & reached).any(dim=0)
+
+    def near_tie_count(self, thresholds=None, eps: float = NEAR_TIE_EPS) -> int:
+        return int(self.near_ties(thresholds, eps).sum().item())
 
     def records(self, site_names: Sequence[str], first_id: int = 0, arrival_ms: float = 0.0):
         """The batch as reference RequestRecords (err/label per site, final label)."""
@@ -95,6 +125,7 @@ class EEPipeline:
         dev = "cuda"
         # thresholds: host floats, or a CUDA f64 [R] tensor read by the kernels at run time
         dev_th = hasattr(thresholds, "data_ptr")
+        th_record = thresholds if dev_th else [float(t) for t in thresholds]
         if dev_th:
             thresholds = [thresholds[r : r + 1] for r in range(R)]
         alive = torch.ones(b, dtype=torch.uint8, device=dev)
@@ -150,7 +181,8 @@ class EEPipeline:
                 # every still-alive row is released with the final model's label
                 exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=R, alive=alive,
                                  slot=rows, slots=slots, compact=(mode != "feedback"))
-        out = BatchResult(slots.label, slots.site, slots.err, ramp_err, ramp_label, final_label)
+        out = BatchResult(slots.label, slots.site, slots.err, ramp_err, ramp_label, final_label,
+                          thresholds=th_record)
         if timed:
             end = torch.cuda.Event(enable_timing=True)
             end.record()
@@ -223,6 +255,19 @@ def fold_batchnorm(model):
                     fold(conv, bn)
             if blk.downsample is not None:
                 fold(blk.downsample[0], blk.downsample[1])
+    return model
+
+
+def prepare_bf16(model, channels_last: bool):
+    """The serving form of a backbone: bf16 weights and activations; CNNs
+    additionally channels_last with BatchNorm folded into the convolutions
+    (the layout cuDNN's tensor-core convolutions want). In place."""
+    import torch
+
+    if channels_last:
+        fold_batchnorm(model)
+        model.to(memory_format=torch.channels_last)
+    model.to(torch.bfloat16)
     return model
 
 
@@ -328,8 +373,14 @@ def bert_base(seq: int = 128, seed: int = 0, conf: str = "entropy"):
     final_w = (torch.randn(2, cfg.hidden_size, generator=g) / cfg.hidden_size ** 0.5).cuda()
 
     class Final(torch.nn.Module):
+        """Final classifier on the token-0 hidden state (fp32 weight [2, 768])."""
+
+        def __init__(self):
+            super().__init__()
+            self.weight = final_w
+
         def forward(self, h):
-            return h[:, 0].float() @ final_w.t()
+            return h[:, 0].float() @ self.weight.t()
 
     return EEPipeline(stages + [Final()], heads, [f"layer{s}" for s in range(len(layers))]), bert
 

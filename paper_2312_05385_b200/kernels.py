@@ -195,15 +195,53 @@ def eval_thresholds(scores, correct_ext, serve, vanilla, thresholds, *, mode: st
     return acc.cpu().numpy(), sav.cpu().numpy()
 
 
+def _reraise_as(errors_mod, fn):
+    """Wrap `fn` so this package's EESimError subclasses surface as the same-named
+    classes of the target package's `errors` module (a reference
+    caller's `except eesim.errors.ParameterError` must still catch them)."""
+    import functools
+
+    from paper_2312_05385_b200 import errors as ours
+
+    names = ("ParameterError", "GridCapError", "ValidationError", "GraphError")
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        try:
+            return fn(*args, **kw)
+        except ours.EESimError as exc:
+            for name in names:
+                if isinstance(exc, getattr(ours, name)) and hasattr(errors_mod, name):
+                    raise getattr(errors_mod, name)(*exc.args) from exc
+            raise
+
+    return wrapper
+
+
 def install_into(module) -> None:
     """Swap these kernels into a reference `eesim._kernels` module object.
 
     engine.py resolves `_kernels.eval_thresholds` / `_kernels.exit_sites` at
     call time (engine.py:168,177), so after this every WindowEvaluator — and
     therefore tune, grid_oracle, evaluate_window and ramp adjustment — runs
-    on the GPU."""
-    module.eval_thresholds = eval_thresholds
-    module.exit_sites = exit_sites
+    on the GPU. When the target package has an `errors` module (eesim.errors,
+    pkg/src/eesim/errors.py:4-21), shape errors are raised as ITS classes."""
+    import importlib
+
+    errors_mod = None
+    name = getattr(module, "__name__", "")
+    pkg = name.rsplit(".", 1)[0] if isinstance(name, str) and "." in name else ""
+    if pkg:
+        try:
+            errors_mod = importlib.import_module(pkg + ".errors")
+        except ImportError:
+            errors_mod = None
+    if errors_mod is None:
+        module.eval_thresholds = eval_thresholds
+        module.exit_sites = exit_sites
+    else:
+        module.eval_thresholds = _reraise_as(errors_mod, eval_thresholds)
+        module.exit_sites = _reraise_as(errors_mod, exit_sites)
     module.BACKEND = BACKEND
 
 
@@ -246,6 +284,15 @@ def eval_thresholds_windows(evaluators, thresholds, order=None):
         if e.n != e0.n or e.r != e0.r or not np.array_equal(e.serve, e0.serve) or e.vanilla_ms != e0.vanilla_ms:
             raise ParameterError("windows must share n, r, serve table and vanilla latency")
     order = list(range(len(evs))) if order is None else [int(i) for i in order]
+    if not order:
+        raise ParameterError("empty window order")
+    if any(i < 0 or i >= len(evs) for i in order):
+        raise ParameterError(f"window order entries must lie in [0, {len(evs)})")
+    if th.ndim != 2 or th.shape[1] != e0.r:
+        raise ParameterError(f"thresholds must be (C, {e0.r}), got {th.shape}")
+    for e in evs:
+        if nat.ptr(e.d_scores) % 16 or e.d_bits.data_ptr() % 16:
+            raise ParameterError("window buffers must be 16-byte aligned")
     sl = torch.tensor([nat.ptr(evs[i].d_scores) for i in order], dtype=torch.int64, device="cuda")
     bl = torch.tensor([evs[i].d_bits.data_ptr() for i in order], dtype=torch.int64, device="cuda")
     c = th.shape[0]

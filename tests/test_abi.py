@@ -95,6 +95,39 @@ def test_backend_surface_mirrors_reference_seam():
     assert seam.exit_sites is kernels.exit_sites
 
 
+def test_install_into_reference_raises_reference_error_classes():
+    """Installed into the reference's `eesim._kernels`, shape errors surface as
+    eesim.errors.ParameterError, so `except EESimError` in a
+    reference caller still catches them. The checks run before any device work."""
+    import importlib
+    import sys
+    import numpy as np
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "eesim")):
+        pytest.skip("reference not installed under baseline/_ref")
+    sys.path.insert(0, ref)
+    try:
+        ek = importlib.import_module("eesim._kernels")
+        ee = importlib.import_module("eesim.errors")
+        saved = (ek.eval_thresholds, ek.exit_sites, ek.BACKEND)
+        try:
+            kernels.install_into(ek)
+            assert ek.BACKEND == "cuda"
+            assert ek.eval_thresholds.__wrapped__ is kernels.eval_thresholds
+            with pytest.raises(ee.ParameterError, match="columns"):
+                ek.eval_thresholds(np.zeros((4, 3)), np.ones((4, 4)), np.zeros(4), 1.0,
+                                   np.zeros((2, 2)))
+            with pytest.raises(ee.EESimError):
+                ek.exit_sites(np.zeros((4, 3)), np.zeros(2))
+            with pytest.raises(ValueError, match="dtype"):  # buffer errors keep Cython's types
+                ek.exit_sites(np.zeros((4, 3), dtype=np.float32), np.zeros(3))
+        finally:
+            ek.eval_thresholds, ek.exit_sites, ek.BACKEND = saved
+    finally:
+        sys.path.remove(ref)
+
+
 def test_no_gpu_means_loud_failure(monkeypatch):
     import numpy as np
     import torch

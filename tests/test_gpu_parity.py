@@ -5,6 +5,8 @@ and — in exact mode — savings; histogram-mode savings within 1e-9 relative
 
 from __future__ import annotations
 
+import hashlib
+import json
 import os
 from fractions import Fraction
 
@@ -204,6 +206,39 @@ def test_tune_config1_window(cuda, golden, device_loop):
     assert (res.accuracy, res.rounds, res.evals) == (want["accuracy"], want["rounds"], want["evals"])
 
 
+@pytest.mark.parametrize("r,n", [(12, 600), (12, 3000), (12, 20000), (20, 600), (20, 3000),
+                                 (31, 600), (31, 3000), (31, 20000)])
+def test_tune_kernel_variants_match_exact_host_loop_and_oracle(cuda, r, n):
+    """Every k_tune variant (R <= 8 / 16 / 32 register buckets) and every
+    shared-memory layout branch (window in shared or global memory, addend rows
+    in shared or global memory) against the exact host loop and the Python
+    Algorithm 1 over the C oracle kernel (tuner.py:97-171): bit-identical."""
+    prof = make_chain(r + 1, layer_ms=1.0, ramp_ms=0.01)
+    sites = find_feasible_sites(prof)
+    curve = {x.position: 0.4 + 0.5 * i / max(1, r - 1) for i, x in enumerate(sites)}
+    w = synthesize_workload(prof, n, 0.8, curve, seed=1000 + r + n, miscalibration=0.1)
+    recs = list(w.records)
+    ev = WindowEvaluator(recs, sites, prof, mode="hist")  # hist: the host loop must still score exactly
+    dev = tune(recs, sites, TunerParams(), prof, evaluator=ev, device_loop=True)
+    host = tune(recs, sites, TunerParams(), prof, evaluator=ev, device_loop=False)
+    assert dev.thresholds == host.thresholds
+    assert dev.savings_ms.hex() == host.savings_ms.hex()
+    assert (dev.accuracy, dev.rounds, dev.evals) == (host.accuracy, host.rounds, host.evals)
+    th, sav, acc, rounds, evals, _ = O.tune(recs, sites, prof)
+    assert [dev.thresholds[x.position] for x in sites] == list(th)
+    assert dev.savings_ms.hex() == float(sav).hex() and dev.accuracy == acc
+    assert (dev.rounds, dev.evals) == (rounds, evals)
+
+
+def test_tune_rejects_mismatched_evaluator(cuda):
+    prof = make_chain(5)
+    sites = find_feasible_sites(prof)
+    w = synthesize_workload(prof, 64, 0.5, {x.position: 0.7 for x in sites}, seed=3)
+    ev = WindowEvaluator(list(w.records), sites[:3], prof)
+    with pytest.raises(Exception, match="evaluator window covers sites"):
+        tune(list(w.records), sites, TunerParams(), prof, evaluator=ev)
+
+
 def test_estimate_utilities_golden(cuda, golden):
     from conftest import make_record
     from paper_2312_05385_b200.engine import EEConfig
@@ -239,34 +274,65 @@ def test_medium_sweep_window_against_reference(cuda):
                 np.testing.assert_allclose(sav, gold[f"{fam}_sav"], rtol=SAV_RTOL, atol=0)
 
 
+def _config4_golden():
+    with open(os.path.join(GOLDEN, "config4_1m.json")) as fh:
+        return json.load(fh)
+
+
+def _unhex(xs):
+    return np.array([float.fromhex(x) for x in xs])
+
+
 def test_full_size_config4_histograms(cuda):
-    """1M x 12 at full size: exact histograms against the C oracle on a subset
-    of candidates, plus size-independent invariants on all of them."""
+    """1M x 12 at full size, ALL 64 diagonal candidates: exact histograms and
+    correct counts against the C oracle, acc bit-identical and sav within
+    1e-9 * vanilla of the REFERENCE's own compiled kernel on the reference's own
+    window (tests/golden/config4_1m.json), plus size-independent invariants."""
     from paper_2312_05385_b200 import synth
 
+    gold = _config4_golden()
     prof = config4_profile()
     sites = find_feasible_sites(prof)
     arrays = synth.config4_window(1_000_000)
+    assert hashlib.sha256(np.ascontiguousarray(arrays.errs).tobytes()).hexdigest() == gold["scores_sha256"]
     ev = WindowEvaluator.from_arrays(arrays, sites, prof, mode="hist")
+    assert [x.hex() for x in ev.serve] == gold["serve"]
     th = diagonal()
     hist, ok = ev.histograms(th)
     n = arrays.n
     assert (hist.sum(axis=1) == n).all()
     # raising every threshold never delays an exit: exits at ramp 0 are monotone
     assert (np.diff(hist[:, 0]) >= 0).all()
-    sel = [0, 17, 40, 63]
     cext = arrays.correct_ext()
-    hist_o, ok_o = O.eval_hist(arrays.errs, cext, th[sel])
-    assert np.array_equal(hist[sel], hist_o) and np.array_equal(ok[sel], ok_o)
-    acc, sav = ev.evaluate_many(th[sel])
-    acc_o, sav_o = O.eval_thresholds(arrays.errs, cext, ev.serve, ev.vanilla_ms, th[sel])
-    assert np.array_equal(acc, acc_o)
+    hist_o, ok_o = O.eval_hist(arrays.errs, cext, th)
+    assert np.array_equal(hist, hist_o) and np.array_equal(ok, ok_o)
+    acc, sav = ev.evaluate_many(th)
+    assert np.array_equal(acc, _unhex(gold["diag_acc"]))
     # sav is a difference of O(vanilla) quantities: compare on the serve-time scale
-    np.testing.assert_allclose(sav, sav_o, rtol=0, atol=1e-9 * ev.vanilla_ms)
+    np.testing.assert_allclose(sav, _unhex(gold["diag_sav"]), rtol=0, atol=1e-9 * ev.vanilla_ms)
     # and our value is the correctly rounded mean (within 2 ulp of the exact rational)
-    for row, s_got in zip(hist[sel], sav):
+    for row, s_got in zip(hist, sav):
         exact = Fraction(ev.vanilla_ms) - sum(int(k) * Fraction(float(v)) for k, v in zip(row, ev.serve)) / n
         assert abs(Fraction(s_got) - exact) <= 2 * np.spacing(abs(float(exact)))
+
+
+def test_full_size_config4_axis_family_vs_reference(cuda):
+    """The 768-row axis family over the full 1M x 12 window: acc
+    bit-identical to the reference's compiled kernel, sav within 1e-9 * vanilla."""
+    from paper_2312_05385_b200 import kernels as K
+    from paper_2312_05385_b200 import synth
+
+    gold = _config4_golden()
+    prof = config4_profile()
+    sites = find_feasible_sites(prof)
+    ev = WindowEvaluator.from_arrays(synth.config4_window(1_000_000), sites, prof, mode="hist")
+    axis = np.full((768, 12), 0.3)
+    for j in range(12):
+        axis[j * 64:(j + 1) * 64, j] = np.arange(64) / 63.0
+    assert K.classify_candidates(axis)[0] == "axis"
+    acc, sav = ev.evaluate_many(axis)
+    assert np.array_equal(acc, _unhex(gold["axis_acc"]))
+    np.testing.assert_allclose(sav, _unhex(gold["axis_sav"]), rtol=0, atol=1e-9 * ev.vanilla_ms)
 
 
 @pytest.mark.parametrize("r,clustered", [(1, False), (3, True), (7, False), (12, False),

@@ -144,3 +144,49 @@ def test_reference_kernel_build_agrees_with_oracle(kernels_random):
     for w in kernels_random[:3]:
         acc, sav = ref.eval_thresholds(w["scores"], w["cext"], w["serve"], float(w["vanilla"]), w["th"])
         assert np.array_equal(acc, w["acc"]) and np.array_equal(sav, w["sav"])
+
+
+def _config4_golden():
+    import json
+    import os
+
+    from conftest import GOLDEN
+
+    with open(os.path.join(GOLDEN, "config4_1m.json")) as fh:
+        return json.load(fh)
+
+
+def test_native_window_replay_equals_reference_generator_at_full_size():
+    """The headline window (synth.config4_window: the native PCG64 replay,
+    csrc/synth.cpp, host-only) equals the reference generator's 1M x 12 window
+    packed by the reference's WindowEvaluator, byte for byte
+    (tests/golden/make_config4_golden.py; trace.py:164-227, engine.py:152-163)."""
+    import hashlib
+
+    from paper_2312_05385_b200 import synth
+
+    gold = _config4_golden()
+    arrays = synth.config4_window(gold["n"])
+    assert arrays.errs.shape == (gold["n"], gold["r"])
+    assert hashlib.sha256(np.ascontiguousarray(arrays.errs).tobytes()).hexdigest() == gold["scores_sha256"]
+    cext_u8 = np.ascontiguousarray(arrays.correct_ext().astype(np.uint8))
+    assert hashlib.sha256(cext_u8.tobytes()).hexdigest() == gold["correct_u8_sha256"]
+    prof = config4_profile()
+    serve = serve_table(find_feasible_sites(prof), prof, 1)
+    assert [x.hex() for x in serve] == gold["serve"]
+
+
+def test_oracle_full_size_diagonal_matches_reference():
+    """The C oracle on the full 1M x 12 window, all 64 diagonal candidates:
+    acc bit-identical and sav bit-identical (same accumulation order) to the
+    reference's compiled kernel."""
+    from paper_2312_05385_b200 import synth
+
+    gold = _config4_golden()
+    arrays = synth.config4_window(gold["n"])
+    prof = config4_profile()
+    serve = serve_table(find_feasible_sites(prof), prof, 1)
+    th = np.repeat((np.arange(64) / 63.0)[:, None], 12, axis=1)
+    acc, sav = O.eval_thresholds(arrays.errs, arrays.correct_ext(), serve, prof.model_latency(1), th)
+    assert [x.hex() for x in acc] == gold["diag_acc"]
+    assert [x.hex() for x in sav] == gold["diag_sav"]

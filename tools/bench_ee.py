@@ -119,10 +119,7 @@ DTYPE_NOTE = ("bf16 autocast over fp32 weights" if AUTOCAST
 def _native_bf16(model, channels_last):
     if AUTOCAST:
         return
-    if channels_last:  # CNNs: BatchNorm folded into the convolutions (inference form)
-        ee_infer.fold_batchnorm(model)
-        model.to(memory_format=torch.channels_last)
-    model.to(torch.bfloat16)
+    ee_infer.prepare_bf16(model, channels_last)
 
 
 def _image(g, channels_last):

@@ -18,7 +18,7 @@ import eesim._kernels  # noqa: E402
 from paper_2312_05385_b200 import kernels  # noqa: E402
 
 kernels.install_into(eesim._kernels)
-assert eesim._kernels.eval_thresholds is kernels.eval_thresholds
+assert getattr(eesim._kernels.eval_thresholds, "__wrapped__", None) is kernels.eval_thresholds
 
 import pytest  # noqa: E402
 
