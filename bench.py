@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--copies", type=int, default=4, help="resident window copies rotated per step")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-replicas", action="store_true",
+                   help="skip the data-parallel serving replicas (config 3, one per GPU)")
     p.add_argument("--no-extra", action="store_true",
                    help="skip the other BASELINE configs (1-3 EE inference, 5 token-level decode)")
     return p.parse_args()
@@ -489,6 +491,17 @@ def run_ours(args):
         "generic_sweep": generic, "latency": latency, "windows_batch": windows_batch,
         "timed_as": "CUDA graph of the K sweeps" if graph_used else "eager stream launches",
     }
+    if not args.no_replicas:
+        # every rank: one ResNet-50 EE replica + controller per GPU (config 3,
+        # B=256 per GPU), round-robin request batches; rank 0 gets the aggregate
+        from paper_2312_05385_b200.replicas import run_replicas
+
+        try:
+            agg = run_replicas("c3", 8 * world)
+        except Exception as exc:  # reported, never fatal to the headline line
+            agg = {"error": repr(exc)[:400]}
+        if rank == 0:
+            line["serving_replicas"] = agg
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, arrays, prof, sites, th, acc, sav)
     if rank == 0 and world == 1 and not args.no_extra:
@@ -635,7 +648,8 @@ def other_configs():
                         ("generative", ["tools/bench_gen.py"], 300),
                         ("serving_loop", ["tools/bench_serve_live.py"], 300),
                         ("candidate_families", ["tools/bench_families.py"], 300),
-                        ("tune", ["tools/bench_tune.py"], 300)):
+                        ("tune", ["tools/bench_tune.py"], 300),
+                        ("cpu_baselines", ["tools/bench_cpu.py"], 900)):
         try:
             r = subprocess.run([sys.executable, os.path.join(ROOT, *cmd[0].split("/"))] + cmd[1:],
                                capture_output=True, text=True, timeout=t, cwd=ROOT)

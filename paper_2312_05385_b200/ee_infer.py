@@ -313,9 +313,14 @@ def resnet18_cifar(num_classes: int = 10, ramp_sites=(0, 2, 3, 5, 6, 8), seed: i
     return EEPipeline(blocks + [final], ramps, [names[s] for s in sorted(ramps)]), m
 
 
-def resnet50_imagenet(seed: int = 0, conf: str = "maxprob", dtype=None):
+def resnet50_imagenet(seed: int = 0, conf: str = "maxprob", dtype=None, head_scale: float = 16.0):
     """BASELINE config 3: ResNet-50, 224x224, a ramp after each of the 16
-    bottlenecks, 1000-class heads on the tensor-core GEMM path."""
+    bottlenecks, 1000-class heads on the tensor-core GEMM path.
+
+    Ramp FC init: N(0, (head_scale / sqrt(C))^2). Random-init pooled features
+    barely vary across inputs, so at the usual 1/sqrt(C) every 1000-class
+    confidence sits within ~1e-4 of 0.998 and every row of a batch is a 1e-5
+    near-tie; at 16/sqrt(C) the per-ramp err spreads over ~0.05-0.1."""
     torch = nat.torch_cuda()
     import torchvision
 
@@ -334,7 +339,7 @@ def resnet50_imagenet(seed: int = 0, conf: str = "maxprob", dtype=None):
     g = torch.Generator().manual_seed(seed + 1)
     ramps = {}
     for s, c in enumerate(chans):
-        w = torch.randn(1000, c, generator=g) / c ** 0.5
+        w = torch.randn(1000, c, generator=g) * (head_scale / c ** 0.5)
         ramps[s] = LargeRampHead(w.cuda(), None, conf=conf, site=s)
     names = [f"bottleneck{s}" for s in range(len(chans))]
     return EEPipeline(stages + [final], ramps, names), m

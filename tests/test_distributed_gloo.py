@@ -79,3 +79,41 @@ def test_two_rank_gloo_histograms_equal_full_window():
     for rank in range(world):
         h, k = out[rank]
         assert np.array_equal(h, hist_full) and np.array_equal(k, ok_full)
+
+
+def _replica_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_05385_b200.replicas import ReplicaStats, aggregate, replica_batches
+
+        mine = replica_batches(10, rank, world)
+        # stand-in for the per-GPU serving loop: fixed per-batch latencies
+        lat = [1.0 + rank + 0.1 * i for i in range(len(mine))]
+        st = ReplicaStats(rank, 256 * len(mine), sum(lat), lat, exits=200 * len(mine),
+                          near_ties=rank)
+        out[rank] = (mine, aggregate(st))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replica_dispatch_and_aggregation_world2_gloo():
+    """Data-parallel serving (replicas only): request batches are
+    split round-robin over replicas with no overlap and no loss, and the job's
+    numbers are all samples / the slowest replica and p50 over every replica's
+    batch latencies, identical on every rank."""
+    world = 2
+    port = _free_port()
+    out = mp.Manager().dict()
+    mp.spawn(_replica_worker, args=(world, port, out), nprocs=world, join=True)
+    b0, a0 = out[0]
+    b1, a1 = out[1]
+    assert sorted(b0 + b1) == list(range(10)) and not set(b0) & set(b1)
+    assert a0 == a1
+    lat = [1.0 + 0.1 * i for i in range(5)] + [2.0 + 0.1 * i for i in range(5)]
+    assert a0["samples"] == 2560 and a0["replicas"] == 2
+    assert a0["slowest_replica_ms"] == sum(lat[5:])
+    assert a0["samples_per_s"] == 2560 / (sum(lat[5:]) / 1e3)
+    assert a0["p50_batch_ms"] == float(np.percentile(lat, 50))
+    assert a0["exit_rate"] == 2000 / 2560 and a0["near_tie_rows"] == 1

@@ -81,3 +81,43 @@ def test_two_rank_sweep_matches_one_gpu(cuda):
         for (acc, sav), (a1, s1) in zip(got[rank], one):
             assert np.array_equal(np.array(acc), a1)
             assert np.array_equal(np.array(sav), s1)
+
+
+def _replica_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.update(WORLD_SIZE=str(world), RANK=str(rank), LOCAL_RANK="0")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_05385_b200.replicas import run_replicas, serve
+
+        agg = run_replicas("c1", n_batches=6)
+        q.put((rank, agg))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_replica_serving_path(cuda):
+    """Data-parallel serving: two replicas (both on cuda:0, gloo
+    standing in for NCCL) each serve their round-robin share of 6 request batches
+    through the captured EE graph with pinned H2D / D2H; rank 0 aggregates."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert got[1] is None
+    agg = got[0]
+    assert agg["replicas"] == 2 and agg["samples"] == 6 * 32
+    assert agg["samples_per_s"] > 0 and agg["p50_batch_ms"] > 0
+    assert 0.0 < agg["exit_rate"] <= 1.0
