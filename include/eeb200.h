@@ -202,21 +202,31 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits, int64_t b, int3
                         uint8_t* d_exit, int32_t* d_keep, int32_t* d_nkeep, int32_t* d_slot_label,
                         float* d_slot_err, int32_t* d_slot_site, void* stream);
 
-/* Tensor-core ramp-head GEMM (tcgen05.mma, TMEM accumulators):
- * d_c f32 [m, n] = d_a bf16 [m, k] (row-major) x d_b bf16 [n, k]^T (row-major,
- * i.e. nn.Linear weight layout) + d_bias f32 [n] (nullable). k % 8 == 0.
- * splits <= 0 picks a split-K that fills the SMs; split partials are summed
- * in a fixed order (deterministic). */
+/* Tensor-core ramp-head GEMM: d_c f32 [m, n] = d_a bf16 [m, k] (row-major) x
+ * d_b bf16 [n, k]^T (row-major, i.e. nn.Linear weight layout) + d_bias f32 [n]
+ * (nullable). k % 8 == 0. Same kernels as ee_gemm_bf16_ex (act none, auto
+ * path); `splits` > 0 pins the swap kernel's split count. Deterministic. */
 int ee_gemm_bf16_tn(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
                     float* d_c, int64_t m, int64_t n, int64_t k, int32_t splits, void* stream);
 
 /* General form: d_c is fp32 [m, n], or bf16 [m, n] (round to nearest even)
- * when out_bf16 != 0 — the backbone layers' output type. Warp-specialized
- * tcgen05 kernel: TMA (SWIZZLE_128B) 4-stage ring, one MMA-issuing thread,
- * TMEM accumulators, 4 epilogue warps; split-K partials are summed in order. */
+ * when out_bf16 != 0 — ee_gemm_bf16_ex with no activation, auto path. */
 int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
                  void* d_c, int32_t out_bf16, int64_t m, int64_t n, int64_t k, int32_t splits,
                  void* stream);
+
+/* Backbone / head GEMM with a fused epilogue (csrc/gemm.cu):
+ *   d_c [m, n] = act(d_a bf16 [m, k] x d_w bf16 [n, k]^T + d_bias f32 [n])
+ * d_c is bf16 (out_bf16 != 0, round to nearest even) or f32. act: 0 none,
+ * 1 GELU (erf), 2 GELU (tanh approximation), 3 ReLU. path: 0 auto, 1 swap-AB
+ * weight-streaming kernel (cluster split-K, DSMEM reduction, any m), 2 / 4 / 3
+ * the persistent CTA-pair kernel (cta_group::2, 256 x 256 / 192 / 128 tiles;
+ * needs 16-byte output rows). Auto takes the swap kernel for m <= 256. k % 8 == 0,
+ * all pointers 16-byte aligned. Results are deterministic. Replaces the
+ * library GEMMs the reference's models would call. */
+int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
+                    void* d_c, int32_t out_bf16, int32_t act, int64_t m, int64_t n, int64_t k,
+                    int32_t splits, int32_t path, void* stream);
 
 /* Global average pool NCHW [b, c, hw] (f32, or bf16 when x_bf16) -> bf16
  * [b, c] (round to nearest even): the A operand of a large ramp head. */

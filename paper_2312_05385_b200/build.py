@@ -9,7 +9,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = [os.path.join(HERE, "csrc", "eeb200.cu"), os.path.join(HERE, "csrc", "synth.cpp")]
+SOURCES = [os.path.join(HERE, "csrc", "eeb200.cu"), os.path.join(HERE, "csrc", "gemm.cu"),
+           os.path.join(HERE, "csrc", "synth.cpp")]
 HEADERS = [os.path.join(ROOT, "include", "eeb200.h")] + sorted(
     glob.glob(os.path.join(HERE, "csrc", "*.cuh")))
 LIB = os.path.join(HERE, "libeeb200.so")
@@ -28,14 +29,23 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each translation unit in parallel, then link the shared library."""
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
-           "-shared", "-o", LIB + ".tmp", *SOURCES]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
+        flags.append("-Xptxas=-v")
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(HERE, "csrc", os.path.basename(src) + ".o")
+        objs.append(obj)
+        procs.append(subprocess.Popen([nvcc(), *flags, "-c", "-o", obj, src]))
+    if any(p.wait() != 0 for p in procs):
+        raise subprocess.CalledProcessError(1, "nvcc")
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs], check=True)
     os.replace(LIB + ".tmp", LIB)
+    for o in objs:
+        os.remove(o)
     return LIB
 
 

@@ -500,7 +500,6 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
 #include "pool.cuh"
-#include "gemm_tc2.cuh"
 namespace {
 
 // L2 eviction for benchmarks: streams a buffer larger than L2 with the same
@@ -2172,103 +2171,37 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
 }
 
 }  // extern "C"
-// TMA descriptors: cuTensorMapEncodeTiled through the runtime's driver entry
-// point (no libcuda link). A bf16 [rows, k] K-major operand, 64 x box_rows
-// boxes (128 B rows), SWIZZLE_128B, zero fill out of bounds.
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-static bool make_operand_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t k,
-                             int box_rows) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)k * 2};
-  cuuint32_t box[2] = {(cuuint32_t)gemm2::BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-template <int BN, bool BF>
-static cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const float* bias,
-                                void* c, int m, int n, int k, int per, float* partials, dim3 grid,
-                                cudaStream_t st) {
-  auto kern = gemm2::k_gemm2<BN, BF>;
-  constexpr int smem = gemm2::smem_bytes<BN>();
-  {
-    cudaError_t e = ensure_smem(kern, smem);
-    if (e != cudaSuccess) return e;
-  }
-  kern<<<grid, gemm2::THREADS, smem, st>>>(ta, tb, bias, c, m, n, k, per, partials);
-  return cudaGetLastError();
-}
+// gemm.cu (tcgen05 pair / swap-AB kernels)
+cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, void* c, int out_bf16,
+                            int act, int m, int n, int k, int splits, int path, cudaStream_t st);
 extern "C" {
 
 int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
                  void* d_c, int32_t out_bf16, int64_t m, int64_t n, int64_t k, int32_t splits,
                  void* stream) {
+  return ee_gemm_bf16_ex(ws, d_a, d_b, d_bias, d_c, out_bf16, 0, m, n, k, splits, 0, stream);
+}
+
+int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
+                    void* d_c, int32_t out_bf16, int32_t act, int64_t m, int64_t n, int64_t k,
+                    int32_t splits, int32_t path, void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
   if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(EE_ERR_ARG, "bad GEMM shape");
   if (k % 8) return fail(EE_ERR_ARG, "K must be a multiple of 8 (16-byte rows)");
-  if (!d_a || !d_b || !d_c) return fail(EE_ERR_ARG, "null pointer");
-  if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_b)) & 15)
-    return fail(EE_ERR_ARG, "A and B must be 16-byte aligned");
+  if (act < 0 || act > 3 || path < 0 || path > 4) return fail(EE_ERR_ARG, "bad act or path");
+  if (!d_a || !d_w || !d_c) return fail(EE_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_w) |
+       reinterpret_cast<uintptr_t>(d_c)) & 15)
+    return fail(EE_ERR_ARG, "A, W and C must be 16-byte aligned");
   std::lock_guard<std::mutex> lock(ws->mu);
   auto st = (cudaStream_t)stream;
-  const int64_t mt = ceil_div(m, gemm2::BM);
-  // wide tiles when they alone fill the SMs, else 128 columns (+ split-K)
-  const int BN = mt * ceil_div(n, 256) >= sm_count() ? 256 : 128;
-  const int64_t nt = ceil_div(n, BN);
-  const int kt_total = (int)ceil_div(k, gemm2::BK);
-  int sp = splits;
-  if (sp <= 0) sp = (int)std::max<int64_t>(1, std::min<int64_t>(kt_total, sm_count() / std::max<int64_t>(1, mt * nt)));
-  sp = std::min(sp, kt_total);
-  const int per = (kt_total + sp - 1) / sp;
-  sp = (kt_total + per - 1) / per;  // no empty splits
-  float* partials = nullptr;
-  if (sp > 1) {
-    int rc = ws_reserve(ws, (size_t)sp * m * n * 4, 0);
-    if (rc) return rc;
-    partials = static_cast<float*>(ws->d_buf);
-  }
-  CUtensorMap ta, tb;
-  if (!make_operand_map(&ta, d_a, m, k, gemm2::BM) || !make_operand_map(&tb, d_b, n, k, BN))
-    return fail(EE_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)sp);
   cudaError_t e;
   {
-    ProfScope ps(ws, st, "k_gemm2");
-    if (BN == 256)
-      e = out_bf16 ? launch_gemm2<256, true>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st)
-                   : launch_gemm2<256, false>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st);
-    else
-      e = out_bf16 ? launch_gemm2<128, true>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st)
-                   : launch_gemm2<128, false>(ta, tb, d_bias, d_c, (int)m, (int)n, (int)k, per, partials, grid, st);
+    ProfScope ps(ws, st, "k_gemm3");
+    e = ee_gemm3_launch(d_a, d_w, d_bias, d_c, out_bf16, act, (int)m, (int)n, (int)k, splits, path, st);
   }
-  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_gemm2: ") + cudaGetErrorString(e));
-  if (sp > 1) {
-    ProfScope ps(ws, st, "k_splitk_sum");
-    const int64_t mn = m * n;
-    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(mn, 256), sm_count() * 8);
-    if (out_bf16)
-      gemm2::k_splitk_sum2<true><<<g, 256, 0, st>>>(partials, sp, mn, (int)n, d_bias, d_c);
-    else
-      gemm2::k_splitk_sum2<false><<<g, 256, 0, st>>>(partials, sp, mn, (int)n, d_bias, d_c);
-    EE_LAUNCH_CHECK();
-  }
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_gemm3: ") + cudaGetErrorString(e));
   return EE_OK;
 }
 

@@ -1,0 +1,764 @@
+// gemm.cu — 5th-generation tensor-core GEMMs for the backbone contractions and
+// the wide ramp heads (north star (1)):
+//
+//     C[M, N] (bf16 or fp32) = act(A[M, K] (bf16, K-major) * W[N, K]^T (bf16) + bias[N])
+//
+// W is an nn.Linear weight (out_features x in_features, row-major), so both
+// operands are K-major and the whole contraction is one tcgen05 "TN" GEMM.
+// Two kernels, picked per shape by the host (dispatch below):
+//
+// k_gemm_pair  (M > 256: BERT encoder projections, GPT-2 prefill)
+//   Persistent, one CTA pair (cluster of 2, cta_group::2) per two SMs. A pair
+//   owns 256 x BN output tiles (BN = 256 or 128); CTA r loads A rows
+//   [m0 + 128r, +128) and W rows [n0 + BN/2 r, +BN/2) into its own half of a
+//   STAGES-deep ring (TMA, SWIZZLE_128B), and the leader's single thread issues
+//   tcgen05.mma.cta_group::2 M=256 over both halves. Accumulators are double
+//   buffered in TMEM (2 x BN fp32 columns), so the pair's 8 epilogue warps
+//   drain tile i (tcgen05.ld -> bias/activation -> bf16 -> swizzled smem ->
+//   TMA store) while the tensor cores already run tile i+1.
+//
+// k_gemm_swap  (M <= 256: decode steps, ramp heads on a batch)
+//   Weight streaming. The roles of the operands swap: W is the MMA's M side
+//   (128 output features per CTA) and up to 128 activation rows are its N side
+//   (32 / 64 / 128; more rows take more CTAs along z). The K range is split
+//   over a cluster of S CTAs along x. Activation row c is owned by cluster rank
+//   c % S: every CTA pushes its fp32 partial for c straight from TMEM into the
+//   owner's receive slot (DSMEM stores), and after one cluster barrier each
+//   owner sums its S slots in rank order (deterministic), adds the bias,
+//   applies the activation and stores. One launch, no global scratch, no
+//   second reduction kernel.
+//
+// Both: warp 0 = TMA producer (one lane), warp 1 = TMEM allocator + MMA issuer
+// (one lane), warps 2..5 = epilogue (warp w owns TMEM lanes 32*(w%4)..).
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace gemm3 {
+
+constexpr int BK = 64;  // bf16 per k-tile row = 128 B = one SWIZZLE_128B atom row
+constexpr int THREADS = 192;       // swap kernel: producer, MMA, 4 epilogue warps
+constexpr int PAIR_THREADS = 320;  // pair kernel: producer, MMA, 8 epilogue warps
+constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the pair's rank 0
+
+enum Act { ACT_NONE = 0, ACT_GELU_ERF = 1, ACT_GELU_TANH = 2, ACT_RELU = 3 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B: 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: fp32 accumulate, bf16 x bf16, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// arrive on the pair leader's copy of this barrier (same smem offset, rank 0)
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                   smem_u32(bar) & PEER_MASK)
+               : "memory");
+}
+
+// TMA 2D load into this CTA's smem, completion bytes on `bar` (this CTA's)
+__device__ __forceinline__ void tma_load(void* smem, const CUtensorMap* map, uint64_t* bar, int x,
+                                         int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+// pair form: data lands in this CTA's smem, completion bytes on the leader's barrier
+__device__ __forceinline__ void tma_load_pair(void* smem, const CUtensorMap* map, uint64_t* bar,
+                                              int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* smem, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem)), "r"(x), "r"(y)
+               : "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t id,
+                                     uint32_t acc) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(id), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(id), "r"(acc));
+}
+// MMA completion -> mbarrier arrive (cta_group::2: on both CTAs of the pair)
+template <int CG>
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  else
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t cols) {
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst)),
+                 "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst)),
+                 "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t cols) {
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols));
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols));
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// 32 lanes x 32 consecutive fp32 columns (one TMEM row per lane); no wait
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {  // RNE, lo in the low half
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+template <int ACT>
+__device__ __forceinline__ float act(float x) {
+  if constexpr (ACT == ACT_GELU_ERF) return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+  if constexpr (ACT == ACT_GELU_TANH) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    return 0.5f * x * (1.f + tanhf(u));
+  }
+  if constexpr (ACT == ACT_RELU) return fmaxf(x, 0.f);
+  return x;
+}
+
+// ===========================================================================
+// k_gemm_pair: persistent, CTA pair, 256 x BN tiles, double-buffered TMEM.
+// ===========================================================================
+template <int BN>
+struct PairCfg {
+  static constexpr int A_BYTES = 128 * BK * 2;         // this CTA's 128 rows of A
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;    // this CTA's BN/2 rows of W
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int EPI = 8 * 2 * 32 * 128;         // 8 warps x 2 buffers x 32 rows x 128 B
+  static constexpr int BIAS = 8 * 64 * 4;              // one 64-float bias row per epilogue warp
+  // dynamic = alignment slack + ring + staging + bias; ~1 KB of static barriers
+  static constexpr int STAGES = std::min(8, (SMEM_LIMIT - 1024 - 1024 - EPI - BIAS) / STAGE);
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BIAS;
+};
+
+template <int BN, int ACT, bool OUT_BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
+    k_gemm_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int M,
+                int N, int K) {
+  using Cfg = PairCfg<BN>;
+  constexpr int ST = Cfg::STAGES;
+  constexpr int CW = OUT_BF16 ? 64 : 32;  // output columns per 128-byte staging row
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* epi_smem = smem + ST * Cfg::STAGE;
+  float* bias_smem = reinterpret_cast<float*>(epi_smem + Cfg::EPI);
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int mt = (M + 255) / 256, nt = (N + BN - 1) / BN;
+  const int tiles = mt * nt;
+  const int kt_n = (K + BK - 1) / BK;
+  const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full_bar[s], 1);   // the leader's expect_tx; both CTAs' bytes
+      mbar_init(&empty_bar[s], 1);  // one multicast MMA commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);   // one multicast MMA commit
+      mbar_init(&tempty_bar[a], 16);  // the 16 epilogue warps of the pair (leader's copy used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 accumulators
+  if (warp == 1) tmem_alloc<2>(&tmem_base, TMEM_COLS);
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer (both CTAs; bytes land on the leader's barrier)
+      uint32_t it = 0;
+      for (int t = pair; t < tiles; t += pairs) {
+        const int m0 = (t % mt) * 256 + (int)rank * 128;
+        const int n0 = (t / mt) * BN + (int)rank * (BN / 2);
+        for (int kt = 0; kt < kt_n; ++kt, ++it) {
+          const int s = it % ST;
+          mbar_wait(&empty_bar[s], ((it / ST) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * Cfg::STAGE);
+          unsigned char* sa = smem + s * Cfg::STAGE;
+          tma_load_pair(sa, &tmA, &full_bar[s], kt * BK, m0);
+          tma_load_pair(sa + Cfg::A_BYTES, &tmB, &full_bar[s], kt * BK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ===== MMA issuer (leader only)
+      constexpr uint32_t id = idesc(256, BN);
+      uint32_t it = 0, ai = 0;
+      for (int t = pair; t < tiles; t += pairs, ++ai) {
+        const uint32_t a = ai & 1;
+        mbar_wait(&tempty_bar[a], ((ai >> 1) & 1) ^ 1);
+        fence_after();
+        const uint32_t d = tmem + a * BN;
+        for (int kt = 0; kt < kt_n; ++kt, ++it) {
+          const int s = it % ST;
+          mbar_wait(&full_bar[s], (it / ST) & 1);
+          fence_after();
+          const uint32_t a0 = smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma<2>(d, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32), id, (kt | k) ? 1u : 0u);
+          umma_commit<2>(&empty_bar[s]);
+        }
+        umma_commit<2>(&tfull_bar[a]);
+      }
+    }
+  } else {  // ===== epilogue: warps 2..9; TMEM lane quarter q = warp % 4, column half h
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    unsigned char* stage0 = epi_smem + (warp - 2) * 2 * 4096;  // two 32 x 128 B staging boxes
+    float* bias_row = bias_smem + (warp - 2) * 64;
+    uint32_t ai = 0;
+    int buf = 0;
+    for (int t = pair; t < tiles; t += pairs, ++ai) {
+      const uint32_t a = ai & 1;
+      const int row0 = (t % mt) * 256 + (int)rank * 128 + q * 32;
+      const int n0 = (t / mt) * BN;
+      mbar_wait(&tfull_bar[a], (ai >> 1) & 1);
+      fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
+      constexpr int NCH = BN / CW;  // chunks per tile; half h takes chunks [h*NCH/2 ...)
+      const int c_lo = h * (NCH / 2) * CW, c_hi = h ? BN : (NCH / 2) * CW;
+#pragma unroll 1
+      for (int c0 = c_lo; c0 < c_hi; c0 += CW) {
+        uint32_t v[CW];
+        if constexpr (CW == 64) {
+          tmem_ld32_nowait(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          tmem_ld32_nowait(tbase + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        } else {
+          tmem_ld32_nowait(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        }
+        tmem_wait_ld();
+        if (c0 + CW >= c_hi) {  // this warp's columns drained: the MMA may reuse them
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(&tempty_bar[a]);
+        }
+        if (n0 + c0 >= N) continue;  // fully out of range (TMA would clip anyway)
+        // bias for these CW columns through a warp-private smem row, read back
+        // as broadcast float4s
+        float f[CW];
+        if (bias) {
+          const int cA = n0 + c0 + lane, cB = cA + 32;
+          bias_row[lane] = cA < N ? __ldg(bias + cA) : 0.f;
+          if (CW == 64) bias_row[lane + 32] = cB < N ? __ldg(bias + cB) : 0.f;
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < CW; j += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bias_row + j);
+            f[j] = act<ACT>(__uint_as_float(v[j]) + b4.x);
+            f[j + 1] = act<ACT>(__uint_as_float(v[j + 1]) + b4.y);
+            f[j + 2] = act<ACT>(__uint_as_float(v[j + 2]) + b4.z);
+            f[j + 3] = act<ACT>(__uint_as_float(v[j + 3]) + b4.w);
+          }
+          __syncwarp();
+        } else {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) f[j] = act<ACT>(__uint_as_float(v[j]));
+        }
+        // the staging buffer we are about to overwrite: its store must have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        const uint32_t sb = smem_u32(stage0 + buf * 4096 + lane * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this row, SWIZZLE_128B position
+          uint4 w;
+          if constexpr (OUT_BF16) {
+            w.x = bf16x2(f[8 * c + 0], f[8 * c + 1]);
+            w.y = bf16x2(f[8 * c + 2], f[8 * c + 3]);
+            w.z = bf16x2(f[8 * c + 4], f[8 * c + 5]);
+            w.w = bf16x2(f[8 * c + 6], f[8 * c + 7]);
+          } else {
+            w.x = __float_as_uint(f[4 * c + 0]);
+            w.y = __float_as_uint(f[4 * c + 1]);
+            w.z = __float_as_uint(f[4 * c + 2]);
+            w.w = __float_as_uint(f[4 * c + 3]);
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + ((c ^ (lane & 7)) << 4)),
+                       "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store(&tmC, stage0 + buf * 4096, n0 + c0, row0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf ^= 1;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  fence_before();
+  cluster_sync();  // neither CTA frees TMEM / exits while the pair still uses it
+  if (warp == 1) tmem_dealloc<2>(tmem, TMEM_COLS);
+}
+
+// ===========================================================================
+// k_gemm_swap: C^T tiles = W (128 features) x A^T (NP <= 256 rows), split-K
+// over a cluster of S CTAs, DSMEM reduction in rank order.
+// ===========================================================================
+template <int NP>
+struct SwapCfg {
+  static_assert(NP == 32 || NP == 64 || NP == 128, "activation rows per CTA");
+  static constexpr int W_BYTES = 128 * BK * 2;
+  static constexpr int A_BYTES = NP * BK * 2;
+  static constexpr int STAGE = W_BYTES + A_BYTES;
+  // receive buffer: S slots x ceil(NP / S) columns x 128 features (fp32), at
+  // most (NP + 16) x 128 floats; separate from the ring so that peers may push
+  // into it while this CTA's MMAs still read the ring
+  static constexpr int RECV = (NP + 16) * 128 * 4;
+  // NP = 32: two CTAs per SM (more weight bytes in flight per SM; one CTA's
+  // prologue/epilogue overlaps the other's stream)
+  static constexpr int CTAS_PER_SM = NP <= 32 ? 2 : 1;
+  static constexpr int STAGES_MAX = (SMEM_LIMIT / CTAS_PER_SM - 2048 - RECV) / STAGE;
+  static constexpr int STAGES = STAGES_MAX > 6 ? 6 : STAGES_MAX;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + RECV;
+  static constexpr int TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : 128;
+};
+
+template <int NP, int ACT, bool OUT_BF16>
+__global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
+    k_gemm_swap(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
+                const float* __restrict__ bias, void* __restrict__ C, int M, int N, int K,
+                int kt_per) {
+  using Cfg = SwapCfg<NP>;
+  constexpr int ST = Cfg::STAGES;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const uint32_t recv = smem_u32(smem + ST * Cfg::STAGE);
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], done_bar;
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = gridDim.x;  // cluster size = split count (the cluster spans x)
+  const int s_rank = blockIdx.x;
+  const int f0 = blockIdx.y * 128;  // output features of this CTA
+  const int r0 = blockIdx.z * NP;   // activation rows of this CTA
+  const int rows = min(NP, M - r0);
+  const int U = (NP + S - 1) / S;   // max columns (activation rows) per owner
+  const int kt_n = (K + BK - 1) / BK;
+  const int kt0 = s_rank * kt_per, kt1 = min(kt_n, kt0 + kt_per);
+  const int nkt = max(0, kt1 - kt0);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc<1>(&tmem_base, Cfg::TMEM_COLS);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base;
+  cluster_arrive_relaxed();  // waited on before the first DSMEM access: every peer has started
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkt; ++i) {
+        const int s = i % ST;
+        if (i >= ST) mbar_wait(&empty_bar[s], ((i / ST) - 1) & 1);
+        unsigned char* sw = smem + s * Cfg::STAGE;
+        mbar_expect_tx(&full_bar[s], Cfg::STAGE);
+        tma_load(sw, &tmW, &full_bar[s], (kt0 + i) * BK, f0);
+        tma_load(sw + Cfg::W_BYTES, &tmA, &full_bar[s], (kt0 + i) * BK, r0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id = idesc(128, NP);
+      for (int i = 0; i < nkt; ++i) {
+        const int s = i % ST;
+        mbar_wait(&full_bar[s], (i / ST) & 1);
+        fence_after();
+        const uint32_t w0 = smem_u32(smem + s * Cfg::STAGE), a0 = w0 + Cfg::W_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma<1>(tmem, desc_sw128(w0 + k * 32), desc_sw128(a0 + k * 32), id, (i | k) ? 1u : 0u);
+        umma_commit<1>(&empty_bar[s]);
+      }
+      umma_commit<1>(&done_bar);
+    }
+  } else {
+    // epilogue warps: TMEM lane = feature q*32 + lane, column = activation row.
+    // Column c belongs to owner c % S; this CTA's partial for it is pushed into
+    // the owner's receive slot [s_rank][c / S] (remote shared stores: posted,
+    // 128 B per warp instruction).
+    const int q = warp & 3;
+    const int feat = q * 32 + lane;
+    if (nkt > 0) mbar_wait(&done_bar, 0);
+    fence_after();
+    cluster_wait();
+#pragma unroll 1
+    for (int c0 = 0; c0 < rows; c0 += 32) {
+      uint32_t v[32];
+      if (nkt > 0) {
+        tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0u;
+      }
+      int owner = c0 % S, u = c0 / S;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (c0 + j < rows) {
+          uint32_t remote;
+          const uint32_t local = recv + (uint32_t)(((s_rank * U + u) * 128 + feat) * 4);
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(owner));
+          asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(__uint_as_float(v[j]))
+                       : "memory");
+        }
+        if (++owner == S) owner = 0, ++u;
+      }
+    }
+  }
+  if (warp < 2) cluster_wait();
+  fence_before();
+  cluster_sync();  // every partial has landed in its owner's receive buffer
+  // owner s: columns s, s + S, ...: the S partials summed in rank order
+  // (deterministic), bias, activation, store (consecutive threads take
+  // consecutive features: coalesced)
+  {
+    const int mine = (rows - s_rank + S - 1) / S;
+    const float* rb = reinterpret_cast<const float*>(smem + ST * Cfg::STAGE);
+    for (int idx = threadIdx.x; idx < mine * 128; idx += THREADS) {
+      const int u = idx >> 7, feat = idx & 127;
+      const int col = s_rank + u * S;
+      float acc = 0.f;
+      for (int r = 0; r < S; ++r) acc += rb[(r * U + u) * 128 + feat];
+      const int f = f0 + feat;
+      if (f < N) {
+        const float y = act<ACT>(acc + (bias ? __ldg(bias + f) : 0.f));
+        const int64_t o = (int64_t)(r0 + col) * N + f;
+        if constexpr (OUT_BF16)
+          static_cast<uint16_t*>(C)[o] = (uint16_t)(bf16x2(y, 0.f) & 0xFFFFu);
+        else
+          static_cast<float*>(C)[o] = y;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<1>(tmem, Cfg::TMEM_COLS);
+}
+
+}  // namespace gemm3
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// row-major [rows, cols] tensor, box {box_cols, box_rows}, 128-byte swizzle
+bool make_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esize, int64_t rows,
+              int64_t cols, int box_cols, int box_rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * esize};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t set_smem(const void* fn, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;  // (fn, device)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& d : done)
+    if (d.first == fn && d.second == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) done.push_back({fn, dev});
+  return e;
+}
+
+int device_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+// how many CTA pairs of k_gemm_pair can be resident at once (cached per kernel)
+template <class Kern>
+int max_pairs(Kern kern, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* key = reinterpret_cast<const void*>(kern);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& c : cache)
+      if (c.first.first == key && c.first.second == dev) return c.second;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * 74, 1, 1);
+  cfg.blockDim = dim3(gemm3::PAIR_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg) != cudaSuccess || n <= 0)
+    n = device_sms() / 2;
+  std::lock_guard<std::mutex> g(mu);
+  cache.push_back({{key, dev}, n});
+  return n;
+}
+
+template <int BN, int ACT, bool BF>
+cudaError_t launch_pair(const void* a, const void* w, const float* bias, void* c, int m, int n,
+                        int k, cudaStream_t st) {
+  using Cfg = gemm3::PairCfg<BN>;
+  auto kern = gemm3::k_gemm_pair<BN, ACT, BF>;
+  cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
+  if (e != cudaSuccess) return e;
+  CUtensorMap ta, tb, tc;
+  if (!make_map(&ta, a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, k, gemm3::BK, 128) ||
+      !make_map(&tb, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, k, gemm3::BK, BN / 2) ||
+      !make_map(&tc, c, BF ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                BF ? 2 : 4, m, n, BF ? 64 : 32, 32))
+    return cudaErrorInvalidValue;
+  const int tiles = ((m + 255) / 256) * ((n + BN - 1) / BN);
+  const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
+  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, m, n, k);
+  return cudaGetLastError();
+}
+
+template <int NP, int ACT, bool BF>
+cudaError_t launch_swap(const void* a, const void* w, const float* bias, void* c, int m, int n,
+                        int k, int splits, cudaStream_t st) {
+  using Cfg = gemm3::SwapCfg<NP>;
+  auto kern = gemm3::k_gemm_swap<NP, ACT, BF>;
+  cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
+  if (e != cudaSuccess) return e;
+  CUtensorMap tw, ta;
+  if (!make_map(&tw, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, k, gemm3::BK, 128) ||
+      !make_map(&ta, a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, k, gemm3::BK, NP))
+    return cudaErrorInvalidValue;
+  const int ft = (n + 127) / 128;
+  const int kt_n = (k + gemm3::BK - 1) / gemm3::BK;
+  int S = splits;
+  if (S <= 0) {  // ~96 CTAs in all, S <= 8, >= 2 k-tiles per split: the
+                 // measured optimum on B200 (tools/sweep_swap.py) — beyond it the
+                 // cluster barrier and the per-CTA latency chain dominate
+    S = std::max(1, 96 / (ft * ((m + NP - 1) / NP)));
+    S = std::min({S, 8, std::max(1, kt_n / 2)});
+  }
+  S = std::max(1, std::min({S, 16, kt_n}));
+  const int per = (kt_n + S - 1) / S;
+  S = (kt_n + per - 1) / per;  // no empty split
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(S, ft, (m + NP - 1) / NP);
+  cfg.blockDim = dim3(gemm3::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, c, m, n, k, per);
+}
+
+template <int ACT, bool BF>
+cudaError_t dispatch_swap(const void* a, const void* w, const float* bias, void* c, int m, int n,
+                          int k, int splits, cudaStream_t st) {
+  if (m <= 32) return launch_swap<32, ACT, BF>(a, w, bias, c, m, n, k, splits, st);
+  if (m <= 64) return launch_swap<64, ACT, BF>(a, w, bias, c, m, n, k, splits, st);
+  return launch_swap<128, ACT, BF>(a, w, bias, c, m, n, k, splits, st);  // z tiles of 128 rows
+}
+
+// 256 x BN tiles: waves x the measured relative cost of one tile of that width
+// (B200, K-bound tiles: a 128-wide tile costs 0.76 of a 256-wide one, a
+// 192-wide one 0.853: the narrower MMAs leave the tensor pipe partly idle);
+// ties go to the wider tile
+int pick_bn(int m, int n, int pairs) {
+  const int bns[3] = {256, 192, 128};
+  const double rel[3] = {1.0, 0.853, 0.76};
+  int best = 256;
+  double best_cost = 1e30;
+  for (int i = 0; i < 3; ++i) {
+    const int64_t tiles = (int64_t)((m + 255) / 256) * ((n + bns[i] - 1) / bns[i]);
+    const double cost = (double)((tiles + pairs - 1) / pairs) * rel[i];
+    if (cost < best_cost * 0.97) best = bns[i], best_cost = cost;
+  }
+  return best;
+}
+
+template <int ACT, bool BF>
+cudaError_t dispatch(const void* a, const void* w, const float* bias, void* c, int m, int n, int k,
+                     int splits, int path, cudaStream_t st) {
+  // TMA stores need 16-byte output rows; otherwise (e.g. the 50257-wide LM
+  // head) the swap kernel's plain stores take any shape
+  const bool c_ok = (n * (BF ? 2 : 4)) % 16 == 0;
+  const bool swap = path == 1 || (path == 0 && (m <= 256 || !c_ok)) || !c_ok;
+  if (swap) return dispatch_swap<ACT, BF>(a, w, bias, c, m, n, k, splits, st);
+  const int bn = path == 3 ? 128 : path == 2 ? 256 : path == 4 ? 192 : pick_bn(m, n, device_sms() / 2);
+  if (bn == 256) return launch_pair<256, ACT, BF>(a, w, bias, c, m, n, k, st);
+  if (bn == 192) return launch_pair<192, ACT, BF>(a, w, bias, c, m, n, k, st);
+  return launch_pair<128, ACT, BF>(a, w, bias, c, m, n, k, st);
+}
+
+}  // namespace
+
+// Internal entry used by ee_gemm_bf16_ex (eeb200.cu). path: 0 auto, 1 swap-AB
+// split-K, 2 / 4 / 3 pair with BN = 256 / 192 / 128 (tests pin each path).
+cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, void* c, int out_bf16,
+                            int act, int m, int n, int k, int splits, int path, cudaStream_t st) {
+  switch (act * 2 + (out_bf16 ? 1 : 0)) {
+    case 0: return dispatch<0, false>(a, w, bias, c, m, n, k, splits, path, st);
+    case 1: return dispatch<0, true>(a, w, bias, c, m, n, k, splits, path, st);
+    case 2: return dispatch<1, false>(a, w, bias, c, m, n, k, splits, path, st);
+    case 3: return dispatch<1, true>(a, w, bias, c, m, n, k, splits, path, st);
+    case 4: return dispatch<2, false>(a, w, bias, c, m, n, k, splits, path, st);
+    case 5: return dispatch<2, true>(a, w, bias, c, m, n, k, splits, path, st);
+    case 6: return dispatch<3, false>(a, w, bias, c, m, n, k, splits, path, st);
+    case 7: return dispatch<3, true>(a, w, bias, c, m, n, k, splits, path, st);
+    default: return cudaErrorInvalidValue;
+  }
+}

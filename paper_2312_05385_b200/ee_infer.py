@@ -30,7 +30,7 @@ import numpy as np
 
 from paper_2312_05385_b200 import _native as nat
 from paper_2312_05385_b200.errors import ParameterError
-from paper_2312_05385_b200.heads import ExitController, LargeRampHead, SlotTable, exit_from_logits
+from paper_2312_05385_b200.heads import ExitController, LargeRampHead, SlotTable, exit_from_logits, gemm
 
 # North star: a sample whose confidence lies within 1e-5 of a threshold is a
 # near-tie — its exit decision may legitimately differ from an fp64 CPU oracle,
@@ -355,22 +355,18 @@ def bert_base(seq: int = 128, seed: int = 0, conf: str = "entropy"):
     cfg = BertConfig(attn_implementation="sdpa")
     bert = BertModel(cfg, add_pooling_layer=False).cuda().eval()
 
-    class Embed(torch.nn.Module):
-        def forward(self, ids):
-            return bert.embeddings(input_ids=ids)
+    class First:
+        """Embeddings + encoder layer 0 (the first ramp sits after layer 0)."""
 
-    class Layer(torch.nn.Module):
         def __init__(self, layer):
-            super().__init__()
             self.layer = layer
 
-        def forward(self, h):
-            out = self.layer(h)
-            return out[0] if isinstance(out, tuple) else out
+        def __call__(self, ids):
+            return self.layer(bert.embeddings(input_ids=ids))
 
     g = torch.Generator().manual_seed(seed + 1)
-    layers = [Layer(l) for l in bert.encoder.layer]
-    stages = [torch.nn.Sequential(Embed(), layers[0])] + layers[1:]
+    layers = [BertLayerTC(l) for l in bert.encoder.layer]
+    stages = [First(layers[0])] + layers[1:]
     heads = {}
     for s in range(len(layers)):
         w = torch.randn(2, cfg.hidden_size, generator=g) / cfg.hidden_size ** 0.5
@@ -388,6 +384,80 @@ def bert_base(seq: int = 128, seed: int = 0, conf: str = "entropy"):
             return h[:, 0].float() @ self.weight.t()
 
     return EEPipeline(stages + [Final()], heads, [f"layer{s}" for s in range(len(layers))]), bert
+
+
+class BertLayerTC:
+    """One post-LN BERT encoder layer (the weights of a transformers BertLayer)
+    with its four contractions on the repo's tcgen05 GEMMs (csrc/gemm.cu, A14):
+
+        qkv = h Wqkv^T + b          one GEMM over the fused [3d, d] weight
+        a   = SDPA(q, k, v)         (flash attention; not a GEMM this repo owns)
+        x   = LN(h + a Wo^T + bo)   GEMM, then ee_add_layernorm_bf16 (add + LN, one pass)
+        y   = LN(x + GELU(x W1^T + b1) W2^T + b2)   GELU fused into the W1 epilogue
+
+    On bf16 weights (the serving form, ee_infer.prepare_bf16) every projection is
+    a tcgen05 kernel; an fp32 model (the parity tests' reference configuration)
+    runs the same math through torch. The fused weight copies are built on the
+    first call after the dtype changes (before any CUDA-graph capture: the graph
+    runner warms up first)."""
+
+    def __init__(self, layer):
+        self.layer = layer
+        self._dtype = None
+
+    def _prep(self):
+        import torch
+
+        L = self.layer
+        sa, ao = L.attention.self, L.attention.output
+        dt = sa.query.weight.dtype
+        if dt == self._dtype:
+            return
+        self.n_head = sa.num_attention_heads
+        self.wqkv = torch.cat([sa.query.weight, sa.key.weight, sa.value.weight]).contiguous()
+        self.bqkv = torch.cat([sa.query.bias, sa.key.bias, sa.value.bias]).float().contiguous()
+        self.wo, self.bo = ao.dense.weight.contiguous(), ao.dense.bias.float().contiguous()
+        self.w1, self.b1 = L.intermediate.dense.weight.contiguous(), L.intermediate.dense.bias.float().contiguous()
+        self.w2, self.b2 = L.output.dense.weight.contiguous(), L.output.dense.bias.float().contiguous()
+        self.ln1, self.ln2 = ao.LayerNorm, L.output.LayerNorm
+        self._dtype = dt
+
+    def _add_ln(self, y, h, ln):
+        """LN(h + y) (y is scratch and receives h + y)."""
+        import torch
+
+        if y.dtype != torch.bfloat16:
+            return torch.nn.functional.layer_norm(h + y, ln.normalized_shape, ln.weight, ln.bias, ln.eps)
+        out = torch.empty_like(y)
+        d = y.shape[-1]
+        nat.check(nat.load_library().ee_add_layernorm_bf16(
+            y.data_ptr(), h.data_ptr(), ln.weight.data_ptr(), ln.bias.data_ptr(), float(ln.eps),
+            y.numel() // d, d, out.data_ptr(), nat.stream_handle(torch)))
+        return out
+
+    def _linear(self, x, w, b, act=None):
+        import torch
+        import torch.nn.functional as F
+
+        if x.dtype == torch.bfloat16:
+            return gemm(x, w, b, act=act)
+        y = F.linear(x, w, b)
+        return F.gelu(y) if act == "gelu" else y
+
+    def __call__(self, h):
+        import torch
+        import torch.nn.functional as F
+
+        self._prep()
+        h = h.contiguous()
+        B, S, d = h.shape
+        H = self.n_head
+        qkv = self._linear(h, self.wqkv, self.bqkv).view(B, S, 3, H, d // H).permute(2, 0, 3, 1, 4)
+        a = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2])
+        a = a.transpose(1, 2).reshape(B, S, d)
+        x = self._add_ln(self._linear(a, self.wo, self.bo), h, self.ln1)
+        f = self._linear(x, self.w1, self.b1, act="gelu")
+        return self._add_ln(self._linear(f, self.w2, self.b2), x, self.ln2)
 
 
 class _Token0Head:

@@ -42,7 +42,7 @@ import numpy as np
 
 from paper_2312_05385_b200 import _native as nat
 from paper_2312_05385_b200.errors import ParameterError
-from paper_2312_05385_b200.heads import exit_from_logits, linear_tc
+from paper_2312_05385_b200.heads import exit_from_logits, gemm, linear_tc
 
 
 @dataclass(frozen=True)
@@ -89,6 +89,9 @@ class GPT2Decoder:
                 "fc_w": normal(4 * d, d), "fc_b": torch.zeros(4 * d, device="cuda", dtype=bf),
                 "pr_w": normal(d, 4 * d, std=proj_std), "pr_b": torch.zeros(d, device="cuda", dtype=bf),
             })
+        for w in self.layers:  # fp32 bias copies: the GEMM epilogues add them in fp32
+            for k in ("qkv", "o", "fc", "pr"):
+                w[k + "_b32"] = w[k + "_b"].float()
         self.lnf_w = torch.ones(d, device="cuda", dtype=bf)
         self.lnf_b = torch.zeros(d, device="cuda", dtype=bf)
         H, Dh = spec.n_head, spec.head_dim
@@ -140,7 +143,9 @@ class GPT2Decoder:
         add_ln(None, self.layers[l0]["ln1_w"], self.layers[l0]["ln1_b"])
         for l in range(l0, l1):
             w = self.layers[l]
-            qkv = F.linear(x, w["qkv_w"], w["qkv_b"])  # [B, q, 3d] contiguous
+            # projections: tcgen05 GEMMs (csrc/gemm.cu): the swap-AB weight-streaming
+            # kernel for decode / flush passes, the CTA-pair kernel for prompts
+            qkv = gemm(x, w["qkv_w"], w["qkv_b32"])  # [B, q, 3d] contiguous
             # K and V rows straight from the projection into their cache slots (one kernel)
             nat.check(lib.ee_kv_append_bf16(qkv.data_ptr(), wpos.data_ptr(), B, q, H, Dh, T + 1,
                                             self.kv_cache[l].data_ptr(), st))
@@ -153,10 +158,10 @@ class GPT2Decoder:
                 qh = qkv.view(B, q, 3, H, Dh)[:, :, 0].transpose(1, 2)
                 att = F.scaled_dot_product_attention(qh, self.k_cache[l], self.v_cache[l],
                                                      attn_mask=mask).transpose(1, 2).reshape(B, q, d)
-            add_ln(F.linear(att, w["o_w"], w["o_b"]), w["ln2_w"], w["ln2_b"])
-            # bias + tanh-GELU in the GEMM epilogue (cuBLASLt), then the projection
-            t = torch._addmm_activation(w["fc_b"], x.reshape(B * q, d), w["fc_w"].t(), use_gelu=True)
-            y = F.linear(t.view(B, q, -1), w["pr_w"], w["pr_b"])
+            add_ln(gemm(att, w["o_w"], w["o_b32"]), w["ln2_w"], w["ln2_b"])
+            # bias + tanh-GELU in the GEMM epilogue, then the projection
+            t = gemm(x, w["fc_w"], w["fc_b32"], act="gelu_tanh")
+            y = gemm(t, w["pr_w"], w["pr_b32"])
             if l + 1 < l1:
                 add_ln(y, self.layers[l + 1]["ln1_w"], self.layers[l + 1]["ln1_b"])
             else:

@@ -185,23 +185,45 @@ def compact_rows(src, keep, n_keep, out=None):
 
 
 def linear_tc(x, weight, bias=None, *, splits: int = 0, out_bf16: bool = False):
-    """[M, N] = x bf16 [M, K] @ weight bf16 [N, K]^T + bias (fp32, or bf16 with
-    out_bf16), on the 5th-gen tensor cores: TMA-fed, warp-specialized
-    tcgen05.mma with TMEM accumulators (ee_gemm_bf16)."""
+    """[M, N] = x bf16 [M, K] @ weight bf16 [N, K]^T + bias, fp32 out by default
+    (ramp-head logits): `gemm` with no activation."""
+    return gemm(x, weight, bias, out_bf16=out_bf16, splits=splits)
+
+
+ACTS = {None: 0, "none": 0, "gelu": 1, "gelu_tanh": 2, "relu": 3}
+
+
+def gemm(x, weight, bias=None, *, act=None, out_bf16: bool = True, path: int = 0,
+         splits: int = 0, out=None):
+    """act(x bf16 [M, K] @ weight bf16 [N, K]^T + bias) on the tcgen05 kernels of
+    csrc/gemm.cu (ee_gemm_bf16_ex): the persistent CTA-pair kernel for M > 256, the
+    swap-AB weight-streaming kernel (cluster split-K) for M <= 256. `act` is fused
+    into the epilogue ("gelu" = erf form, "gelu_tanh", "relu"). x may have leading
+    batch dimensions; they are flattened into M."""
     torch = nat.torch_cuda()
     if x.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
-        raise ParameterError("linear_tc takes bf16 operands")
-    x, weight = x.contiguous(), weight.contiguous()
-    m, k = x.shape
-    n = weight.shape[0]
+        raise ParameterError("gemm takes bf16 operands")
+    if act not in ACTS:
+        raise ParameterError(f"unknown activation {act!r}")
+    lead = x.shape[:-1]
+    k = x.shape[-1]
+    x2 = x.reshape(-1, k)
+    if not x2.is_contiguous():
+        x2 = x2.contiguous()
+    weight = weight if weight.is_contiguous() else weight.contiguous()
+    m, n = x2.shape[0], weight.shape[0]
     if weight.shape[1] != k:
         raise ParameterError("inner dimensions differ")
-    out = torch.empty((m, n), dtype=torch.bfloat16 if out_bf16 else torch.float32, device="cuda")
-    b = None if bias is None else bias.float().contiguous()
-    nat.check(nat.load_library().ee_gemm_bf16(
-        nat.workspace(), x.data_ptr(), weight.data_ptr(), nat.ptr(b), out.data_ptr(), int(out_bf16),
-        m, n, k, splits, nat.stream_handle(torch)))
-    return out
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.bfloat16 if out_bf16 else torch.float32,
+                          device=x.device)
+    b = None
+    if bias is not None:
+        b = bias if bias.dtype == torch.float32 and bias.is_contiguous() else bias.float().contiguous()
+    nat.check(nat.load_library().ee_gemm_bf16_ex(
+        nat.workspace(), x2.data_ptr(), weight.data_ptr(), nat.ptr(b), out.data_ptr(),
+        int(out_bf16), ACTS[act], m, n, k, splits, path, nat.stream_handle(torch)))
+    return out.view(*lead, n)
 
 
 def pool_bf16(x):

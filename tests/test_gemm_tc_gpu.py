@@ -90,3 +90,99 @@ def test_gemm_bf16_out_and_backbone_shapes(cuda, m, n, k):
     gb = linear_tc(x, w, bias, out_bf16=True)
     assert gb.dtype == torch.bfloat16
     assert torch.allclose(gb.float(), ref, rtol=1e-2, atol=1e-2 * scale)
+
+
+# ---------------------------------------------------------------- csrc/gemm.cu paths
+def _ref_act(y, act):
+    F = torch.nn.functional
+    if act == "gelu":
+        return F.gelu(y)
+    if act == "gelu_tanh":
+        return F.gelu(y, approximate="tanh")
+    if act == "relu":
+        return F.relu(y)
+    return y
+
+
+# (path, m, n, k): 1 = swap-AB split-K (any m: z tiles of 128 rows), 2 / 4 / 3 =
+# persistent CTA pair with 256 x 256 / 192 / 128 tiles. Ragged m, n, k at every
+# tile edge; k spans one to many k-tiles; several persistent tiles per pair.
+PATH_CASES = [
+    (1, 1, 64, 64), (1, 32, 3072, 1024), (1, 33, 130, 200), (1, 100, 1000, 2048),
+    (1, 300, 777, 520), (1, 256, 50257, 256),
+    (2, 257, 256, 64), (2, 1000, 700, 136), (2, 8192, 2304, 768), (2, 2048, 4096, 4096),
+    (4, 600, 776, 1000), (4, 8192, 768, 3072),
+    (3, 777, 136, 72), (3, 4096, 1024, 512),
+]
+
+
+@pytest.mark.parametrize("path,m,n,k", PATH_CASES)
+@pytest.mark.parametrize("out_bf16", [False, True])
+def test_gemm3_paths_match_torch(cuda, path, m, n, k, out_bf16):
+    """Every kernel path against torch fp32 on the same bf16 operands: fp32 out
+    within 1e-3 of the output scale (accumulation order only), bf16 out within
+    one bf16 rounding (2^-8 relative) on top of that."""
+    from paper_2312_05385_b200.heads import gemm
+
+    if path != 1 and (n * (2 if out_bf16 else 4)) % 16:
+        pytest.skip("the pair kernel's TMA store needs 16-byte output rows")
+    g = torch.Generator(device="cuda").manual_seed(m * 31 + n * 7 + k + path)
+    x = torch.randn(m, k, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(n, k, generator=g, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(n, generator=g, device="cuda") * 0.1
+    ref = torch.nn.functional.linear(x.float(), w.float(), bias)
+    scale = ref.abs().max().item()
+    got = gemm(x, w, bias, out_bf16=out_bf16, path=path)
+    assert got.dtype == (torch.bfloat16 if out_bf16 else torch.float32)
+    tol = 1e-3 * scale + (ref.abs() * 2.0 ** -8 if out_bf16 else 0)
+    assert ((got.float() - ref).abs() <= tol).all(), (got.float() - ref).abs().max()
+
+
+@pytest.mark.parametrize("act", ["gelu", "gelu_tanh", "relu"])
+@pytest.mark.parametrize("path,m,n,k", [(1, 32, 4096, 1024), (2, 1024, 3072, 768), (3, 512, 512, 256)])
+def test_gemm3_fused_activation(cuda, act, path, m, n, k):
+    """bias + activation in the epilogue (fp32) == torch's activation of the fp32
+    product, bf16 output within one rounding."""
+    from paper_2312_05385_b200.heads import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(n + k)
+    x = torch.randn(m, k, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(n, k, generator=g, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(n, generator=g, device="cuda") * 0.1
+    ref = _ref_act(torch.nn.functional.linear(x.float(), w.float(), bias), act)
+    got = gemm(x, w, bias, act=act, path=path).float()
+    tol = 1e-3 * ref.abs().max().item() + ref.abs() * 2.0 ** -8
+    assert ((got - ref).abs() <= tol).all(), (got - ref).abs().max()
+
+
+@pytest.mark.parametrize("path,m,n,k,splits", [(1, 64, 1024, 4096, 8), (1, 200, 3072, 1024, 0),
+                                                 (2, 4096, 2304, 768, 0), (4, 8192, 768, 3072, 0)])
+def test_gemm3_deterministic(cuda, path, m, n, k, splits):
+    """Bit-identical across runs: split-K partials are reduced in rank order,
+    the pair kernel has no cross-CTA reduction."""
+    from paper_2312_05385_b200.heads import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(m, k, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(n, k, generator=g, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    r1 = gemm(x, w, None, path=path, splits=splits, out_bf16=False)
+    r2 = gemm(x, w, None, path=path, splits=splits, out_bf16=False)
+    assert torch.equal(r1, r2)
+
+
+def test_gemm3_leading_dims_and_errors(cuda):
+    from paper_2312_05385_b200.errors import ParameterError
+    from paper_2312_05385_b200.heads import gemm
+
+    x = torch.randn(4, 16, 256, device="cuda").to(torch.bfloat16)
+    w = torch.randn(512, 256, device="cuda").to(torch.bfloat16)
+    y = gemm(x, w)
+    assert y.shape == (4, 16, 512)
+    ref = torch.nn.functional.linear(x.float(), w.float())
+    assert torch.allclose(y.float(), ref, rtol=1e-2, atol=1e-2 * ref.abs().max().item())
+    with pytest.raises(ParameterError):
+        gemm(x, w[:, :128])
+    with pytest.raises(ParameterError):
+        gemm(x.float(), w)
+    with pytest.raises(ParameterError):
+        gemm(x, w, act="swish")
