@@ -226,7 +226,13 @@ int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float
  * library GEMMs the reference's models would call. */
 int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
                     void* d_c, int32_t out_bf16, int32_t act, int64_t m, int64_t n, int64_t k,
-                    int32_t splits, int32_t path, void* stream);
+                    int32_t splits, int32_t path, void* d_work, int64_t work_bytes, void* stream);
+/* Bytes of device workspace ee_gemm_bf16_ex needs for this call (split-K
+ * partial tiles of the swap kernel; 0 when none). Pass a buffer at least this
+ * large as d_work, or NULL to let the call take stream-ordered pool memory
+ * (cudaMallocAsync). Negative on a bad shape. */
+int64_t ee_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t splits, int32_t path,
+                               int32_t out_bf16);
 
 /* Global average pool NCHW [b, c, hw] (f32, or bf16 when x_bf16) -> bf16
  * [b, c] (round to nearest even): the A operand of a large ramp head. */

@@ -88,8 +88,10 @@ SIGNATURES = {
     "ee_gemm_bf16_tn": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _vp]),
     "ee_gemm_bf16_ex": (
         ctypes.c_int,
-        [_vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _vp],
+        [_vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _vp,
+         _c_i64, _vp],
     ),
+    "ee_gemm_workspace_size": (_c_i64, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32]),
     "ee_pool_bf16": (ctypes.c_int, [_vp, _c_i32, _c_i64, _c_i32, _c_i32, _vp, _vp]),
     "ee_pool_nhwc_bf16": (ctypes.c_int, [_vp, _c_i32, _c_i64, _c_i32, _c_i32, _vp, _vp]),
     "ee_classify_candidates": (ctypes.c_int, [_vp, _c_i64, _c_i32, _vp, _vp, _vp]),

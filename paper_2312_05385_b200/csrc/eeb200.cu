@@ -2173,18 +2173,29 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
 }  // extern "C"
 // gemm.cu (tcgen05 pair / swap-AB kernels)
 cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, void* c, int out_bf16,
-                            int act, int m, int n, int k, int splits, int path, cudaStream_t st);
+                            int act, int m, int n, int k, int splits, int path, void* work,
+                            size_t work_bytes, cudaStream_t st);
+size_t ee_gemm3_workspace(int m, int n, int k, int splits, int path, int out_bf16);
 extern "C" {
 
 int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
                  void* d_c, int32_t out_bf16, int64_t m, int64_t n, int64_t k, int32_t splits,
                  void* stream) {
-  return ee_gemm_bf16_ex(ws, d_a, d_b, d_bias, d_c, out_bf16, 0, m, n, k, splits, 0, stream);
+  return ee_gemm_bf16_ex(ws, d_a, d_b, d_bias, d_c, out_bf16, 0, m, n, k, splits, 0, nullptr, 0,
+                         stream);
+}
+
+int64_t ee_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t splits, int32_t path,
+                               int32_t out_bf16) {
+  if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff ||
+      path < 0 || path > 4)
+    return fail(EE_ERR_ARG, "bad GEMM shape or path");
+  return (int64_t)ee_gemm3_workspace((int)m, (int)n, (int)k, splits, path, out_bf16);
 }
 
 int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
                     void* d_c, int32_t out_bf16, int32_t act, int64_t m, int64_t n, int64_t k,
-                    int32_t splits, int32_t path, void* stream) {
+                    int32_t splits, int32_t path, void* d_work, int64_t work_bytes, void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
   if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(EE_ERR_ARG, "bad GEMM shape");
@@ -2199,7 +2210,8 @@ int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const fl
   cudaError_t e;
   {
     ProfScope ps(ws, st, "k_gemm3");
-    e = ee_gemm3_launch(d_a, d_w, d_bias, d_c, out_bf16, act, (int)m, (int)n, (int)k, splits, path, st);
+    e = ee_gemm3_launch(d_a, d_w, d_bias, d_c, out_bf16, act, (int)m, (int)n, (int)k, splits, path,
+                        d_work, (size_t)std::max<int64_t>(0, work_bytes), st);
   }
   if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_gemm3: ") + cudaGetErrorString(e));
   return EE_OK;

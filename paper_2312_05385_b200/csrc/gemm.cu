@@ -21,12 +21,13 @@
 //   Weight streaming. The roles of the operands swap: W is the MMA's M side
 //   (128 output features per CTA) and up to 128 activation rows are its N side
 //   (32 / 64 / 128; more rows take more CTAs along z). The K range is split
-//   over a cluster of S CTAs along x. Activation row c is owned by cluster rank
-//   c % S: every CTA pushes its fp32 partial for c straight from TMEM into the
-//   owner's receive slot (DSMEM stores), and after one cluster barrier each
-//   owner sums its S slots in rank order (deterministic), adds the bias,
-//   applies the activation and stores. One launch, no global scratch, no
-//   second reduction kernel.
+//   over a cluster of S CTAs along x: each CTA writes its fp32 partial tile to
+//   an L2-resident workspace slot, one cluster barrier (release/acquire at
+//   cluster scope), then rank s sums activation rows s, s + S, ... over the S
+//   slots in rank order (deterministic), adds the bias, applies the activation
+//   and stores. S = 1 stores straight from the TMEM registers. One launch, no
+//   second reduction kernel. (Pushing the partials through DSMEM stores
+//   measured 3-4x slower end to end: ~0.15 us per column per CTA.)
 //
 // Both: warp 0 = TMA producer (one lane), warp 1 = TMEM allocator + MMA issuer
 // (one lane), warps 2..5 = epilogue (warp w owns TMEM lanes 32*(w%4)..).
@@ -57,12 +58,6 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
-}
-__device__ __forceinline__ void cluster_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
@@ -414,16 +409,12 @@ struct SwapCfg {
   static constexpr int W_BYTES = 128 * BK * 2;
   static constexpr int A_BYTES = NP * BK * 2;
   static constexpr int STAGE = W_BYTES + A_BYTES;
-  // receive buffer: S slots x ceil(NP / S) columns x 128 features (fp32), at
-  // most (NP + 16) x 128 floats; separate from the ring so that peers may push
-  // into it while this CTA's MMAs still read the ring
-  static constexpr int RECV = (NP + 16) * 128 * 4;
   // NP = 32: two CTAs per SM (more weight bytes in flight per SM; one CTA's
   // prologue/epilogue overlaps the other's stream)
   static constexpr int CTAS_PER_SM = NP <= 32 ? 2 : 1;
-  static constexpr int STAGES_MAX = (SMEM_LIMIT / CTAS_PER_SM - 2048 - RECV) / STAGE;
-  static constexpr int STAGES = STAGES_MAX > 6 ? 6 : STAGES_MAX;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + RECV;
+  static constexpr int STAGES_MAX = (SMEM_LIMIT / CTAS_PER_SM - 2048) / STAGE;
+  static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
+  static constexpr int SMEM = 1024 + STAGES * STAGE;
   static constexpr int TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : 128;
 };
 
@@ -431,13 +422,12 @@ template <int NP, int ACT, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
     k_gemm_swap(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const float* __restrict__ bias, void* __restrict__ C, int M, int N, int K,
-                int kt_per) {
+                int kt_per, float* __restrict__ part) {
   using Cfg = SwapCfg<NP>;
   constexpr int ST = Cfg::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const uint32_t recv = smem_u32(smem + ST * Cfg::STAGE);
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], done_bar;
   __shared__ uint32_t tmem_base;
 
@@ -447,10 +437,11 @@ __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
   const int f0 = blockIdx.y * 128;  // output features of this CTA
   const int r0 = blockIdx.z * NP;   // activation rows of this CTA
   const int rows = min(NP, M - r0);
-  const int U = (NP + S - 1) / S;   // max columns (activation rows) per owner
   const int kt_n = (K + BK - 1) / BK;
   const int kt0 = s_rank * kt_per, kt1 = min(kt_n, kt0 + kt_per);
   const int nkt = max(0, kt1 - kt0);
+  // this cluster's S partial tiles [S][NP cols][128 features] in the workspace
+  float* cpart = part ? part + (size_t)(blockIdx.z * gridDim.y + blockIdx.y) * S * NP * 128 : nullptr;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
@@ -467,7 +458,6 @@ __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base;
-  cluster_arrive_relaxed();  // waited on before the first DSMEM access: every peer has started
 
   if (warp == 0) {
     if (lane == 0) {
@@ -496,15 +486,17 @@ __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
       umma_commit<1>(&done_bar);
     }
   } else {
-    // epilogue warps: TMEM lane = feature q*32 + lane, column = activation row.
-    // Column c belongs to owner c % S; this CTA's partial for it is pushed into
-    // the owner's receive slot [s_rank][c / S] (remote shared stores: posted,
-    // 128 B per warp instruction).
+    // epilogue warps: TMEM lane = feature f0 + 32q + lane (fixed per thread),
+    // TMEM column = activation row. S == 1: bias + activation + store straight
+    // from the registers; S > 1: the fp32 partial goes to this rank's slot of
+    // the cluster's workspace tile (lanes on consecutive features: 128-byte
+    // coalesced stores, L2-resident).
     const int q = warp & 3;
     const int feat = q * 32 + lane;
+    const int f = f0 + feat;
+    const float bf = (S == 1 && bias && f < N) ? __ldg(bias + f) : 0.f;
     if (nkt > 0) mbar_wait(&done_bar, 0);
     fence_after();
-    cluster_wait();
 #pragma unroll 1
     for (int c0 = 0; c0 < rows; c0 += 32) {
       uint32_t v[32];
@@ -515,42 +507,74 @@ __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0u;
       }
-      int owner = c0 % S, u = c0 / S;
+      if (S == 1) {
+        if (f < N) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (c0 + j < rows) {
-          uint32_t remote;
-          const uint32_t local = recv + (uint32_t)(((s_rank * U + u) * 128 + feat) * 4);
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(owner));
-          asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(__uint_as_float(v[j]))
-                       : "memory");
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < rows) {
+              const float y = act<ACT>(__uint_as_float(v[j]) + bf);
+              const int64_t o = (int64_t)(r0 + c0 + j) * N + f;
+              if constexpr (OUT_BF16)
+                static_cast<uint16_t*>(C)[o] = (uint16_t)(bf16x2(y, 0.f) & 0xFFFFu);
+              else
+                static_cast<float*>(C)[o] = y;
+            }
         }
-        if (++owner == S) owner = 0, ++u;
+      } else {
+        float* dst = cpart + ((size_t)s_rank * NP + c0) * 128 + feat;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < rows) dst[j * 128] = __uint_as_float(v[j]);
       }
     }
   }
-  if (warp < 2) cluster_wait();
-  fence_before();
-  cluster_sync();  // every partial has landed in its owner's receive buffer
-  // owner s: columns s, s + S, ...: the S partials summed in rank order
-  // (deterministic), bias, activation, store (consecutive threads take
-  // consecutive features: coalesced)
-  {
+  if (S > 1) {
+    // all S partials of this cluster are in L2 (release/acquire at cluster
+    // scope orders the global stores); rank s then reduces activation rows
+    // s, s + S, ... in rank order (deterministic), adds the bias, applies the
+    // activation and stores (consecutive threads: consecutive features)
+    cluster_sync();
+    // float4 groups of 4 features, two groups per thread per round: up to 2 x S
+    // independent 16-byte L2 loads in flight before the first add
     const int mine = (rows - s_rank + S - 1) / S;
-    const float* rb = reinterpret_cast<const float*>(smem + ST * Cfg::STAGE);
-    for (int idx = threadIdx.x; idx < mine * 128; idx += THREADS) {
-      const int u = idx >> 7, feat = idx & 127;
-      const int col = s_rank + u * S;
-      float acc = 0.f;
-      for (int r = 0; r < S; ++r) acc += rb[(r * U + u) * 128 + feat];
-      const int f = f0 + feat;
-      if (f < N) {
-        const float y = act<ACT>(acc + (bias ? __ldg(bias + f) : 0.f));
-        const int64_t o = (int64_t)(r0 + col) * N + f;
-        if constexpr (OUT_BF16)
-          static_cast<uint16_t*>(C)[o] = (uint16_t)(bf16x2(y, 0.f) & 0xFFFFu);
-        else
-          static_cast<float*>(C)[o] = y;
+    const int groups = mine * 32;
+    for (int g0 = threadIdx.x; g0 < groups; g0 += 2 * THREADS) {
+      float4 xs[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int g = g0 + u * THREADS;
+        const int col = s_rank + (g >> 5) * S;
+        const float4* src = reinterpret_cast<const float4*>(cpart + (size_t)col * 128 + (g & 31) * 4);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (g < groups && r < S) xs[u][r] = __ldcg(src + (size_t)r * NP * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int g = g0 + u * THREADS;
+        if (g >= groups) continue;
+        const int col = s_rank + (g >> 5) * S;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < S) {  // rank order: deterministic
+            acc.x += xs[u][r].x;
+            acc.y += xs[u][r].y;
+            acc.z += xs[u][r].z;
+            acc.w += xs[u][r].w;
+          }
+        const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+        const int fb = f0 + (g & 31) * 4;
+        const int64_t o = (int64_t)(r0 + col) * N + fb;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (fb + e >= N) break;
+          const float y = act<ACT>(a4[e] + (bias ? __ldg(bias + fb + e) : 0.f));
+          if constexpr (OUT_BF16)
+            static_cast<uint16_t*>(C)[o + e] = (uint16_t)(bf16x2(y, 0.f) & 0xFFFFu);
+          else
+            static_cast<float*>(C)[o + e] = y;
+        }
       }
     }
   }
@@ -667,9 +691,50 @@ cudaError_t launch_pair(const void* a, const void* w, const float* bias, void* c
   return cudaGetLastError();
 }
 
+// how one call runs (host-side plan; the workspace query uses the same one)
+struct Plan {
+  bool swap = false;
+  int np = 32;       // swap: activation rows per CTA (32 / 64 / 128)
+  int S = 1;         // swap: split count = cluster size
+  int per = 1;       // swap: k-tiles per split
+  int bn = 256;      // pair: tile width
+  size_t work = 0;   // swap with S > 1: fp32 partial tiles
+};
+
+int pick_bn(int m, int n, int pairs);
+
+Plan make_plan(int m, int n, int k, int splits, int path, bool bf) {
+  Plan p;
+  // TMA stores need 16-byte output rows; otherwise (e.g. the 50257-wide LM
+  // head) the swap kernel's plain stores take any shape
+  const bool c_ok = (n * (bf ? 2 : 4)) % 16 == 0;
+  p.swap = path == 1 || (path == 0 && m <= 256) || !c_ok;
+  if (!p.swap) {
+    p.bn = path == 3 ? 128 : path == 2 ? 256 : path == 4 ? 192 : pick_bn(m, n, device_sms() / 2);
+    return p;
+  }
+  p.np = m <= 32 ? 32 : m <= 64 ? 64 : 128;
+  const int zt = (m + p.np - 1) / p.np;
+  const int ft = (n + 127) / 128;
+  const int kt_n = (k + gemm3::BK - 1) / gemm3::BK;
+  int S = splits;
+  if (S <= 0) {  // the largest power of two with <= ~96 CTAs in all, S <= 8 and
+                 // >= 2 k-tiles per split: the measured optimum on B200
+                 // (tools/sweep_swap.py); beyond it the reduction and the
+                 // per-CTA latency chain cost more than the shorter K loop saves
+    S = 1;
+    while (S * 2 * ft * zt <= 96 && S * 2 <= 8 && S * 2 * 2 <= kt_n) S *= 2;
+  }
+  S = std::max(1, std::min({S, 8, kt_n}));  // the reduction keeps <= 8 partials in registers
+  p.per = (kt_n + S - 1) / S;
+  p.S = (kt_n + p.per - 1) / p.per;  // no empty split
+  if (p.S > 1) p.work = (size_t)p.S * ft * zt * p.np * 128 * 4;
+  return p;
+}
+
 template <int NP, int ACT, bool BF>
-cudaError_t launch_swap(const void* a, const void* w, const float* bias, void* c, int m, int n,
-                        int k, int splits, cudaStream_t st) {
+cudaError_t launch_swap(const Plan& p, const void* a, const void* w, const float* bias, void* c,
+                        int m, int n, int k, void* work, cudaStream_t st) {
   using Cfg = gemm3::SwapCfg<NP>;
   auto kern = gemm3::k_gemm_swap<NP, ACT, BF>;
   cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
@@ -678,39 +743,28 @@ cudaError_t launch_swap(const void* a, const void* w, const float* bias, void* c
   if (!make_map(&tw, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, k, gemm3::BK, 128) ||
       !make_map(&ta, a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, k, gemm3::BK, NP))
     return cudaErrorInvalidValue;
-  const int ft = (n + 127) / 128;
-  const int kt_n = (k + gemm3::BK - 1) / gemm3::BK;
-  int S = splits;
-  if (S <= 0) {  // ~96 CTAs in all, S <= 8, >= 2 k-tiles per split: the
-                 // measured optimum on B200 (tools/sweep_swap.py) — beyond it the
-                 // cluster barrier and the per-CTA latency chain dominate
-    S = std::max(1, 96 / (ft * ((m + NP - 1) / NP)));
-    S = std::min({S, 8, std::max(1, kt_n / 2)});
-  }
-  S = std::max(1, std::min({S, 16, kt_n}));
-  const int per = (kt_n + S - 1) / S;
-  S = (kt_n + per - 1) / per;  // no empty split
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(S, ft, (m + NP - 1) / NP);
+  cfg.gridDim = dim3(p.S, (n + 127) / 128, (m + NP - 1) / NP);
   cfg.blockDim = dim3(gemm3::THREADS, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = S;
+  at[0].val.clusterDim.x = p.S;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, c, m, n, k, per);
-}
-
-template <int ACT, bool BF>
-cudaError_t dispatch_swap(const void* a, const void* w, const float* bias, void* c, int m, int n,
-                          int k, int splits, cudaStream_t st) {
-  if (m <= 32) return launch_swap<32, ACT, BF>(a, w, bias, c, m, n, k, splits, st);
-  if (m <= 64) return launch_swap<64, ACT, BF>(a, w, bias, c, m, n, k, splits, st);
-  return launch_swap<128, ACT, BF>(a, w, bias, c, m, n, k, splits, st);  // z tiles of 128 rows
+  if (p.S == 1 || work)
+    return cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, c, m, n, k, p.per, (float*)work);
+  // no caller workspace: stream-ordered pool memory (capturable: inside a CUDA
+  // graph it becomes an allocation node)
+  float* part = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&part), p.work, st);
+  if (e != cudaSuccess) return e;
+  e = cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, c, m, n, k, p.per, part);
+  cudaError_t e2 = cudaFreeAsync(part, st);
+  return e != cudaSuccess ? e : e2;
 }
 
 // 256 x BN tiles: waves x the measured relative cost of one tile of that width
@@ -731,34 +785,41 @@ int pick_bn(int m, int n, int pairs) {
 }
 
 template <int ACT, bool BF>
-cudaError_t dispatch(const void* a, const void* w, const float* bias, void* c, int m, int n, int k,
-                     int splits, int path, cudaStream_t st) {
-  // TMA stores need 16-byte output rows; otherwise (e.g. the 50257-wide LM
-  // head) the swap kernel's plain stores take any shape
-  const bool c_ok = (n * (BF ? 2 : 4)) % 16 == 0;
-  const bool swap = path == 1 || (path == 0 && (m <= 256 || !c_ok)) || !c_ok;
-  if (swap) return dispatch_swap<ACT, BF>(a, w, bias, c, m, n, k, splits, st);
-  const int bn = path == 3 ? 128 : path == 2 ? 256 : path == 4 ? 192 : pick_bn(m, n, device_sms() / 2);
-  if (bn == 256) return launch_pair<256, ACT, BF>(a, w, bias, c, m, n, k, st);
-  if (bn == 192) return launch_pair<192, ACT, BF>(a, w, bias, c, m, n, k, st);
+cudaError_t dispatch(const Plan& p, const void* a, const void* w, const float* bias, void* c, int m,
+                     int n, int k, void* work, cudaStream_t st) {
+  if (p.swap) {
+    if (p.np == 32) return launch_swap<32, ACT, BF>(p, a, w, bias, c, m, n, k, work, st);
+    if (p.np == 64) return launch_swap<64, ACT, BF>(p, a, w, bias, c, m, n, k, work, st);
+    return launch_swap<128, ACT, BF>(p, a, w, bias, c, m, n, k, work, st);  // z tiles of 128 rows
+  }
+  if (p.bn == 256) return launch_pair<256, ACT, BF>(a, w, bias, c, m, n, k, st);
+  if (p.bn == 192) return launch_pair<192, ACT, BF>(a, w, bias, c, m, n, k, st);
   return launch_pair<128, ACT, BF>(a, w, bias, c, m, n, k, st);
 }
 
 }  // namespace
 
-// Internal entry used by ee_gemm_bf16_ex (eeb200.cu). path: 0 auto, 1 swap-AB
-// split-K, 2 / 4 / 3 pair with BN = 256 / 192 / 128 (tests pin each path).
+// Internal entries used by ee_gemm_bf16_ex / ee_gemm_workspace_size
+// (eeb200.cu). path: 0 auto, 1 swap-AB split-K, 2 / 4 / 3 pair with BN =
+// 256 / 192 / 128 (tests pin each path).
+size_t ee_gemm3_workspace(int m, int n, int k, int splits, int path, int out_bf16) {
+  return make_plan(m, n, k, splits, path, out_bf16 != 0).work;
+}
+
 cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, void* c, int out_bf16,
-                            int act, int m, int n, int k, int splits, int path, cudaStream_t st) {
+                            int act, int m, int n, int k, int splits, int path, void* work,
+                            size_t work_bytes, cudaStream_t st) {
+  const Plan p = make_plan(m, n, k, splits, path, out_bf16 != 0);
+  if (work && work_bytes < p.work) return cudaErrorInvalidValue;
   switch (act * 2 + (out_bf16 ? 1 : 0)) {
-    case 0: return dispatch<0, false>(a, w, bias, c, m, n, k, splits, path, st);
-    case 1: return dispatch<0, true>(a, w, bias, c, m, n, k, splits, path, st);
-    case 2: return dispatch<1, false>(a, w, bias, c, m, n, k, splits, path, st);
-    case 3: return dispatch<1, true>(a, w, bias, c, m, n, k, splits, path, st);
-    case 4: return dispatch<2, false>(a, w, bias, c, m, n, k, splits, path, st);
-    case 5: return dispatch<2, true>(a, w, bias, c, m, n, k, splits, path, st);
-    case 6: return dispatch<3, false>(a, w, bias, c, m, n, k, splits, path, st);
-    case 7: return dispatch<3, true>(a, w, bias, c, m, n, k, splits, path, st);
+    case 0: return dispatch<0, false>(p, a, w, bias, c, m, n, k, work, st);
+    case 1: return dispatch<0, true>(p, a, w, bias, c, m, n, k, work, st);
+    case 2: return dispatch<1, false>(p, a, w, bias, c, m, n, k, work, st);
+    case 3: return dispatch<1, true>(p, a, w, bias, c, m, n, k, work, st);
+    case 4: return dispatch<2, false>(p, a, w, bias, c, m, n, k, work, st);
+    case 5: return dispatch<2, true>(p, a, w, bias, c, m, n, k, work, st);
+    case 6: return dispatch<3, false>(p, a, w, bias, c, m, n, k, work, st);
+    case 7: return dispatch<3, true>(p, a, w, bias, c, m, n, k, work, st);
     default: return cudaErrorInvalidValue;
   }
 }

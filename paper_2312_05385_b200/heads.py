@@ -220,10 +220,23 @@ def gemm(x, weight, bias=None, *, act=None, out_bf16: bool = True, path: int = 0
     b = None
     if bias is not None:
         b = bias if bias.dtype == torch.float32 and bias.is_contiguous() else bias.float().contiguous()
-    nat.check(nat.load_library().ee_gemm_bf16_ex(
+    lib = nat.load_library()
+    key = (m, n, k, splits, path, int(out_bf16))
+    wb = _WORK_BYTES.get(key)
+    if wb is None:
+        wb = int(lib.ee_gemm_workspace_size(m, n, k, splits, path, int(out_bf16)))
+        nat.check(min(wb, 0))
+        _WORK_BYTES[key] = wb
+    # split-K partials in torch's stream-ordered (and CUDA-graph-aware) allocator
+    work = torch.empty(wb, dtype=torch.uint8, device=x.device) if wb else None
+    nat.check(lib.ee_gemm_bf16_ex(
         nat.workspace(), x2.data_ptr(), weight.data_ptr(), nat.ptr(b), out.data_ptr(),
-        int(out_bf16), ACTS[act], m, n, k, splits, path, nat.stream_handle(torch)))
+        int(out_bf16), ACTS[act], m, n, k, splits, path, nat.ptr(work), wb,
+        nat.stream_handle(torch)))
     return out.view(*lead, n)
+
+
+_WORK_BYTES: dict = {}
 
 
 def pool_bf16(x):
