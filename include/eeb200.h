@@ -125,6 +125,16 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
                             const double* h_th, int64_t c, int32_t mode, double* h_acc,
                             double* h_sav, int32_t n_threads, void* stream);
 
+/* The counting half of ee_eval_thresholds_host for a sample shard (SURVEY
+ * §8e): the same host staging (bits packed on the CPU, 8r + 4 bytes per sample
+ * over PCIe), then exact int64 per-candidate exit histograms d_hist [c, r+1]
+ * and correct counts d_ok [c] on the device (HIST mode, no finalisation) —
+ * the buffers a rank all-reduces before ee_finalize_hist. Returns once the
+ * host inputs are no longer read. */
+int ee_eval_counts_host(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
+                        int64_t n, int32_t r, const double* h_th, int64_t c, int64_t* d_hist,
+                        int64_t* d_ok, int32_t n_threads, void* stream);
+
 /* Host-side packing of correct_ext f64 [n, r1] into u32 bit rows (bit j =
  * column j) on n_threads threads (<= 0: all cores); EE_ERR_NOT_BINARY if any
  * entry is not exactly 0.0 or 1.0. */
@@ -274,6 +284,15 @@ int ee_decode_attention_bf16(const void* d_qkv, const void* d_kv, const int64_t*
 
 int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
                     const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream);
+
+/* Compaction bookkeeping for the next stage of a compacted batch (capacity cap
+ * rows): d_rows_out[i] = d_rows_in[d_keep[i]] (d_keep[i] if d_rows_in is NULL)
+ * for i < *d_nkeep, else `dummy`; d_alive_out[i] = i < *d_nkeep; *d_n_out =
+ * *d_nkeep when d_n_out is given. Everything stays on the device (no host
+ * round trip), so it can sit inside a CUDA graph. */
+int ee_compact_meta(const int32_t* d_keep, const int32_t* d_nkeep, const int32_t* d_rows_in,
+                    int64_t cap, int32_t dummy, int32_t* d_rows_out, uint8_t* d_alive_out,
+                    int32_t* d_n_out, void* stream);
 
 /* Finalises externally reduced histograms (e.g. after an all-reduce across
  * ranks of per-shard d_hist/d_ok from ee_eval_thresholds in HIST mode):

@@ -65,6 +65,7 @@ SIGNATURES = {
     "ee_gemm_bf16": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i32, _c_i64, _c_i64, _c_i64, _c_i32, _vp]),
     "ee_eval_thresholds_host": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i32, _vp, ctypes.c_double,
                                                 _vp, _c_i64, _c_i32, _vp, _vp, _c_i32, _vp]),
+    "ee_eval_counts_host": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i32, _vp, _c_i64, _vp, _vp, _c_i32, _vp]),
     "ee_pack_correct_host": (ctypes.c_int, [_vp, _c_i64, _c_i32, _vp, _c_i32]),
     "ee_diag_trace": (ctypes.c_int, [_vp, _vp]),
     "ee_l2_flush": (ctypes.c_int, [_vp, _c_i64, _vp]),
@@ -85,6 +86,7 @@ SIGNATURES = {
          _vp, _vp, _vp, _vp, _vp, _vp],
     ),
     "ee_compact_rows": (ctypes.c_int, [_vp, _c_i64, _vp, _vp, _c_i64, _vp, _vp]),
+    "ee_compact_meta": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i32, _vp, _vp, _vp, _vp]),
     "ee_gemm_bf16_tn": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _vp]),
     "ee_gemm_bf16_ex": (
         ctypes.c_int,
@@ -157,6 +159,8 @@ class _Workspace:
         h = _vp()
         check(lib.ee_workspace_create(ctypes.byref(h)))
         self.handle = h
+        if os.environ.get("EEB200_DIAG_VERSION"):  # A/B runs of the diagonal kernels
+            check(lib.ee_workspace_set_diag_version(h, int(os.environ["EEB200_DIAG_VERSION"])))
 
     def __del__(self):  # pragma: no cover - interpreter shutdown ordering
         try:

@@ -1114,6 +1114,9 @@ static cudaError_t launch_diag2(const diag2::Params& p, int64_t n, int upd, cuda
 template <int R>
 static cudaError_t launch_diag3(const diag2::Params& p, int64_t n, bool pair, cudaStream_t st,
                                 ee_workspace* ws) {
+  if (ws->diag_version == 6)  // scan-then-merge, parallel last-ticket finalisation
+    return launch_diag_kernel(diag3::k_diag3<R, 1024, 32, true>, "k_diag3",
+                              diag3::Big::smem_bytes<R>(), p, n, st, ws, 1024);
   if (pair)
     return launch_diag_kernel(diag3::k_diag3<R, 512, 16>, "k_diag3",
                               diag3::Pair::smem_bytes<R>(), p, n, st, ws, 512);
@@ -1172,12 +1175,13 @@ static int eval_diag2(ee_workspace* ws, const double* d_scores, const uint32_t* 
   if ((reinterpret_cast<uintptr_t>(d_scores) & 15) != 0) return 1;
   diag2::Params p{};
   if (!plan_bins(u, &p.a, &p.c0, p.tab)) return 1;
+  constexpr size_t acc_bytes = (size_t)diag2::ACC_WORDS * 8;
   if (!ws->d_diag_acc) {
-    EE_CUDA(cudaMalloc(&ws->d_diag_acc, (size_t)diag2::ACC_WORDS * 8));
+    EE_CUDA(cudaMalloc(&ws->d_diag_acc, acc_bytes));
     ws->diag_acc_dirty = true;
   }
   if (ws->diag_acc_dirty) {
-    EE_CUDA(cudaMemsetAsync(ws->d_diag_acc, 0, (size_t)diag2::ACC_WORDS * 8, st));
+    EE_CUDA(cudaMemsetAsync(ws->d_diag_acc, 0, acc_bytes, st));
     ws->diag_acc_dirty = false;
   }
   p.s = d_scores;
@@ -1814,22 +1818,16 @@ static cudaError_t copy_to_device(ee_workspace* ws, void* dst, const void* src, 
   return cudaSuccess;
 }
 
-int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
-                            int64_t n, int32_t r, const double* h_serve, double vanilla,
-                            const double* h_th, int64_t c, int32_t mode, double* h_acc,
-                            double* h_sav, int32_t n_threads, void* stream) {
-  if (!ws) return fail(EE_ERR_ARG, "null workspace");
-  if (n < 0 || r < 0 || c < 0) return fail(EE_ERR_ARG, "negative shape");
-  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
-  if (c == 0) return EE_OK;
-  if (!h_serve || !h_acc || !h_sav) return fail(EE_ERR_ARG, "null pointer");
-  if (n > 0 && ((!h_scores && r > 0) || !h_correct_ext)) return fail(EE_ERR_ARG, "null inputs");
-  if (r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
-  std::lock_guard<std::mutex> lock(ws->mu);
-  auto st = (cudaStream_t)stream;
+// Host inputs -> device window in the workspace: correct_ext is packed into
+// 4-byte bit rows on worker threads (25x fewer bytes over PCIe) while the
+// scores stream to the device; `extra` bytes of output space follow the bits.
+// Returns with the copies queued on st (the caller synchronises before it
+// hands the host buffers back).
+static int stage_host_window(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
+                             int64_t n, int32_t r, size_t extra, int32_t n_threads, cudaStream_t st,
+                             double** d_scores, uint32_t** d_bits, unsigned char** d_extra) {
   const size_t s_b = align_up((size_t)n * r * 8, 256), b_b = align_up((size_t)n * 4, 256);
-  const size_t o_b = align_up((size_t)c * 8, 256);
-  const size_t need = s_b + b_b + 2 * o_b;
+  const size_t need = s_b + b_b + extra;
   if (need > ws->d_in_cap) {
     if (ws->d_in) EE_CUDA(cudaFree(ws->d_in));
     ws->d_in = nullptr;
@@ -1844,12 +1842,9 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
     ws->h_bits_cap = (size_t)n;
   }
   auto* base = static_cast<unsigned char*>(ws->d_in);
-  double* d_scores = reinterpret_cast<double*>(base);
-  uint32_t* d_bits = reinterpret_cast<uint32_t*>(base + s_b);
-  double* d_acc = reinterpret_cast<double*>(base + s_b + b_b);
-  double* d_sav = reinterpret_cast<double*>(base + s_b + b_b + o_b);
-  // the CPU packs correct_ext into 4-byte bit rows (25x fewer bytes over PCIe)
-  // on worker threads while the scores stream to the device
+  *d_scores = reinterpret_cast<double*>(base);
+  *d_bits = reinterpret_cast<uint32_t*>(base + s_b);
+  *d_extra = base + s_b + b_b;
   int prc = EE_OK;
   std::string perr;
   // leave kStagers cores to the score copy threads when the scores are pageable
@@ -1863,16 +1858,47 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
     if (prc) perr = g_err;  // thread-local
   });
   cudaError_t ce = cudaSuccess;
-  if (n > 0 && r > 0) ce = copy_to_device(ws, d_scores, h_scores, (size_t)n * r * 8, st);
+  if (n > 0 && r > 0) ce = copy_to_device(ws, *d_scores, h_scores, (size_t)n * r * 8, st);
   packer.join();
   if (prc) {
     cudaStreamSynchronize(st);  // the caller's buffers stay in use until the copy is done
     return fail(prc, perr);
   }
   if (ce != cudaSuccess) return fail(EE_ERR_CUDA, std::string("scores H2D: ") + cudaGetErrorString(ce));
-  if (n > 0) EE_CUDA(cudaMemcpyAsync(d_bits, ws->h_bits, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-  int rc = eval_dispatch(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, mode, nullptr,
-                         nullptr, d_acc, d_sav, st);
+  if (n > 0) EE_CUDA(cudaMemcpyAsync(*d_bits, ws->h_bits, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+  return EE_OK;
+}
+
+static int check_host_eval(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
+                           int64_t n, int32_t r, const double* h_th, int64_t c) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (n < 0 || r < 0 || c < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (r > EE_MAX_RAMPS) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (n > 0 && ((!h_scores && r > 0) || !h_correct_ext)) return fail(EE_ERR_ARG, "null inputs");
+  if (c > 0 && r > 0 && !h_th) return fail(EE_ERR_ARG, "null thresholds");
+  return EE_OK;
+}
+
+int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
+                            int64_t n, int32_t r, const double* h_serve, double vanilla,
+                            const double* h_th, int64_t c, int32_t mode, double* h_acc,
+                            double* h_sav, int32_t n_threads, void* stream) {
+  int rc = check_host_eval(ws, h_scores, h_correct_ext, n, r, h_th, c);
+  if (rc) return rc;
+  if (c == 0) return EE_OK;
+  if (!h_serve || !h_acc || !h_sav) return fail(EE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  const size_t o_b = align_up((size_t)c * 8, 256);
+  double* d_scores;
+  uint32_t* d_bits;
+  unsigned char* d_out;
+  rc = stage_host_window(ws, h_scores, h_correct_ext, n, r, 2 * o_b, n_threads, st, &d_scores, &d_bits, &d_out);
+  if (rc) return rc;
+  double* d_acc = reinterpret_cast<double*>(d_out);
+  double* d_sav = reinterpret_cast<double*>(d_out + o_b);
+  rc = eval_dispatch(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, mode, nullptr,
+                     nullptr, d_acc, d_sav, st);
   if (rc) {
     cudaStreamSynchronize(st);
     return rc;
@@ -1880,6 +1906,31 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
   EE_CUDA(cudaMemcpyAsync(h_acc, d_acc, (size_t)c * 8, cudaMemcpyDeviceToHost, st));
   EE_CUDA(cudaMemcpyAsync(h_sav, d_sav, (size_t)c * 8, cudaMemcpyDeviceToHost, st));
   EE_CUDA(cudaStreamSynchronize(st));
+  return EE_OK;
+}
+
+int ee_eval_counts_host(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
+                        int64_t n, int32_t r, const double* h_th, int64_t c, int64_t* d_hist,
+                        int64_t* d_ok, int32_t n_threads, void* stream) {
+  int rc = check_host_eval(ws, h_scores, h_correct_ext, n, r, h_th, c);
+  if (rc) return rc;
+  if (c == 0) return EE_OK;
+  if (!d_hist || !d_ok) return fail(EE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  double* d_scores;
+  uint32_t* d_bits;
+  unsigned char* d_out;
+  rc = stage_host_window(ws, h_scores, h_correct_ext, n, r, 0, n_threads, st, &d_scores, &d_bits, &d_out);
+  if (rc) return rc;
+  // the serve table and vanilla latency only enter the finalisation, which the
+  // caller runs on the reduced counts (ee_finalize_hist)
+  std::vector<double> serve((size_t)r + 1, 0.0);
+  rc = eval_dispatch(ws, d_scores, d_bits, n, r, serve.data(), 0.0, h_th, c, EE_MODE_HIST, d_hist,
+                     d_ok, nullptr, nullptr, st);
+  cudaError_t e = cudaStreamSynchronize(st);  // host inputs are the caller's again
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("counts: ") + cudaGetErrorString(e));
   return EE_OK;
 }
 
@@ -1945,7 +1996,7 @@ int ee_workspace_set_special(ee_workspace* ws, int32_t on) {
 
 int ee_workspace_set_diag_version(ee_workspace* ws, int32_t version) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
-  if (version < 1 || version > 5) return fail(EE_ERR_ARG, "diagonal kernel version must be 1..5");
+  if (version < 1 || version > 6) return fail(EE_ERR_ARG, "diagonal kernel version must be 1..6");
   std::lock_guard<std::mutex> lock(ws->mu);
   ws->diag_version = version;
   return EE_OK;
@@ -2113,15 +2164,33 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
   if (rc) return rc;
   const size_t smem = (size_t)(c + k) * 4;
   if (smem > 200 * 1024) return fail(EE_ERR_ARG, "too many channels for the fused head");
+  // S CTAs (one thread-block cluster) per row, ~8 KB of the map each, at most 8
+  // (the portable cluster size); S depends on the row shape only
+  const int64_t row_bytes = (int64_t)c * hw * (feat_bf16 ? 2 : 4);
+  int S = 1;
+  while (S < 8 && S * 2 <= hw && row_bytes >= (int64_t)S * 2 * 8192) S *= 2;
+  if ((int64_t)b * S > 0x7fffffff) S = 1;
   ProfScope ps(ws, st, "k_exit_fused");
 #define EE_EXITK(TF, TW)                                                                       \
   do {                                                                                         \
     auto kern = exitc::k_exit_fused<TF, TW>;                                                   \
     if (smem > 48 * 1024)                                                                      \
       EE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kern<<<(unsigned)b, exitc::THREADS, smem, st>>>(static_cast<const TF*>(d_feat), b, c, hw,   \
-                                                     nhwc, static_cast<const TW*>(d_w), d_bias, k, \
-                                                     conf, threshold, d_threshold, d_alive, o); \
+    cudaLaunchConfig_t cfg{};                                                                  \
+    cfg.gridDim = dim3((unsigned)(b * S));                                                     \
+    cfg.blockDim = dim3(exitc::THREADS);                                                       \
+    cfg.dynamicSmemBytes = smem;                                                               \
+    cfg.stream = st;                                                                           \
+    cudaLaunchAttribute attr[1];                                                               \
+    attr[0].id = cudaLaunchAttributeClusterDimension;                                          \
+    attr[0].val.clusterDim.x = (unsigned)S;                                                    \
+    attr[0].val.clusterDim.y = 1;                                                              \
+    attr[0].val.clusterDim.z = 1;                                                              \
+    cfg.attrs = attr;                                                                          \
+    cfg.numAttrs = 1;                                                                          \
+    EE_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const TF*>(d_feat), b, c, hw, nhwc,     \
+                               static_cast<const TW*>(d_w), d_bias, k, conf, threshold,        \
+                               d_threshold, d_alive, o, S));                                   \
   } while (0)
   if (feat_bf16 && w_bf16)
     EE_EXITK(uint16_t, uint16_t);
@@ -2533,6 +2602,18 @@ int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
   exitc::k_compact_rows<<<(unsigned)blocks, 256, 0, st>>>(
       static_cast<const uint8_t*>(d_src), row_bytes, d_keep, d_nkeep,
       static_cast<uint8_t*>(d_dst));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_compact_meta(const int32_t* d_keep, const int32_t* d_nkeep, const int32_t* d_rows_in,
+                    int64_t cap, int32_t dummy, int32_t* d_rows_out, uint8_t* d_alive_out,
+                    int32_t* d_n_out, void* stream) {
+  if (!d_keep || !d_nkeep || !d_rows_out || !d_alive_out) return fail(EE_ERR_ARG, "null pointer");
+  if (cap < 1) return EE_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(cap, 256), 64);
+  exitc::k_compact_meta<<<blocks, 256, 0, (cudaStream_t)stream>>>(d_keep, d_nkeep, d_rows_in, cap, dummy,
+                                                                   d_rows_out, d_alive_out, d_n_out);
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

@@ -20,7 +20,11 @@
 // runs the same epilogue.
 #pragma once
 
+#include <cooperative_groups.h>
+
 namespace exitc {
+
+namespace cg = cooperative_groups;
 
 constexpr int THREADS = 256;
 constexpr int MAXK_FUSED = 256;
@@ -146,40 +150,50 @@ __device__ __forceinline__ void scatter_row(const Out& o, int64_t row, int32_t l
   o.slot_site[s] = o.site;
 }
 
-__device__ __forceinline__ bool last_cta(unsigned* done) {
+// `arrivals` CTAs count in (default: the whole grid; the clustered head: one per row)
+__device__ __forceinline__ bool last_cta(unsigned* done, unsigned arrivals = 0u) {
   __shared__ bool last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == (arrivals ? arrivals : gridDim.x) - 1;
   __syncthreads();
   if (last) __threadfence();
   return last;
 }
 
-// pool + FC + confidence + compare for one row per CTA, K <= MAXK_FUSED
+// pool + FC + confidence + compare for one row per CLUSTER of S CTAs, K <= MAXK_FUSED.
+// The row's HW positions are split into S contiguous slices, one per CTA of the
+// cluster, so a large map (a CIFAR stem: 64 x 32 x 32 bf16 = 128 KB per row) is
+// read by S SMs at once instead of one; each CTA leaves its slice's channel
+// sums in its own shared memory and the cluster's rank 0 adds them over DSMEM
+// in rank order (deterministic, and independent of the batch size since S
+// depends on the row shape only), then runs the FC / confidence / compare.
 template <typename TF, typename TW>
 __global__ void __launch_bounds__(THREADS)
     k_exit_fused(const TF* __restrict__ feat, int64_t B, int C, int HW, int nhwc,
                  const TW* __restrict__ W, const float* __restrict__ bias, int K, int conf,
                  double threshold, const double* __restrict__ d_threshold,
-                 uint8_t* __restrict__ alive_in, Out o) {
+                 uint8_t* __restrict__ alive_in, Out o, int S) {
   if (d_threshold) threshold = *d_threshold;
   extern __shared__ float sh[];  // pooled[C], logits[K]
   float* pooled = sh;
   float* logits = sh + C;
-  const int64_t row = blockIdx.x;
+  const int64_t row = blockIdx.x / S;
+  const int rank = (int)(blockIdx.x % S);
+  const int p_begin = (int)((int64_t)HW * rank / S), p_end = (int)((int64_t)HW * (rank + 1) / S);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const float inv = 1.f / (float)HW;
   if ((nhwc || HW == 1) && C % 4 == 0 && C <= 4 * THREADS &&
       (reinterpret_cast<uintptr_t>(feat) & (4 * sizeof(TF) - 1)) == 0) {
     // channels contiguous: a thread owns 4 channels (one 8/16-byte load per
-    // position) and the CTA's threads split the positions into THREADS / (C/4)
-    // slices, so every thread keeps loads in flight; slices meet in shared memory
+    // position) and the CTA's threads split the slice's positions into
+    // THREADS / (C/4) sub-slices, so every thread keeps loads in flight;
+    // sub-slices meet in shared memory
     __shared__ float4 part[THREADS];
-    const int G = C / 4, S = THREADS / G;
+    const int G = C / 4, SS = THREADS / G;
     const int g = threadIdx.x % G, sl = threadIdx.x / G;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (sl < S) {
+    if (sl < SS) {
       const TF* base = feat + row * (int64_t)HW * C + 4 * g;
       using V = typename std::conditional<sizeof(TF) == 2, uint2, float4>::type;
       auto add = [&](const V& v) {
@@ -193,34 +207,34 @@ __global__ void __launch_bounds__(THREADS)
         }
       };
       constexpr int DEPTH = 8;  // loads issued before any is consumed
-      int p = sl;
-      for (; p + (DEPTH - 1) * S < HW; p += DEPTH * S) {
+      int p = p_begin + sl;
+      for (; p + (DEPTH - 1) * SS < p_end; p += DEPTH * SS) {
         V v[DEPTH];
 #pragma unroll
-        for (int i = 0; i < DEPTH; ++i) v[i] = __ldg(reinterpret_cast<const V*>(base + (int64_t)(p + i * S) * C));
+        for (int i = 0; i < DEPTH; ++i) v[i] = __ldg(reinterpret_cast<const V*>(base + (int64_t)(p + i * SS) * C));
 #pragma unroll
         for (int i = 0; i < DEPTH; ++i) add(v[i]);
       }
-      for (; p < HW; p += S) add(__ldg(reinterpret_cast<const V*>(base + (int64_t)p * C)));
+      for (; p < p_end; p += SS) add(__ldg(reinterpret_cast<const V*>(base + (int64_t)p * C)));
     }
     part[threadIdx.x] = acc;
     __syncthreads();
     for (int c = threadIdx.x; c < C; c += THREADS) {
       const int gc = c / 4, k = c % 4;
       float t = 0.f;
-      for (int q = 0; q < S; ++q) {
+      for (int q = 0; q < SS; ++q) {
         const float4 v = part[q * G + gc];
         t += k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
       }
-      pooled[c] = t * inv;
+      pooled[c] = t;
     }
   } else if (nhwc || HW == 1) {
     // channels contiguous: threads over channels, loop over positions
     const TF* base = feat + row * (int64_t)HW * C;
     for (int c = threadIdx.x; c < C; c += THREADS) {
       float acc = 0.f;
-      for (int p = 0; p < HW; ++p) acc += ld_f32(base, (int64_t)p * C + c);
-      pooled[c] = acc * inv;
+      for (int p = p_begin; p < p_end; ++p) acc += ld_f32(base, (int64_t)p * C + c);
+      pooled[c] = acc;
     }
   } else if (HW <= 64) {
     // NCHW, small planes (late CNN stages, 4x4 .. 8x8): a thread per channel,
@@ -228,18 +242,33 @@ __global__ void __launch_bounds__(THREADS)
     const TF* base = feat + row * (int64_t)C * HW;
     for (int c = threadIdx.x; c < C; c += THREADS) {
       float acc = 0.f;
-      for (int p = 0; p < HW; ++p) acc += ld_f32(base, (int64_t)c * HW + p);
-      pooled[c] = acc * inv;
+      for (int p = p_begin; p < p_end; ++p) acc += ld_f32(base, (int64_t)c * HW + p);
+      pooled[c] = acc;
     }
   } else {
-    // NCHW: one warp per channel, lanes over the contiguous HW plane
+    // NCHW: one warp per channel, lanes over the contiguous slice of the plane
     const TF* base = feat + row * (int64_t)C * HW;
     for (int c = wid; c < C; c += THREADS / 32) {
       float acc = 0.f;
-      for (int p = lane; p < HW; p += 32) acc += ld_f32(base, (int64_t)c * HW + p);
+      for (int p = p_begin + lane; p < p_end; p += 32) acc += ld_f32(base, (int64_t)c * HW + p);
       acc = warp_sum(acc);
-      if (lane == 0) pooled[c] = acc * inv;
+      if (lane == 0) pooled[c] = acc;
     }
+  }
+  if (S > 1) {
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();  // every slice's sums are in its CTA's shared memory
+    if (rank == 0) {
+      for (int c = threadIdx.x; c < C; c += THREADS) {
+        float t = pooled[c];
+        for (int q = 1; q < S; ++q) t += cluster.map_shared_rank(pooled, q)[c];
+        pooled[c] = t * inv;
+      }
+    }
+    cluster.sync();  // the other ranks' shared memory stays alive until read
+    if (rank != 0) return;
+  } else {
+    for (int c = threadIdx.x; c < C; c += THREADS) pooled[c] *= inv;
   }
   __syncthreads();
   // logits: one warp per output class, lanes over channels
@@ -266,7 +295,7 @@ __global__ void __launch_bounds__(THREADS)
       if (ex) scatter_row(o, row, label, err);
     }
   }
-  if (o.keep && last_cta(o.done)) compact_and_scatter(B, alive_in, o);
+  if (o.keep && last_cta(o.done, (unsigned)B)) compact_and_scatter(B, alive_in, o);
 }
 
 // confidence() with the row held in registers (NPL values per lane, K <= 32
@@ -435,6 +464,22 @@ __global__ void k_compact_rows(const uint8_t* __restrict__ src, int64_t row_byte
     const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)keep[r] * row_bytes);
     uint4* d = reinterpret_cast<uint4*>(dst + r * row_bytes);
     for (int64_t q = threadIdx.x; q < row_bytes / 16; q += blockDim.x) d[q] = __ldg(s + q);
+  }
+}
+
+// the survivors' bookkeeping for the next compacted stage (capacity cap rows):
+// request slot of each dense row (dummy past n_keep), its alive byte, and a
+// persistent copy of n_keep the host reads
+__global__ void k_compact_meta(const int32_t* __restrict__ keep, const int32_t* __restrict__ n_keep,
+                               const int32_t* __restrict__ rows_in, int64_t cap, int32_t dummy,
+                               int32_t* __restrict__ rows_out, uint8_t* __restrict__ alive_out,
+                               int32_t* __restrict__ n_out) {
+  const int64_t nk = *n_keep;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool live = i < nk;
+    rows_out[i] = live ? (rows_in ? rows_in[keep[i]] : keep[i]) : dummy;
+    alive_out[i] = live ? 1 : 0;
+    if (i == 0 && n_out) *n_out = (int32_t)nk;
   }
 }
 

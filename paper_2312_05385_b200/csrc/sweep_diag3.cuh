@@ -171,7 +171,100 @@ __device__ void finalize_window(const Params& P, unsigned char* scratch, long lo
   }
 }
 
-template <int R, int NT, int CP>
+// Finalise one window whose accumulator already holds PREFIX sums over positions
+// (k_diag3<DIST>: every CTA scanned its own counts before merging, and the scan
+// is linear): gD[j][p] = F_j(p), gD[R][p] = O(p). One thread per position turns
+// its column into the histogram, the correct count and the k_finalize TwoSum
+// chain in registers (the operations of finalize_window, in the same order, so
+// the same bits); the accumulator is read once and left zeroed.
+template <int R, int THREADS>
+__device__ void finalize_prefixed(const Params& P, unsigned char* scratch, long long* gD, int64_t n) {
+  const int tid = threadIdx.x;
+  const int m = P.m;
+  const int M1 = m + 1;
+  long long* hst = reinterpret_cast<long long*>(scratch);  // [R+1][M1]: F_j, then histograms
+  long long* okp = hst + (R + 1) * M1;
+  double* accp = reinterpret_cast<double*>(okp + M1);
+  double* savp = accp + M1;
+  __shared__ long long s_corr_all;
+  if (tid == THREADS - 1) {
+    s_corr_all = (long long)__ldcg(gD + diag2::CORR_IDX);
+    gD[diag2::CORR_IDX] = 0;
+  }
+  for (int q = tid; q < (R + 1) * m; q += THREADS) {
+    const int j = q / m, p = q - j * m;
+    hst[j * M1 + p] = __ldcg(gD + j * diag2::W + p);
+    gD[j * diag2::W + p] = 0;
+  }
+  __syncthreads();
+  const long long corrR = s_corr_all;
+  for (int p = tid; p < M1; p += THREADS) {
+    long long h[R + 1];
+    long long ok;
+    if (p == m) {  // NaN threshold row: nothing exits
+#pragma unroll
+      for (int j = 0; j < R; ++j) h[j] = 0;
+      h[R] = n;
+      ok = corrR;
+    } else {
+      ok = corrR + hst[R * M1 + p];
+      long long fprev = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const long long f = hst[j * M1 + p];
+        h[j] = f - fprev;
+        fprev = f;
+      }
+      h[R] = n - fprev;
+    }
+    double hi = 0.0, lo = 0.0;
+#pragma unroll
+    for (int site = 0; site <= R; ++site) {
+      const double x = (double)h[site];
+      const double pr = __dmul_rn(x, P.serve[site]);
+      const double pe = __fma_rn(x, P.serve[site], -pr);
+      double s2, e;
+      two_sum(hi, pr, s2, e);
+      hi = s2;
+      lo = __dadd_rn(lo, __dadd_rn(e, pe));
+      hst[site * M1 + p] = h[site];
+    }
+    double tot2, e;
+    two_sum(hi, lo, tot2, e);
+    const double dn = (double)n;
+    okp[p] = ok;
+    accp[p] = __ddiv_rn((double)ok, dn);
+    savp[p] = __dsub_rn(P.vanilla, __ddiv_rn(tot2, dn));
+  }
+  __syncthreads();
+  auto posof = [&](int64_t c) -> int {
+    const int q = P.C <= diag2::MAX_POS ? P.pos[c] : P.pos_dev[c];
+    return q == 255 ? m : q;
+  };
+  if (P.hist)
+    for (int64_t i = tid; i < P.C * (R + 1); i += THREADS) {
+      const int64_t c = i / (R + 1);
+      const int site = (int)(i - c * (R + 1));
+      P.hist[i] = hst[site * M1 + posof(c)];
+    }
+  for (int64_t c = tid; c < P.C; c += THREADS) {
+    const int p = posof(c);
+    if (P.ok) P.ok[c] = okp[p];
+    if (P.acc) {
+      P.acc[c] = accp[p];
+      P.sav[c] = savp[p];
+    }
+  }
+}
+
+// DIST = false: the CTA elected first-to-finish-streaming last waits for every
+// other CTA's merge, then finalises the whole window (finalize_window: scan,
+// histograms, products, chain in separate block-wide phases).
+// DIST = true: each CTA folds its lane copies with 16-byte reads, scans its own
+// counts over positions, merges the prefix sums and takes a ticket; the last
+// ticket finalises with one thread per position (finalize_prefixed). Nobody
+// waits on anybody: the tail is fold + scan + merge + one parallel finalise.
+template <int R, int NT, int CP, bool DIST = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_diag3(const __grid_constant__ Params P) {
   using C = Cfg<NT, CP>;
   constexpr int THREADS = C::THREADS, WARPS = C::WARPS, ROWC = C::ROWC;
@@ -344,28 +437,84 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_diag3(const __grid_constant__
   __syncthreads();
   // Elect the last CTA now; the round trip overlaps the fold below (the last
   // thread has no cell to fold unless R * m = 1024).
-  if (tid == THREADS - 1) s_last = atomicAdd(P.done, 1u) == gridDim.x - 1;
+  if constexpr (!DIST)
+    if (tid == THREADS - 1) s_last = atomicAdd(P.done, 1u) == gridDim.x - 1;
   if (lane == 0 && corr) atomicAdd(&s_corr, (unsigned long long)corr);
 
-  // ---- per-CTA sums: fold the 32 lane copies of each cell (rotated so a warp's
-  // reads hit 32 distinct banks). F stays per ramp; O is summed over ramps. The
-  // prefix over positions is linear, so only the last CTA takes it, on totals.
+  // ---- per-CTA sums: fold the lane copies of each cell. F stays per ramp; O is
+  // summed over ramps.
   int* cF = reinterpret_cast<int*>(skey);  // F [R][MAX_M] raw per-position counts
-  for (int q = tid; q < R * m; q += THREADS) {
-    const int j = q / m, p = q - j * m;
-    const uint32_t* cell = cells + (j * CELLS + p) * CP;
-    int lo = 0, hi = 0;
-#pragma unroll 8
-    for (int k = 0; k < CP; ++k) {
-      const uint32_t w = cell[(k + lane) % CP];
-      lo += (int)(w & 0xffffu);
-      hi += (int)(short)(w >> 16);  // each copy's high half is its exact signed sum mod 2^16
+  {
+    // 16-byte reads of 4 copies at a time, the chunk order rotated by thread so
+    // the CP / 4 threads of a group cover all 32 banks (4 wavefronts per warp
+    // read, the minimum for 512 bytes) with a dependent chain of CP / 4 loads.
+    // Under DIST the prefix over positions follows per CTA; otherwise it is
+    // linear, so only the last CTA takes it, on totals.
+    constexpr int NQ = CP / 4;
+    for (int q = tid; q < R * m; q += THREADS) {
+      const int j = q / m, p = q - j * m;
+      const uint4* cell = reinterpret_cast<const uint4*>(cells + (j * CELLS + p) * CP);
+      int lo = 0, hi = 0;
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const uint4 w = cell[(k + tid) % NQ];
+        lo += (int)(w.x & 0xffffu) + (int)(w.y & 0xffffu) + (int)(w.z & 0xffffu) + (int)(w.w & 0xffffu);
+        // each copy's high half is its exact signed sum mod 2^16
+        hi += (int)(short)(w.x >> 16) + (int)(short)(w.y >> 16) + (int)(short)(w.z >> 16) +
+              (int)(short)(w.w >> 16);
+      }
+      cF[j * MAX_M + p] = lo;
+      if (hi) atomicAdd(&s_osum[p], hi);
     }
-    cF[j * MAX_M + p] = lo;
-    if (hi) atomicAdd(&s_osum[p], hi);
   }
   __syncthreads();
   if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 3] = diag2::gtimer();
+  if constexpr (DIST) {
+    // this CTA's inclusive prefix over positions (warp j < R: row j, warp R: O)
+    if (warp <= R) {
+      int* a = warp < R ? cF + warp * MAX_M : s_osum;
+      int carry = 0;
+      for (int p0 = 0; p0 < m; p0 += 32) {
+        const int p = p0 + lane;
+        int x = p < m ? a[p] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, x, o);
+          if (lane >= o) x += y;
+        }
+        x += carry;
+        if (p < m) a[p] = x;
+        carry = __shfl_sync(FULL, x, 31);
+      }
+    }
+    __syncthreads();
+    long long* gD = P.gD;
+    for (int q = tid; q < (R + 1) * m; q += THREADS) {
+      const int j = q / m, p = q - j * m;
+      const long long x = j < R ? (long long)cF[j * MAX_M + p] : (long long)s_osum[p];
+      if (x) atomicAdd(reinterpret_cast<unsigned long long*>(gD + j * diag2::W + p), (unsigned long long)x);
+    }
+    if (tid == 0 && s_corr)
+      atomicAdd(reinterpret_cast<unsigned long long*>(gD + diag2::CORR_IDX), s_corr);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    __syncthreads();
+    if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 5] = diag2::gtimer();
+    if (tid == 0) {
+      unsigned t;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(P.done) : "memory");
+      s_last = t == gridDim.x - 1;
+      if (s_last) P.done[0] = 0u;  // the next launch counts after its griddepcontrol.wait
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (P.trace && tid == 0) P.trace[blockIdx.x * 6 + 1] = diag2::gtimer();
+    finalize_prefixed<R, THREADS>(P, sm + OFF_C, gD, n);
+    if (P.trace) {
+      __syncthreads();
+      if (tid == 0) P.trace[blockIdx.x * 6 + 4] = diag2::gtimer();
+    }
+    return;
+  }
   long long* gD = P.gD;  // [j * W + p]: F_j[p] for j < R, row R: sum_j O_j[p] (two's complement)
   if (!s_last) {
     for (int q = tid; q < (R + 1) * m; q += THREADS) {

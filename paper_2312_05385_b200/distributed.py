@@ -156,20 +156,30 @@ def eval_thresholds_host_sharded(scores, correct_ext, serve, vanilla, thresholds
     serve = np.ascontiguousarray(serve, dtype=np.float64)
     n, r = scores.shape
     c = th.shape[0]
-    d_s = kernels._to_device(torch, scores)
-    bits, flag = kernels.pack_correct(correct_ext, torch)
+    if tuple(correct_ext.shape) != (n, r + 1) or serve.shape != (r + 1,) or th.ndim != 2 or th.shape[1] != r:
+        raise ParameterError("shard shapes disagree: scores (n, r), correct_ext (n, r+1), serve (r+1,), th (c, r)")
     hist = torch.empty((c, r + 1), dtype=torch.int64, device="cuda")
     ok = torch.empty(c, dtype=torch.int64, device="cuda")
     acc = torch.empty(c, dtype=torch.float64, device="cuda")
     sav = torch.empty(c, dtype=torch.float64, device="cuda")
     st = nat.stream_handle(torch)
-    nat.check(lib.ee_eval_thresholds(nat.workspace(), nat.ptr(d_s), nat.ptr(bits), n, r,
-                                     serve.ctypes.data, float(vanilla), th.ctypes.data, c,
-                                     nat.MODE_HIST, hist.data_ptr(), ok.data_ptr(), None, None, st))
+    # correct_ext packed to bit rows on the host cores while the scores stream
+    # (8r + 4 bytes per sample over PCIe, as the 1-GPU host path); a non-binary
+    # entry raises ValueError (EE_ERR_NOT_BINARY) before any exchange
+    bad = None
+    try:
+        nat.check(lib.ee_eval_counts_host(
+            nat.workspace(), scores.ctypes.data if scores.size else None,
+            correct_ext.ctypes.data if correct_ext.size else None, n, r,
+            th.ctypes.data if th.size else None, c, hist.data_ptr(), ok.data_ptr(), 0, st))
+    except ValueError as e:  # still take part in the exchange: the other ranks wait on it
+        bad = e
+        hist.zero_()
+        ok.zero_()
     hist, ok = reduce_counts(hist, ok, group)
     nat.check(lib.ee_finalize_hist(nat.workspace(), hist.data_ptr(), ok.data_ptr(), c, r, n_total,
                                    serve.ctypes.data, float(vanilla), acc.data_ptr(),
                                    sav.data_ptr(), st))
-    if int(flag.item()):
-        raise ValueError("correct_ext must contain only 0.0 and 1.0")
+    if bad is not None:
+        raise bad
     return acc.cpu().numpy(), sav.cpu().numpy()

@@ -30,7 +30,8 @@ import numpy as np
 
 from paper_2312_05385_b200 import _native as nat
 from paper_2312_05385_b200.errors import ParameterError
-from paper_2312_05385_b200.heads import ExitController, LargeRampHead, SlotTable, exit_from_logits, gemm
+from paper_2312_05385_b200.heads import (ExitController, LargeRampHead, SlotTable, compact_meta, compact_rows,
+                                        exit_from_logits, gemm)
 
 # North star: a sample whose confidence lies within 1e-5 of a threshold is a
 # near-tie — its exit decision may legitimately differ from an fp64 CPU oracle,
@@ -96,6 +97,9 @@ class EEPipeline:
     stages: list
     ramps: dict
     site_names: list = field(default_factory=list)
+    # feedback mode: ramp heads run on a side stream, overlapped with the next
+    # stages (they feed nothing downstream but each other, in ramp order)
+    overlap_ramps: bool = True
 
     def __post_init__(self):
         self.ramp_order = sorted(self.ramps)
@@ -112,6 +116,10 @@ class EEPipeline:
         """Capture one feedback-mode batch into a CUDA graph (static shapes; the
         thresholds live in device memory, so retuning needs no re-capture)."""
         return GraphRunner(self, example, thresholds)
+
+    def capture_compact(self, example, thresholds) -> "CompactRunner":
+        """Compaction mode as CUDA graphs, one per (segment, batch bucket)."""
+        return CompactRunner(self, example, thresholds)
 
     def run(self, x, thresholds, *, mode: str = "feedback",
             timed: bool = False) -> BatchResult:
@@ -147,6 +155,18 @@ class EEPipeline:
         if timed:
             start = torch.cuda.Event(enable_timing=True)
             start.record()
+        main = torch.cuda.current_stream()
+        side = None
+        if mode == "feedback" and self.overlap_ramps and R:
+            # The ramp heads form their own chain on a side stream (ramp j reads
+            # the alive mask ramp j - 1 wrote), each forked off the main stream
+            # right after its stage, so a head's pooling / FC / compare runs
+            # while the backbone moves on; joined before the final classifier.
+            # Stage outputs a head still reads are held until the join (the
+            # caching allocator must not hand them to a later stage).
+            side = self._side_stream(torch)
+            side.wait_stream(main)
+        held = []
         h = x
         r = 0
         with torch.no_grad():
@@ -158,6 +178,18 @@ class EEPipeline:
                 if head is None:
                     continue
                 th = thresholds[r] if dev_th else float(thresholds[r])
+                if side is not None:
+                    side.wait_stream(main)
+                    held.append(h)
+                    with torch.cuda.stream(side):
+                        head(h, th, alive=alive, slot=rows, slots=slots,
+                             out_err=ramp_err[r], out_label=ramp_label[r], compact=False)
+                        if timed:
+                            ev = torch.cuda.Event(enable_timing=True)
+                            ev.record()
+                            marks.append(ev)
+                    r += 1
+                    continue
                 if mode == "feedback":  # rows are the identity: write signals in place
                     res = head(h, th, alive=alive, slot=rows, slots=slots,
                                out_err=ramp_err[r], out_label=ramp_label[r], compact=False)
@@ -170,17 +202,24 @@ class EEPipeline:
                     ev.record()
                     marks.append(ev)
                 if mode == "compact":
-                    keep = res.survivors().long()  # host sync: the next stage's batch size
-                    h = h.index_select(0, keep)
-                    rows = rows.index_select(0, keep)
-                    alive = torch.ones(keep.numel(), dtype=torch.uint8, device=dev)
+                    n = int(res.n_keep.item())  # host sync: the next stage's batch size
+                    # gather in the activation's own memory format (index_select
+                    # would turn a channels_last map into NCHW for every later conv)
+                    h = compact_rows(h, res.keep, res.n_keep)[:n]
+                    rows = rows.index_select(0, res.keep[:n].long())
+                    alive = torch.ones(n, dtype=torch.uint8, device=dev)
                 r += 1
             if h.shape[0]:
                 logits = self.stages[-1](h).float()
+                if side is not None:  # join: every ramp has decided
+                    main.wait_stream(side)
+                    held.clear()
                 final_label.index_copy_(0, rows.long(), torch.argmax(logits, dim=1).to(torch.int32))
                 # every still-alive row is released with the final model's label
                 exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=R, alive=alive,
                                  slot=rows, slots=slots, compact=(mode != "feedback"))
+        if side is not None:
+            main.wait_stream(side)
         out = BatchResult(slots.label, slots.site, slots.err, ramp_err, ramp_label, final_label,
                           thresholds=th_record)
         if timed:
@@ -192,6 +231,14 @@ class EEPipeline:
             out.release_ms = np.asarray(t)[np.clip(site, 0, R)]
             out.batch_ms = t[-1]
         return out
+
+
+    def _side_stream(self, torch):
+        s = self.__dict__.get("_side")
+        if s is None or s.device != torch.device("cuda", torch.cuda.current_device()):
+            s = torch.cuda.Stream()
+            self.__dict__["_side"] = s
+        return s
 
 
 class GraphRunner:
@@ -221,6 +268,132 @@ class GraphRunner:
         if x is not None:
             self.x.copy_(x)
         self.graph.replay()
+        return self.out
+
+
+class CompactRunner:
+    """Compaction mode (north star (2): downstream blocks run only on the rows
+    that have not exited) without per-stage host work.
+
+    The pipeline is cut into segments, each ending at a ramp (the last one at
+    the final classifier). A segment runs at a power-of-two batch bucket >= its
+    live row count, as a CUDA graph captured once per (segment, bucket):
+    stages -> ramp head / exit controller (compaction on) -> scatter of the
+    exiting rows -> gather of the survivors' activations, request slots and
+    alive bytes into the next segment's fixed input buffers (ee_compact_rows /
+    ee_compact_meta, all on the device). Rows past the live count inside a
+    bucket are padding: alive = 0 and a dummy request slot (index B of the
+    B + 1 result tables), so they never exit, scatter or count. Between
+    segments the host reads the 4-byte survivor count once to pick the next
+    bucket, and stops when nothing survives. Decisions equal EEPipeline.run's
+    compaction mode (same kernels on the same rows), and rows far from a
+    threshold equal feedback mode's."""
+
+    def __init__(self, pipe: EEPipeline, example, thresholds):
+        torch = nat.torch_cuda()
+        self.pipe = pipe
+        self.B = b = example.shape[0]
+        self.R = R = pipe.n_ramps
+        self.th = torch.tensor([float(t) for t in thresholds], dtype=torch.float64, device="cuda")
+        ends = list(pipe.ramp_order) + [len(pipe.stages) - 1]
+        starts = [0] + [e + 1 for e in ends[:-1]]
+        self.segments = list(zip(starts, ends))
+        self.buckets = sorted({min(b, 1 << k) for k in range(b.bit_length() + 1)})
+        dev = "cuda"
+        # result tables: B request slots + one dummy slot for padding rows
+        self.slots = SlotTable(torch.empty(b + 1, dtype=torch.int32, device=dev),
+                               torch.empty(b + 1, dtype=torch.float32, device=dev),
+                               torch.empty(b + 1, dtype=torch.int32, device=dev))
+        self.ramp_err = torch.empty((R, b + 1), dtype=torch.float32, device=dev)
+        self.ramp_label = torch.empty((R, b + 1), dtype=torch.int32, device=dev)
+        self.final_label = torch.empty((b + 1,), dtype=torch.int32, device=dev)
+        self.n_live = torch.zeros(len(self.segments), dtype=torch.int32, device=dev)
+        # each segment's input buffer (capacity B, the activation's own layout)
+        self.x_in, self.rows_in, self.alive_in = [], [], []
+        h = example
+        with torch.no_grad():
+            for a, e in self.segments:
+                self.x_in.append(torch.zeros_like(h))
+                self.rows_in.append(torch.full((b,), b, dtype=torch.int32, device=dev))
+                self.alive_in.append(torch.zeros(b, dtype=torch.uint8, device=dev))
+                for j in range(a, e + 1):
+                    h = pipe.stages[j](h)
+        self.x_in[0].copy_(example)  # run() without an input replays the example
+        self.graphs = {}
+        self.pool = torch.cuda.graph_pool_handle()
+        self.out = BatchResult(self.slots.label[:b], self.slots.site[:b], self.slots.err[:b],
+                               self.ramp_err[:, :b], self.ramp_label[:, :b], self.final_label[:b],
+                               thresholds=self.th)
+
+    def set_thresholds(self, thresholds):
+        self.th.copy_(self.th.new_tensor([float(t) for t in thresholds]))
+
+    def _segment(self, k: int, bb: int):
+        """Segment k at bucket bb: the eager body the graphs capture."""
+        torch = nat.torch_cuda()
+        a, e = self.segments[k]
+        h = self.x_in[k][:bb]
+        alive, rows = self.alive_in[k][:bb], self.rows_in[k][:bb]
+        last = k == len(self.segments) - 1
+        with torch.no_grad():
+            for j in range(a, e + 1 if not last else e):
+                h = self.pipe.stages[j](h)
+            if last:
+                logits = self.pipe.stages[e](h).float()
+                self.final_label.index_copy_(0, rows.long(), torch.argmax(logits, dim=1).to(torch.int32))
+                exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=self.R, alive=alive,
+                                 slot=rows, slots=self.slots, compact=False)
+                return
+            res = self.pipe.ramps[e](h, self.th[k:k + 1], alive=alive, slot=rows, slots=self.slots)
+            self.ramp_err[k].index_copy_(0, rows.long(), res.err)
+            self.ramp_label[k].index_copy_(0, rows.long(), res.label)
+            compact_rows(h, res.keep, res.n_keep, out=self.x_in[k + 1])
+            compact_meta(res.keep, res.n_keep, rows, self.B, self.B, self.rows_in[k + 1],
+                         self.alive_in[k + 1], self.n_live[k:k + 1])
+
+    def _graph(self, k: int, bb: int):
+        g = self.graphs.get((k, bb))
+        if g is None:
+            torch = nat.torch_cuda()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self._segment(k, bb)  # warm-up (idempotent on the live state)
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=self.pool):
+                self._segment(k, bb)
+            self.graphs[(k, bb)] = g
+        return g
+
+    def bucket(self, n: int) -> int:
+        for bb in self.buckets:
+            if bb >= n:
+                return bb
+        return self.B
+
+    def run(self, x=None) -> BatchResult:
+        torch = nat.torch_cuda()
+        b = self.B
+        if x is not None:
+            self.x_in[0].copy_(x)
+        self.slots.label.fill_(-1)
+        self.slots.site.fill_(-1)
+        self.slots.err.fill_(float("nan"))
+        self.ramp_err.fill_(float("nan"))
+        self.ramp_label.fill_(-1)
+        self.final_label.fill_(-1)
+        self.alive_in[0].fill_(1)
+        torch.arange(b, dtype=torch.int32, device="cuda", out=self.rows_in[0])
+        bb = b
+        for k in range(len(self.segments)):
+            self._graph(k, bb).replay()
+            if k == len(self.segments) - 1:
+                break
+            n = int(self.n_live[k].item())  # 4-byte read: the next bucket
+            if n == 0:
+                break
+            bb = self.bucket(n)
         return self.out
 
 

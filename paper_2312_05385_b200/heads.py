@@ -166,22 +166,45 @@ def exit_from_logits(logits, threshold, *, conf: str = "maxprob", site: int = 0,
     return ExitResult(err, label, exits, keep, n_keep, None)
 
 
+def _rows_dense(t) -> bool:
+    """Each row t[i] is one contiguous block at stride numel / B (contiguous,
+    or channels_last: the batch dimension is outermost in both)."""
+    import torch
+
+    return t.is_contiguous() or (t.dim() == 4 and t.is_contiguous(memory_format=torch.channels_last))
+
+
 def compact_rows(src, keep, n_keep, out=None):
-    """Gather the surviving rows of `src` ([B, ...], contiguous) into a dense
-    buffer (compaction mode: downstream blocks run only on these rows).
-    Returns the full-capacity output; its first n_keep rows are valid."""
+    """Gather the surviving rows of `src` ([B, ...], contiguous or channels_last)
+    into a dense buffer of the same memory format (compaction mode: downstream
+    blocks run only on these rows). Returns the full-capacity output (or `out`,
+    whose capacity may exceed B); its first n_keep rows are valid."""
     torch = nat.torch_cuda()
-    src = src.contiguous()
+    if not _rows_dense(src):
+        src = src.contiguous()
     b = src.shape[0]
     row_bytes = src.numel() // max(b, 1) * src.element_size()
     if row_bytes % 16:
         raise ParameterError("row size must be a multiple of 16 bytes")
     if out is None:
-        out = torch.empty_like(src)
+        out = torch.empty_like(src)  # preserves channels_last
+    elif (not _rows_dense(out) or out.dtype != src.dtype or out.shape[0] < b
+          or out.numel() // max(out.shape[0], 1) * out.element_size() != row_bytes):
+        raise ParameterError("out must be a dense row buffer of the same row size and dtype")
     nat.check(nat.load_library().ee_compact_rows(
         src.data_ptr(), row_bytes, keep.data_ptr(), n_keep.data_ptr(), b, out.data_ptr(),
         nat.stream_handle(torch)))
     return out
+
+
+def compact_meta(keep, n_keep, rows_in, cap: int, dummy: int, rows_out, alive_out, n_out=None):
+    """Bookkeeping of the next compacted stage, on the device: rows_out[i] =
+    rows_in[keep[i]] for i < n_keep (dummy after), alive_out[i] = i < n_keep,
+    n_out = n_keep (ee_compact_meta)."""
+    torch = nat.torch_cuda()
+    nat.check(nat.load_library().ee_compact_meta(
+        keep.data_ptr(), n_keep.data_ptr(), nat.ptr(rows_in), int(cap), int(dummy),
+        rows_out.data_ptr(), alive_out.data_ptr(), nat.ptr(n_out), nat.stream_handle(torch)))
 
 
 def linear_tc(x, weight, bias=None, *, splits: int = 0, out_bf16: bool = False):

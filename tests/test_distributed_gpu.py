@@ -49,6 +49,15 @@ def _worker(rank, world, port, q):
         dev = [ov.evaluate_many(th, to_host=False) for th in (diag, rnd, diag)]
         ov.join()
         res += [(a.cpu().numpy(), s.cpu().numpy()) for a, s in dev]
+        # the drop-in call on this rank's HOST shard (bits packed on the CPU)
+        from paper_2312_05385_b200.distributed import eval_thresholds_host_sharded, shard_range
+        from paper_2312_05385_b200.engine import WindowEvaluator
+
+        evf = WindowEvaluator.from_arrays(arrays, sites, prof, mode="hist")
+        lo, hi = shard_range(arrays.n, rank, world)
+        res.append(eval_thresholds_host_sharded(
+            np.ascontiguousarray(arrays.errs[lo:hi]), arrays.correct[lo:hi].astype(np.float64),
+            evf.serve, evf.vanilla_ms, diag, n_total=arrays.n))
         q.put((rank, [(a.tolist(), s.tolist()) for a, s in res]))
     finally:
         dist.destroy_process_group()
@@ -68,6 +77,7 @@ def test_two_rank_sweep_matches_one_gpu(cuda):
     rnd = (np.arange(64) / 63.0)[np.random.default_rng(3).integers(0, 64, size=(50, 12))]
     one = [ShardedSweep(arrays, sites, prof).evaluate_many(th) for th in (diag, rnd)]
     one += one + one[:1]  # the overlapped exchange: diag, rnd, diag
+    one += one[:1]  # host shards through eval_thresholds_host_sharded: diag
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

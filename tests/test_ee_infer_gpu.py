@@ -118,3 +118,97 @@ def test_cuda_graph_replay_matches_eager_and_retunes(cuda):
     out3 = runner.run(x2)
     ref3 = pipe.run(x2, th2)
     assert torch.equal(out3.released_label, ref3.released_label)
+
+
+def _near(fb, th, margin):
+    e = fb.ramp_err.float().cpu().numpy()
+    near = np.zeros(e.shape[1], dtype=bool)
+    for j, t in enumerate(th):
+        near |= np.abs(e[j] - t) < margin
+    return near
+
+
+@pytest.mark.parametrize("config", ["resnet18_fp32", "resnet18_bf16", "resnet50_bf16", "bert_bf16"])
+def test_compact_runner_matches_feedback_and_censors(cuda, config):
+    """CompactRunner (per-(segment, bucket) CUDA graphs, survivors gathered on
+    the device) releases what feedback mode releases for every row farther
+    than a margin from a threshold (cuDNN/GEMM results may change in the last
+    bits with the batch size, hence the margin: 1e-4 fp32, 2e-3 bf16), censors
+    later ramps of exited rows (NaN / -1), keeps running under retuned
+    thresholds and new inputs, and stops early when every row has exited."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    if config.startswith("resnet18"):
+        pipe, m = ee_infer.resnet18_cifar()
+        b, shape = 32, (3, 32, 32)
+    elif config == "resnet50_bf16":
+        pipe, m = ee_infer.resnet50_imagenet()
+        b, shape = 48, (3, 224, 224)
+    else:
+        pipe, m = ee_infer.bert_base()
+        b = 16
+    bf16 = config.endswith("bf16")
+    if bf16:
+        ee_infer.prepare_bf16(m, channels_last=not config.startswith("bert"))
+    margin = 2e-3 if bf16 else 1e-4
+
+    def make(n):
+        if config.startswith("bert"):
+            return torch.randint(0, 30522, (n, 128), generator=g, device="cuda")
+        x = torch.randn(n, *shape, generator=g, device="cuda")
+        if bf16:
+            x = x.to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+        return x
+
+    th = _thresholds(pipe, make(64))
+    x = make(b)
+    runner = pipe.capture_compact(x, th)
+    for trial, (xx, tt) in enumerate([(x, th), (make(b), th), (x, [t * 0.5 for t in th])]):
+        if trial == 2:
+            runner.set_thresholds(tt)
+        out = runner.run(xx)
+        fb = pipe.run(xx, tt)
+        near = _near(fb, tt, margin)
+        site = out.released_site.cpu().numpy()
+        assert (site >= 0).all()
+        assert np.array_equal(site[~near], fb.released_site.cpu().numpy()[~near]), trial
+        assert np.array_equal(out.released_label.cpu().numpy()[~near],
+                              fb.released_label.cpu().numpy()[~near]), trial
+        err = out.ramp_err.cpu().numpy()
+        for i in range(b):
+            s = site[i]
+            assert np.isfinite(err[: min(s + 1, pipe.n_ramps), i]).all(), (trial, i)
+            assert np.isnan(err[s + 1:, i]).all(), (trial, i)
+            assert (out.ramp_label.cpu().numpy()[s + 1:, i] == -1).all()
+        fin = out.final_label.cpu().numpy()
+        assert ((fin >= 0) == (site == pipe.n_ramps)).all()
+        # the eager compaction path agrees as well (same margin)
+        ref = pipe.run(xx, tt, mode="compact")
+        assert np.array_equal(site[~near], ref.released_site.cpu().numpy()[~near]), trial
+    # everything exits at the first ramp: only the first segment runs
+    runner.set_thresholds([2.0] * pipe.n_ramps)
+    out = runner.run(x)
+    assert (out.released_site.cpu() == 0).all()
+
+
+def test_overlapped_ramps_equal_serial_ramps(cuda):
+    """Feedback mode runs the ramp heads on a side stream overlapped with the
+    backbone; the results are bit-identical to the serial schedule, eager and
+    graph-captured."""
+    pipe, m = ee_infer.resnet18_cifar()
+    ee_infer.prepare_bf16(m, channels_last=True)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    mk = lambda n: torch.randn(n, 3, 32, 32, generator=g, device="cuda").to(torch.bfloat16).contiguous(
+        memory_format=torch.channels_last)
+    th = _thresholds(pipe, mk(128))
+    x = mk(32)
+    over = pipe.run(x, th, timed=True)
+    gr = pipe.capture(x, th).run()
+    pipe.overlap_ramps = False
+    try:
+        ser = pipe.run(x, th)
+    finally:
+        pipe.overlap_ramps = True
+    for a in (over, gr):
+        for f in ("released_site", "released_label", "released_err", "ramp_err", "ramp_label", "final_label"):
+            assert torch.equal(getattr(a, f), getattr(ser, f)), f
+    assert np.all(over.release_ms > 0)

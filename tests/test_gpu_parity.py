@@ -509,7 +509,7 @@ def test_diag2_matches_diag1_and_oracle(cuda, r, n, m, c_rep):
     ev = WindowEvaluator.from_arrays(arrays, find_feasible_sites(prof)[:r], prof, mode="hist")
     hist2, ok2 = ev.histograms(th)
     acc2, sav2 = ev.evaluate_many(th)
-    for ver in (5, 2, 1):
+    for ver in (6, 5, 2, 1):
         _native.set_diag_version(ver)
         try:
             hist1, ok1 = ev.histograms(th)

@@ -46,13 +46,20 @@ def _check(res, feat, w, bias, conf, thr, alive=None, check_logits=True):
 @pytest.mark.parametrize("layout", ["nchw", "nhwc", "pooled"])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("conf", ["maxprob", "entropy"])
-def test_fused_head_matches_torch(cuda, layout, dtype, conf):
+@pytest.mark.parametrize("shape", [(64, 96, 7), (32, 64, 32), (32, 128, 16), (16, 512, 4), (8, 24, 57)])
+def test_fused_head_matches_torch(cuda, layout, dtype, conf, shape):
+    """Every pooling path, including the cluster-split ones (a row's map split
+    over 2-8 CTAs of one cluster when it is >= 16 KB: the CIFAR ResNet-18 ramp
+    shapes) and a ragged 57x57 plane."""
     g = torch.Generator().manual_seed(1)
-    b, c, k = 64, 96, 10
+    b, c, hw = shape
+    k = 10
     if layout == "pooled":
+        if hw != 7:
+            pytest.skip("pooled rows have no spatial split")
         feat = torch.randn(b, c, generator=g)
     else:
-        feat = torch.randn(b, c, 7, 7, generator=g)
+        feat = torch.randn(b, c, hw, hw, generator=g)
     w = torch.randn(k, c, generator=g) * 0.3
     bias = torch.randn(k, generator=g) * 0.1
     feat_d = feat.to(dtype).cuda()

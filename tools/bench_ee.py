@@ -60,7 +60,49 @@ def bench(name, pipe, make_input, batch, iters, warmup=5):
                 and torch.equal(runner.out.released_label, ref.released_label))
     out["feedback_graph"] = {"samples_per_s": batch / (np.mean(ts) / 1e3),
                              "p50_batch_ms": float(np.percentile(ts, 50)),
-                             "matches_eager": same}
+                             "matches_eager": same, "ramps": "side stream, overlapped with the backbone"}
+    # the same graph with the ramp heads serialised on the backbone's stream
+    pipe.overlap_ramps = False
+    try:
+        srun = pipe.capture(x, th)
+    finally:
+        pipe.overlap_ramps = True
+    for _ in range(warmup):
+        srun.run()
+    ts = []
+    for _ in range(iters):
+        ev0.record()
+        srun.run()
+        ev1.record()
+        ev1.synchronize()
+        ts.append(ev0.elapsed_time(ev1))
+    out["feedback_graph_serial_ramps"] = {"samples_per_s": batch / (np.mean(ts) / 1e3),
+                                          "p50_batch_ms": float(np.percentile(ts, 50))}
+    # compaction mode as per-(segment, bucket) CUDA graphs (survivors gathered on the device)
+    crun = pipe.capture_compact(x, th)
+    for _ in range(warmup):
+        crun.run()
+    ts, exits = [], []
+    for _ in range(iters):
+        ev0.record()
+        crun.run()
+        ev1.record()
+        ev1.synchronize()
+        ts.append(ev0.elapsed_time(ev1))
+        exits.append(float((crun.out.released_site < pipe.n_ramps).float().mean().item()))
+    fb = pipe.run(x, th)
+    margin = 2e-3
+    e = fb.ramp_err.float()
+    near = torch.zeros(batch, dtype=torch.bool, device="cuda")
+    for j, t in enumerate(th):
+        near |= (e[j] - t).abs() < margin
+    agree = bool(torch.equal(crun.out.released_site[~near], fb.released_site[~near]))
+    out["compact_graph"] = {"samples_per_s": batch / (np.mean(ts) / 1e3),
+                            "p50_batch_ms": float(np.percentile(ts, 50)),
+                            "exit_rate": float(np.mean(exits)),
+                            "graphs_captured": len(crun.graphs),
+                            "matches_feedback_off_margin": agree,
+                            "rows_within_margin": int(near.sum().item())}
     # vanilla: the same stages, no ramps
     x = make_input(batch)
     with torch.no_grad():

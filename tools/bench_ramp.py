@@ -17,15 +17,21 @@ for c, h, w in shapes:
     alive = torch.ones(32, dtype=torch.uint8, device="cuda")
     rows = torch.arange(32, dtype=torch.int32, device="cuda")
     slots = SlotTable.empty(32)
-    for _ in range(3):
-        ctl(x, th, alive=alive, slot=rows, slots=slots)
-    torch.cuda.synchronize()
-    gr = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gr):
-        for _ in range(200):
-            ctl(x, th, alive=alive, slot=rows, slots=slots)
-    gr.replay(); torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); gr.replay(); b.record(); torch.cuda.synchronize()
-    out[f"{c}x{h}x{w}"] = round(a.elapsed_time(b) / 200 * 1e3, 2)
+    err = torch.empty(32, dtype=torch.float32, device="cuda")
+    lab = torch.empty(32, dtype=torch.int32, device="cuda")
+    for compact in (True, False):
+        kw = dict(alive=alive, slot=rows, slots=slots, compact=compact)
+        if not compact:
+            kw.update(out_err=err, out_label=lab)
+        for _ in range(3):
+            ctl(x, th, **kw)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            for _ in range(200):
+                ctl(x, th, **kw)
+        gr.replay(); torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); gr.replay(); b.record(); torch.cuda.synchronize()
+        out[f"{c}x{h}x{w}" + ("" if compact else "_feedback")] = round(a.elapsed_time(b) / 200 * 1e3, 2)
 print(json.dumps({"us_per_ramp_call": out}))
