@@ -229,14 +229,24 @@ int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float
  *   d_c [m, n] = act(d_a bf16 [m, k] x d_w bf16 [n, k]^T + d_bias f32 [n])
  * d_c is bf16 (out_bf16 != 0, round to nearest even) or f32. act: 0 none,
  * 1 GELU (erf), 2 GELU (tanh approximation), 3 ReLU. path: 0 auto, 1 swap-AB
- * weight-streaming kernel (cluster split-K, DSMEM reduction, any m), 2 / 4 / 3
- * the persistent CTA-pair kernel (cta_group::2, 256 x 256 / 192 / 128 tiles;
+ * weight-streaming kernel (cluster split-K, DSMEM reduction, any m), 2 / 4 / 3 / 5
+ * the persistent CTA-pair kernel (cta_group::2, 256 x 256 / 192 / 128 / 64 tiles;
  * needs 16-byte output rows). Auto takes the swap kernel for m <= 256. k % 8 == 0,
  * all pointers 16-byte aligned. Results are deterministic. Replaces the
  * library GEMMs the reference's models would call. */
 int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
                     void* d_c, int32_t out_bf16, int32_t act, int64_t m, int64_t n, int64_t k,
                     int32_t splits, int32_t path, void* d_work, int64_t work_bytes, void* stream);
+
+/* ee_gemm_bf16_ex with a residual added before the activation:
+ *   d_c [m, n] = act(d_a x d_w^T + d_bias + d_res bf16 [m, n])
+ * (a ResNet bottleneck's conv3 + shortcut + ReLU as one kernel over NHWC
+ * activations). d_res may be NULL; when given, out_bf16 != 0, n % 8 == 0 and
+ * d_res is 16-byte aligned. */
+int ee_gemm_bf16_res(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
+                     const void* d_res, void* d_c, int32_t out_bf16, int32_t act, int64_t m,
+                     int64_t n, int64_t k, int32_t splits, int32_t path, void* d_work,
+                     int64_t work_bytes, void* stream);
 /* Bytes of device workspace ee_gemm_bf16_ex needs for this call (split-K
  * partial tiles of the swap kernel; 0 when none). Pass a buffer at least this
  * large as d_work, or NULL to let the call take stream-ordered pool memory
@@ -269,6 +279,38 @@ int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_
  * (bf16, rounded like torch's add), then x[r] = LayerNorm(h[r]) * gamma + beta
  * (fp32 statistics, two-pass), bf16 throughout; y may be null (LayerNorm only).
  * One CTA of d / 8 threads per row; d a multiple of 8, at most 8192. */
+/* Convolution as an implicit GEMM on the tcgen05 pair kernel (csrc/gemm.cu):
+ * y bf16 NHWC [n, ho, wo, cout] = act(conv(x bf16 NHWC [n, h, w, c],
+ * w bf16 [cout, kh, kw, c]) + bias f32 [cout] (nullable) + res bf16
+ * [n, ho, wo, cout] (nullable)), ho = (h + 2 pad - kh) / stride + 1 (same for
+ * wo); act 0 none / 3 ReLU. The A operand is never materialised: each k-tile
+ * is one TMA im2col load (128 consecutive output pixels x 64 channels of one
+ * filter tap, zero padding by the TMA unit). c % 64 == 0, cout % 8 == 0,
+ * 16-byte aligned pointers. (A ResNet's spatial convolutions.) */
+int ee_conv_bf16(ee_workspace* ws, const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c,
+                 const void* d_w, int32_t cout, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                 const float* d_bias, const void* d_res, int32_t act, void* d_y, void* stream);
+
+/* im2col of an NHWC bf16 map for a convolution with too few input channels
+ * for ee_conv_bf16 (the 3-channel stem): out bf16 [n*ho*wo, kp], column k =
+ * (kh, kw, c) as in a channels_last weight, zero past kh*kw*c (kp % 64 == 0)
+ * and outside the image; the GEMM then runs on ee_gemm_bf16_res. */
+int ee_im2col_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, int32_t kh, int32_t kw,
+                   int32_t stride, int32_t pad, int32_t kp, void* d_out, void* stream);
+
+/* k x k max pooling (stride, pad; padding = -inf) of an NHWC bf16 map
+ * [n, h, w, c] -> [n, ho, wo, c]; c % 8 == 0, 16-byte aligned pointers. */
+int ee_maxpool_nhwc_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, int32_t k,
+                         int32_t stride, int32_t pad, void* d_out, void* stream);
+
+/* Convolution epilogue over an NHWC bf16 map viewed as [m, c] rows:
+ * y = act(x + bias[c] (+ res)) with act 0 none / 3 ReLU, bias f32 (nullable),
+ * res bf16 [m, c] (nullable, e.g. a ResNet shortcut). c % 8 == 0, 16-byte
+ * aligned pointers; y may alias x. For the convolutions the repo's GEMM does
+ * not run (bias, ReLU and shortcut then cost one pass instead of three). */
+int ee_bias_act_bf16(const void* d_x, const float* d_bias, const void* d_res, int32_t act, int64_t m,
+                     int32_t c, void* d_y, void* stream);
+
 int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const void* d_beta,
                           double eps, int64_t rows, int32_t d, void* d_x, void* stream);
 

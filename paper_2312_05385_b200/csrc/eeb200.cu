@@ -500,6 +500,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
 #include "pool.cuh"
+#include "conv_aux.cuh"
 namespace {
 
 // L2 eviction for benchmarks: streams a buffer larger than L2 with the same
@@ -2241,11 +2242,42 @@ int ee_exit_from_logits(ee_workspace* ws, const float* d_logits_in, int64_t b, i
 
 }  // extern "C"
 // gemm.cu (tcgen05 pair / swap-AB kernels)
-cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, void* c, int out_bf16,
-                            int act, int m, int n, int k, int splits, int path, void* work,
+cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, const void* res, void* c,
+                            int out_bf16, int act, int m, int n, int k, int splits, int path, void* work,
                             size_t work_bytes, cudaStream_t st);
 size_t ee_gemm3_workspace(int m, int n, int k, int splits, int path, int out_bf16);
+cudaError_t ee_conv3_launch(const void* x, const void* w, const float* bias, const void* res, void* y,
+                            int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad,
+                            int act, cudaStream_t st);
 extern "C" {
+
+int ee_conv_bf16(ee_workspace* ws, const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c,
+                 const void* d_w, int32_t cout, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                 const float* d_bias, const void* d_res, int32_t act, void* d_y, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (n < 1 || h < 1 || w < 1 || c < 1 || cout < 1 || kh < 1 || kw < 1 || stride < 1 || stride > 8 ||
+      pad < 0 || pad >= std::min(kh, kw) + 8 || kh > h + 2 * pad || kw > w + 2 * pad)
+    return fail(EE_ERR_ARG, "bad convolution shape");
+  if (c % 64) return fail(EE_ERR_ARG, "input channels must be a multiple of 64");
+  if (cout % 8) return fail(EE_ERR_ARG, "output channels must be a multiple of 8");
+  if (act != 0 && act != 3) return fail(EE_ERR_ARG, "act must be 0 (none) or 3 (ReLU)");
+  if (!d_x || !d_w || !d_y) return fail(EE_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(d_x) | reinterpret_cast<uintptr_t>(d_w) |
+       reinterpret_cast<uintptr_t>(d_y) | reinterpret_cast<uintptr_t>(d_res)) & 15)
+    return fail(EE_ERR_ARG, "pointers must be 16-byte aligned");
+  const int64_t ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  if (n * ho * wo > 0x7fffffff || n > 0x7fffffff || (int64_t)kh * kw * c > 0x7fffffff)
+    return fail(EE_ERR_ARG, "convolution too large");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  cudaError_t e;
+  {
+    ProfScope ps(ws, st, "k_conv3");
+    e = ee_conv3_launch(d_x, d_w, d_bias, d_res, d_y, (int)n, h, w, c, cout, kh, kw, stride, pad, act, st);
+  }
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_conv3: ") + cudaGetErrorString(e));
+  return EE_OK;
+}
 
 int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float* d_bias,
                  void* d_c, int32_t out_bf16, int64_t m, int64_t n, int64_t k, int32_t splits,
@@ -2257,7 +2289,7 @@ int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float
 int64_t ee_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t splits, int32_t path,
                                int32_t out_bf16) {
   if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff ||
-      path < 0 || path > 4)
+      path < 0 || path > 5)
     return fail(EE_ERR_ARG, "bad GEMM shape or path");
   return (int64_t)ee_gemm3_workspace((int)m, (int)n, (int)k, splits, path, out_bf16);
 }
@@ -2265,11 +2297,21 @@ int64_t ee_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t splits, 
 int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
                     void* d_c, int32_t out_bf16, int32_t act, int64_t m, int64_t n, int64_t k,
                     int32_t splits, int32_t path, void* d_work, int64_t work_bytes, void* stream) {
+  return ee_gemm_bf16_res(ws, d_a, d_w, d_bias, nullptr, d_c, out_bf16, act, m, n, k, splits, path,
+                          d_work, work_bytes, stream);
+}
+
+int ee_gemm_bf16_res(ee_workspace* ws, const void* d_a, const void* d_w, const float* d_bias,
+                     const void* d_res, void* d_c, int32_t out_bf16, int32_t act, int64_t m,
+                     int64_t n, int64_t k, int32_t splits, int32_t path, void* d_work,
+                     int64_t work_bytes, void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (d_res && (!out_bf16 || n % 8 || (reinterpret_cast<uintptr_t>(d_res) & 15)))
+    return fail(EE_ERR_ARG, "a residual needs bf16 output, N % 8 == 0 and a 16-byte aligned R");
   if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(EE_ERR_ARG, "bad GEMM shape");
   if (k % 8) return fail(EE_ERR_ARG, "K must be a multiple of 8 (16-byte rows)");
-  if (act < 0 || act > 3 || path < 0 || path > 4) return fail(EE_ERR_ARG, "bad act or path");
+  if (act < 0 || act > 3 || path < 0 || path > 5) return fail(EE_ERR_ARG, "bad act or path");
   if (!d_a || !d_w || !d_c) return fail(EE_ERR_ARG, "null pointer");
   if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_w) |
        reinterpret_cast<uintptr_t>(d_c)) & 15)
@@ -2279,7 +2321,7 @@ int ee_gemm_bf16_ex(ee_workspace* ws, const void* d_a, const void* d_w, const fl
   cudaError_t e;
   {
     ProfScope ps(ws, st, "k_gemm3");
-    e = ee_gemm3_launch(d_a, d_w, d_bias, d_c, out_bf16, act, (int)m, (int)n, (int)k, splits, path,
+    e = ee_gemm3_launch(d_a, d_w, d_bias, d_res, d_c, out_bf16, act, (int)m, (int)n, (int)k, splits, path,
                         d_work, (size_t)std::max<int64_t>(0, work_bytes), st);
   }
   if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_gemm3: ") + cudaGetErrorString(e));
@@ -2576,6 +2618,93 @@ int ee_decode_attention_bf16(const void* d_qkv, const void* d_kv, const int64_t*
   return EE_OK;
 }
 
+}  // extern "C"
+// y[m, c] = act(x[m, c] + bias[c] (+ r[m, c])) over a row-major bf16 [M, C]
+// map (an NHWC activation after a convolution without its own epilogue), 8
+// channels per 16-byte vector; act 0 none, 3 ReLU (the GEMM's codes)
+__global__ void k_bias_act_bf16(const uint4* x, const float* __restrict__ bias,
+                                const uint4* __restrict__ r, int act, int64_t nvec, int cvec,
+                                uint4* y) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 a = __ldcs(x + v);
+    const int c0 = (int)(v % cvec) * 8;
+    const float4 b0 = bias ? __ldg(reinterpret_cast<const float4*>(bias + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b1 = bias ? __ldg(reinterpret_cast<const float4*>(bias + c0 + 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint4 rr = make_uint4(0u, 0u, 0u, 0u);
+    if (r) rr = __ldcs(r + v);
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, rw[4] = {rr.x, rr.y, rr.z, rr.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float lo = bf_lo(aw[e]) + bb[2 * e], hi = bf_hi(aw[e]) + bb[2 * e + 1];
+      if (r) lo += bf_lo(rw[e]), hi += bf_hi(rw[e]);
+      if (act == 3) lo = fmaxf(lo, 0.f), hi = fmaxf(hi, 0.f);
+      o[e] = bf_round(lo) | (bf_round(hi) << 16);
+    }
+    y[v] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+extern "C" {
+int ee_im2col_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, int32_t kh, int32_t kw,
+                   int32_t stride, int32_t pad, int32_t kp, void* d_out, void* stream) {
+  if (n < 1 || h < 1 || w < 1 || c < 1 || kh < 1 || kw < 1 || stride < 1 || pad < 0 ||
+      kh > h + 2 * pad || kw > w + 2 * pad)
+    return fail(EE_ERR_ARG, "bad convolution shape");
+  if (kp % 64 || kp < kh * kw * c) return fail(EE_ERR_ARG, "kp must be a multiple of 64 >= kh*kw*c");
+  if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
+  if (reinterpret_cast<uintptr_t>(d_out) & 15) return fail(EE_ERR_ARG, "output must be 16-byte aligned");
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  const int64_t m = n * ho * wo;
+  const int64_t nv = m * (kp / 8);
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(nv, 256), (int64_t)sm_count() * 16);
+  convaux::k_im2col_nhwc<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint16_t*>(d_x), h, w, c, kh, kw, stride, pad, ho, wo, m, kp,
+      static_cast<uint4*>(d_out));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_maxpool_nhwc_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, int32_t k,
+                         int32_t stride, int32_t pad, void* d_out, void* stream) {
+  if (n < 1 || h < 1 || w < 1 || c < 1 || k < 1 || stride < 1 || pad < 0 || 2 * pad > k ||
+      k > h + 2 * pad || k > w + 2 * pad)
+    return fail(EE_ERR_ARG, "bad pooling shape");
+  if (c % 8) return fail(EE_ERR_ARG, "channels must be a multiple of 8");
+  if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(d_x) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+    return fail(EE_ERR_ARG, "pointers must be 16-byte aligned");
+  const int ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
+  const int64_t nv = n * ho * wo * (c / 8);
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(nv, 256), (int64_t)sm_count() * 16);
+  convaux::k_maxpool_nhwc<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint4*>(d_x), h, w, c / 8, k, stride, pad, ho, wo, nv, static_cast<uint4*>(d_out));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_bias_act_bf16(const void* d_x, const float* d_bias, const void* d_res, int32_t act, int64_t m,
+                     int32_t c, void* d_y, void* stream) {
+  if (m < 0 || c < 1 || c % 8) return fail(EE_ERR_ARG, "C must be a positive multiple of 8");
+  if (act != 0 && act != 3) return fail(EE_ERR_ARG, "act must be 0 (none) or 3 (ReLU)");
+  if (!d_x || !d_y) return fail(EE_ERR_ARG, "null pointer");
+  if ((reinterpret_cast<uintptr_t>(d_x) | reinterpret_cast<uintptr_t>(d_y) |
+       reinterpret_cast<uintptr_t>(d_res) | reinterpret_cast<uintptr_t>(d_bias)) & 15)
+    return fail(EE_ERR_ARG, "pointers must be 16-byte aligned");
+  const int64_t nvec = m * (c / 8);
+  if (nvec == 0) return EE_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(nvec, 256), (int64_t)sm_count() * 8);
+  k_bias_act_bf16<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint4*>(d_x), d_bias, static_cast<const uint4*>(d_res), act, nvec, c / 8,
+      static_cast<uint4*>(d_y));
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+}  // extern "C"
+
+extern "C" {
 int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const void* d_beta,
                           double eps, int64_t rows, int32_t d, void* d_x, void* stream) {
   if (rows < 1 || d < 8 || d % 8 || d > 8192 || rows > 0x7fffffff) return fail(EE_ERR_ARG, "bad shape");

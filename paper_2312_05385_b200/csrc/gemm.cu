@@ -1,7 +1,8 @@
 // gemm.cu — 5th-generation tensor-core GEMMs for the backbone contractions and
 // the wide ramp heads (north star (1)):
 //
-//     C[M, N] (bf16 or fp32) = act(A[M, K] (bf16, K-major) * W[N, K]^T (bf16) + bias[N])
+//     C[M, N] (bf16 or fp32) = act(A[M, K] (bf16, K-major) * W[N, K]^T (bf16) + bias[N]
+//                                  [+ R[M, N] (bf16 residual, e.g. a ResNet shortcut)])
 //
 // W is an nn.Linear weight (out_features x in_features, row-major), so both
 // operands are K-major and the whole contraction is one tcgen05 "TN" GEMM.
@@ -50,6 +51,16 @@ constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the pair's rank 0
 
 enum Act { ACT_NONE = 0, ACT_GELU_ERF = 1, ACT_GELU_TANH = 2, ACT_RELU = 3 };
+
+// implicit-GEMM convolution (k_gemm_pair<..., true>): GEMM row m = output pixel
+// (n, oh, ow) of an NHWC map, k = (kh, kw, c) with 64-channel blocks
+struct ConvGeom {
+  int hw_out;   // Ho * Wo
+  int wo;       // Wo
+  int kw;       // filter width
+  int cblocks;  // C / 64
+  int stride, pad;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -114,6 +125,19 @@ __device__ __forceinline__ void tma_load_pair(void* smem, const CUtensorMap* map
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(x), "r"(y)
+      : "memory");
+}
+// pair form of an im2col load (implicit-GEMM convolution): 128 consecutive
+// output pixels x 64 channels of the NHWC input for filter tap (ow_off, oh_off);
+// (c, w, h, n) is the input position of the first pixel's window corner
+__device__ __forceinline__ void tma_load_im2col_pair(void* smem, const CUtensorMap* map, uint64_t* bar,
+                                                     int c, int w, int h, int n, int ow_off, int oh_off) {
+  const uint16_t ow16 = (uint16_t)ow_off, oh16 = (uint16_t)oh_off;
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c), "r"(w), "r"(h),
+      "r"(n), "h"(ow16), "h"(oh16)
       : "memory");
 }
 __device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* smem, int x, int y) {
@@ -227,11 +251,11 @@ struct PairCfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BIAS;
 };
 
-template <int BN, int ACT, bool OUT_BF16>
+template <int BN, int ACT, bool OUT_BF16, bool IM2COL = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int M,
-                int N, int K) {
+                const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias,
+                const uint16_t* __restrict__ res, int M, int N, int K, const ConvGeom G) {
   using Cfg = PairCfg<BN>;
   constexpr int ST = Cfg::STAGES;
   constexpr int CW = OUT_BF16 ? 64 : 32;  // output columns per 128-byte staging row
@@ -277,12 +301,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       for (int t = pair; t < tiles; t += pairs) {
         const int m0 = (t % mt) * 256 + (int)rank * 128;
         const int n0 = (t / mt) * BN + (int)rank * (BN / 2);
+        // implicit GEMM: the input window corner of this CTA's first output pixel
+        int img = 0, hb = 0, wb = 0;
+        if constexpr (IM2COL) {
+          img = m0 / G.hw_out;
+          const int rem = m0 - img * G.hw_out;
+          const int oh = rem / G.wo;
+          hb = oh * G.stride - G.pad;
+          wb = (rem - oh * G.wo) * G.stride - G.pad;
+        }
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % ST;
           mbar_wait(&empty_bar[s], ((it / ST) & 1) ^ 1);
           if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * Cfg::STAGE);
           unsigned char* sa = smem + s * Cfg::STAGE;
-          tma_load_pair(sa, &tmA, &full_bar[s], kt * BK, m0);
+          if constexpr (IM2COL) {
+            const int tap = kt / G.cblocks, cb = kt - tap * G.cblocks;
+            const int kh = tap / G.kw;
+            tma_load_im2col_pair(sa, &tmA, &full_bar[s], cb * BK, wb, hb, img, tap - kh * G.kw, kh);
+          } else {
+            tma_load_pair(sa, &tmA, &full_bar[s], kt * BK, m0);
+          }
           tma_load_pair(sa + Cfg::A_BYTES, &tmB, &full_bar[s], kt * BK, n0);
         }
       }
@@ -324,6 +363,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
       constexpr int NCH = BN / CW;  // chunks per tile; half h takes chunks [h*NCH/2 ...)
       const int c_lo = h * (NCH / 2) * CW, c_hi = h ? BN : (NCH / 2) * CW;
+      if (c_lo >= c_hi) {  // a one-chunk tile (BN = 64, bf16): half 0 only releases TMEM
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty_bar[a]);
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = c_lo; c0 < c_hi; c0 += CW) {
         uint32_t v[CW];
@@ -333,7 +378,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         } else {
           tmem_ld32_nowait(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
         }
+        // residual row segment of this lane (row0 + lane, CW columns), loaded
+        // while the TMEM read is in flight (bf16 output: CW = 64 = 8 x 16 B)
+        uint4 rv[CW / 8];
+        const bool has_res = res != nullptr && OUT_BF16;
+        if (has_res) {
+          const int row = row0 + lane, col = n0 + c0;
+          const bool in = row < M && col < N;
+          const uint4* rp = reinterpret_cast<const uint4*>(res + (int64_t)row * N + col);
+#pragma unroll
+          for (int i = 0; i < CW / 8; ++i)
+            rv[i] = in && col + 8 * i < N ? __ldg(rp + i) : make_uint4(0u, 0u, 0u, 0u);
+        }
         tmem_wait_ld();
+        if (has_res) {  // v += residual (fp32), before the bias / activation
+#pragma unroll
+          for (int i = 0; i < CW / 8; ++i) {
+            const uint32_t w4[4] = {rv[i].x, rv[i].y, rv[i].z, rv[i].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * i + 2 * e] = __float_as_uint(__uint_as_float(v[8 * i + 2 * e]) + __uint_as_float(w4[e] << 16));
+              v[8 * i + 2 * e + 1] =
+                  __float_as_uint(__uint_as_float(v[8 * i + 2 * e + 1]) + __uint_as_float(w4[e] & 0xffff0000u));
+            }
+          }
+        }
         if (c0 + CW >= c_hi) {  // this warp's columns drained: the MMA may reuse them
           fence_before();
           __syncwarp();
@@ -421,8 +490,8 @@ struct SwapCfg {
 template <int NP, int ACT, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
     k_gemm_swap(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
-                const float* __restrict__ bias, void* __restrict__ C, int M, int N, int K,
-                int kt_per, float* __restrict__ part) {
+                const float* __restrict__ bias, const uint16_t* __restrict__ res,
+                void* __restrict__ C, int M, int N, int K, int kt_per, float* __restrict__ part) {
   using Cfg = SwapCfg<NP>;
   constexpr int ST = Cfg::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -512,8 +581,9 @@ __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (c0 + j < rows) {
-              const float y = act<ACT>(__uint_as_float(v[j]) + bf);
               const int64_t o = (int64_t)(r0 + c0 + j) * N + f;
+              const float rr = res ? __uint_as_float((uint32_t)__ldg(res + o) << 16) : 0.f;
+              const float y = act<ACT>((__uint_as_float(v[j]) + rr) + bf);
               if constexpr (OUT_BF16)
                 static_cast<uint16_t*>(C)[o] = (uint16_t)(bf16x2(y, 0.f) & 0xFFFFu);
               else
@@ -569,7 +639,8 @@ __global__ void __launch_bounds__(THREADS, SwapCfg<NP>::CTAS_PER_SM)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (fb + e >= N) break;
-          const float y = act<ACT>(a4[e] + (bias ? __ldg(bias + fb + e) : 0.f));
+          const float rr = res ? __uint_as_float((uint32_t)__ldg(res + o + e) << 16) : 0.f;
+          const float y = act<ACT>((a4[e] + rr) + (bias ? __ldg(bias + fb + e) : 0.f));
           if constexpr (OUT_BF16)
             static_cast<uint16_t*>(C)[o + e] = (uint16_t)(bf16x2(y, 0.f) & 0xFFFFu);
           else
@@ -616,6 +687,45 @@ bool make_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esize
   return enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+PFN_cuTensorMapEncodeIm2col_v12000 encoder_im2col() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  });
+  return fn;
+}
+
+// im2col view of an NHWC bf16 map [n, h, w, c] for a kh x kw / stride / pad
+// convolution: each load is 128 consecutive output pixels (w fastest, then h,
+// then n) x 64 channels of one filter tap, zero outside the image (SWIZZLE_128B,
+// the same smem layout as a 2D K-major tile)
+bool make_im2col_map(CUtensorMap* m, const void* x, int n, int h, int w, int c, int kh, int kw,
+                     int stride, int pad) {
+  auto enc = encoder_im2col();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  int lower[2] = {-pad, -pad};                          // (w, h)
+  int upper[2] = {pad - (kw - 1), pad - (kh - 1)};      // Wo = (w + upper - lower - 1) / s + 1
+  cuuint32_t estr[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper,
+          (cuuint32_t)gemm3::BK, 128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  // drivers up to 13.1 mis-set one descriptor bit for tensors under 128 KB
+  // (the same workaround as CUTLASS's im2col copy traits)
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && (uint64_t)n * h * w * c * 2 < 131072)
+    reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+  return true;
 }
 
 cudaError_t set_smem(const void* fn, int smem) {
@@ -673,8 +783,8 @@ int max_pairs(Kern kern, int smem) {
 }
 
 template <int BN, int ACT, bool BF>
-cudaError_t launch_pair(const void* a, const void* w, const float* bias, void* c, int m, int n,
-                        int k, cudaStream_t st) {
+cudaError_t launch_pair(const void* a, const void* w, const float* bias, const uint16_t* res, void* c,
+                        int m, int n, int k, cudaStream_t st) {
   using Cfg = gemm3::PairCfg<BN>;
   auto kern = gemm3::k_gemm_pair<BN, ACT, BF>;
   cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
@@ -687,7 +797,30 @@ cudaError_t launch_pair(const void* a, const void* w, const float* bias, void* c
     return cudaErrorInvalidValue;
   const int tiles = ((m + 255) / 256) * ((n + BN - 1) / BN);
   const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
-  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, m, n, k);
+  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, res, m, n, k,
+                                                                 gemm3::ConvGeom{});
+  return cudaGetLastError();
+}
+
+template <int BN, int ACT>
+cudaError_t launch_conv(const void* x, const void* w, const float* bias, const uint16_t* res, void* y,
+                        int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad,
+                        cudaStream_t st) {
+  using Cfg = gemm3::PairCfg<BN>;
+  auto kern = gemm3::k_gemm_pair<BN, ACT, true, true>;
+  cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
+  if (e != cudaSuccess) return e;
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (wd + 2 * pad - kw) / stride + 1;
+  const int m = n * ho * wo, k = kh * kw * c;
+  CUtensorMap ta, tb, tc;
+  if (!make_im2col_map(&ta, x, n, h, wd, c, kh, kw, stride, pad) ||
+      !make_map(&tb, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cout, k, gemm3::BK, BN / 2) ||
+      !make_map(&tc, y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, cout, 64, 32))
+    return cudaErrorInvalidValue;
+  const gemm3::ConvGeom g{ho * wo, wo, kw, c / gemm3::BK, stride, pad};
+  const int tiles = ((m + 255) / 256) * ((cout + BN - 1) / BN);
+  const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
+  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, res, m, cout, k, g);
   return cudaGetLastError();
 }
 
@@ -710,7 +843,7 @@ Plan make_plan(int m, int n, int k, int splits, int path, bool bf) {
   const bool c_ok = (n * (bf ? 2 : 4)) % 16 == 0;
   p.swap = path == 1 || (path == 0 && m <= 256) || !c_ok;
   if (!p.swap) {
-    p.bn = path == 3 ? 128 : path == 2 ? 256 : path == 4 ? 192 : pick_bn(m, n, device_sms() / 2);
+    p.bn = path == 3 ? 128 : path == 2 ? 256 : path == 4 ? 192 : path == 5 ? 64 : pick_bn(m, n, device_sms() / 2);
     return p;
   }
   p.np = m <= 32 ? 32 : m <= 64 ? 64 : 128;
@@ -733,8 +866,8 @@ Plan make_plan(int m, int n, int k, int splits, int path, bool bf) {
 }
 
 template <int NP, int ACT, bool BF>
-cudaError_t launch_swap(const Plan& p, const void* a, const void* w, const float* bias, void* c,
-                        int m, int n, int k, void* work, cudaStream_t st) {
+cudaError_t launch_swap(const Plan& p, const void* a, const void* w, const float* bias,
+                        const uint16_t* res, void* c, int m, int n, int k, void* work, cudaStream_t st) {
   using Cfg = gemm3::SwapCfg<NP>;
   auto kern = gemm3::k_gemm_swap<NP, ACT, BF>;
   cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
@@ -756,13 +889,13 @@ cudaError_t launch_swap(const Plan& p, const void* a, const void* w, const float
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (p.S == 1 || work)
-    return cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, c, m, n, k, p.per, (float*)work);
+    return cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, res, c, m, n, k, p.per, (float*)work);
   // no caller workspace: stream-ordered pool memory (capturable: inside a CUDA
   // graph it becomes an allocation node)
   float* part = nullptr;
   e = cudaMallocAsync(reinterpret_cast<void**>(&part), p.work, st);
   if (e != cudaSuccess) return e;
-  e = cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, c, m, n, k, p.per, part);
+  e = cudaLaunchKernelEx(&cfg, kern, tw, ta, bias, res, c, m, n, k, p.per, part);
   cudaError_t e2 = cudaFreeAsync(part, st);
   return e != cudaSuccess ? e : e2;
 }
@@ -772,11 +905,11 @@ cudaError_t launch_swap(const Plan& p, const void* a, const void* w, const float
 // 192-wide one 0.853: the narrower MMAs leave the tensor pipe partly idle);
 // ties go to the wider tile
 int pick_bn(int m, int n, int pairs) {
-  const int bns[3] = {256, 192, 128};
-  const double rel[3] = {1.0, 0.853, 0.76};
+  const int bns[4] = {256, 192, 128, 64};
+  const double rel[4] = {1.0, 0.853, 0.76, 0.6};
   int best = 256;
   double best_cost = 1e30;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < (n <= 64 ? 4 : 3); ++i) {
     const int64_t tiles = (int64_t)((m + 255) / 256) * ((n + bns[i] - 1) / bns[i]);
     const double cost = (double)((tiles + pairs - 1) / pairs) * rel[i];
     if (cost < best_cost * 0.97) best = bns[i], best_cost = cost;
@@ -785,41 +918,64 @@ int pick_bn(int m, int n, int pairs) {
 }
 
 template <int ACT, bool BF>
-cudaError_t dispatch(const Plan& p, const void* a, const void* w, const float* bias, void* c, int m,
-                     int n, int k, void* work, cudaStream_t st) {
+cudaError_t dispatch(const Plan& p, const void* a, const void* w, const float* bias,
+                     const uint16_t* res, void* c, int m, int n, int k, void* work, cudaStream_t st) {
   if (p.swap) {
-    if (p.np == 32) return launch_swap<32, ACT, BF>(p, a, w, bias, c, m, n, k, work, st);
-    if (p.np == 64) return launch_swap<64, ACT, BF>(p, a, w, bias, c, m, n, k, work, st);
-    return launch_swap<128, ACT, BF>(p, a, w, bias, c, m, n, k, work, st);  // z tiles of 128 rows
+    if (p.np == 32) return launch_swap<32, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);
+    if (p.np == 64) return launch_swap<64, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);
+    return launch_swap<128, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);  // z tiles of 128 rows
   }
-  if (p.bn == 256) return launch_pair<256, ACT, BF>(a, w, bias, c, m, n, k, st);
-  if (p.bn == 192) return launch_pair<192, ACT, BF>(a, w, bias, c, m, n, k, st);
-  return launch_pair<128, ACT, BF>(a, w, bias, c, m, n, k, st);
+  if (p.bn == 256) return launch_pair<256, ACT, BF>(a, w, bias, res, c, m, n, k, st);
+  if (p.bn == 192) return launch_pair<192, ACT, BF>(a, w, bias, res, c, m, n, k, st);
+  if (p.bn == 64) return launch_pair<64, ACT, BF>(a, w, bias, res, c, m, n, k, st);
+  return launch_pair<128, ACT, BF>(a, w, bias, res, c, m, n, k, st);
 }
 
 }  // namespace
 
+// Implicit-GEMM convolution entry (ee_conv_bf16, eeb200.cu): NHWC bf16 x
+// [n, h, w, c], weight [cout, kh, kw, c], y [n, ho, wo, cout] = act(conv + bias
+// (+ res)); c % 64 == 0, cout % 8 == 0, act 0 or 3.
+cudaError_t ee_conv3_launch(const void* x, const void* w, const float* bias, const void* res, void* y,
+                            int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad,
+                            int act, cudaStream_t st) {
+  const auto* r = static_cast<const uint16_t*>(res);
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (wd + 2 * pad - kw) / stride + 1;
+  const int bn = pick_bn(n * ho * wo, cout, device_sms() / 2);
+  if (act == 3) {
+    if (bn == 256) return launch_conv<256, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+    if (bn == 192) return launch_conv<192, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+    if (bn == 64) return launch_conv<64, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+    return launch_conv<128, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+  }
+  if (bn == 256) return launch_conv<256, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+  if (bn == 192) return launch_conv<192, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+  if (bn == 64) return launch_conv<64, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+  return launch_conv<128, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+}
+
 // Internal entries used by ee_gemm_bf16_ex / ee_gemm_workspace_size
-// (eeb200.cu). path: 0 auto, 1 swap-AB split-K, 2 / 4 / 3 pair with BN =
-// 256 / 192 / 128 (tests pin each path).
+// (eeb200.cu). path: 0 auto, 1 swap-AB split-K, 2 / 4 / 3 / 5 pair with BN =
+// 256 / 192 / 128 / 64 (tests pin each path).
 size_t ee_gemm3_workspace(int m, int n, int k, int splits, int path, int out_bf16) {
   return make_plan(m, n, k, splits, path, out_bf16 != 0).work;
 }
 
-cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, void* c, int out_bf16,
-                            int act, int m, int n, int k, int splits, int path, void* work,
+cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, const void* res, void* c,
+                            int out_bf16, int act, int m, int n, int k, int splits, int path, void* work,
                             size_t work_bytes, cudaStream_t st) {
+  const auto* r = static_cast<const uint16_t*>(res);
   const Plan p = make_plan(m, n, k, splits, path, out_bf16 != 0);
   if (work && work_bytes < p.work) return cudaErrorInvalidValue;
   switch (act * 2 + (out_bf16 ? 1 : 0)) {
-    case 0: return dispatch<0, false>(p, a, w, bias, c, m, n, k, work, st);
-    case 1: return dispatch<0, true>(p, a, w, bias, c, m, n, k, work, st);
-    case 2: return dispatch<1, false>(p, a, w, bias, c, m, n, k, work, st);
-    case 3: return dispatch<1, true>(p, a, w, bias, c, m, n, k, work, st);
-    case 4: return dispatch<2, false>(p, a, w, bias, c, m, n, k, work, st);
-    case 5: return dispatch<2, true>(p, a, w, bias, c, m, n, k, work, st);
-    case 6: return dispatch<3, false>(p, a, w, bias, c, m, n, k, work, st);
-    case 7: return dispatch<3, true>(p, a, w, bias, c, m, n, k, work, st);
+    case 0: return dispatch<0, false>(p, a, w, bias, r, c, m, n, k, work, st);
+    case 1: return dispatch<0, true>(p, a, w, bias, r, c, m, n, k, work, st);
+    case 2: return dispatch<1, false>(p, a, w, bias, r, c, m, n, k, work, st);
+    case 3: return dispatch<1, true>(p, a, w, bias, r, c, m, n, k, work, st);
+    case 4: return dispatch<2, false>(p, a, w, bias, r, c, m, n, k, work, st);
+    case 5: return dispatch<2, true>(p, a, w, bias, r, c, m, n, k, work, st);
+    case 6: return dispatch<3, false>(p, a, w, bias, r, c, m, n, k, work, st);
+    case 7: return dispatch<3, true>(p, a, w, bias, r, c, m, n, k, work, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -276,16 +276,23 @@ class CompactRunner:
     that have not exited) without per-stage host work.
 
     The pipeline is cut into segments, each ending at a ramp (the last one at
-    the final classifier). A segment runs at a power-of-two batch bucket >= its
-    live row count, as a CUDA graph captured once per (segment, bucket):
+    the final classifier). A segment runs at a batch bucket >= its live row
+    count (a multiple of B/16, or a power of two below that), as a CUDA graph
+    captured once per (segment, bucket):
     stages -> ramp head / exit controller (compaction on) -> scatter of the
     exiting rows -> gather of the survivors' activations, request slots and
     alive bytes into the next segment's fixed input buffers (ee_compact_rows /
     ee_compact_meta, all on the device). Rows past the live count inside a
     bucket are padding: alive = 0 and a dummy request slot (index B of the
-    B + 1 result tables), so they never exit, scatter or count. Between
-    segments the host reads the 4-byte survivor count once to pick the next
-    bucket, and stops when nothing survives. Decisions equal EEPipeline.run's
+    B + 1 result tables), so they never exit, scatter or count.
+
+    Bucket choice never stalls the device: every segment's graph copies its
+    survivor count into pinned host memory, and segment k + 1 is launched at
+    the bucket of the count after segment k - 1 (an upper bound of its live
+    rows: counts only fall), which the host reads while segment k runs. The
+    host therefore stays one segment ahead and the GPU never drains between
+    segments; the price is one segment of lag in shrinking. The run stops
+    once a count reaches zero. Decisions equal EEPipeline.run's
     compaction mode (same kernels on the same rows), and rows far from a
     threshold equal feedback mode's."""
 
@@ -298,7 +305,9 @@ class CompactRunner:
         ends = list(pipe.ramp_order) + [len(pipe.stages) - 1]
         starts = [0] + [e + 1 for e in ends[:-1]]
         self.segments = list(zip(starts, ends))
-        self.buckets = sorted({min(b, 1 << k) for k in range(b.bit_length() + 1)})
+        granule = max(1, b // 16)
+        self.buckets = sorted({min(b, 1 << k) for k in range(granule.bit_length() + 1)}
+                              | set(range(granule, b + 1, granule)) | {b})
         dev = "cuda"
         # result tables: B request slots + one dummy slot for padding rows
         self.slots = SlotTable(torch.empty(b + 1, dtype=torch.int32, device=dev),
@@ -308,6 +317,8 @@ class CompactRunner:
         self.ramp_label = torch.empty((R, b + 1), dtype=torch.int32, device=dev)
         self.final_label = torch.empty((b + 1,), dtype=torch.int32, device=dev)
         self.n_live = torch.zeros(len(self.segments), dtype=torch.int32, device=dev)
+        self.n_host = torch.zeros(len(self.segments), dtype=torch.int32, pin_memory=True)
+        self.done = [torch.cuda.Event() for _ in self.segments]
         # each segment's input buffer (capacity B, the activation's own layout)
         self.x_in, self.rows_in, self.alive_in = [], [], []
         h = example
@@ -350,6 +361,7 @@ class CompactRunner:
             compact_rows(h, res.keep, res.n_keep, out=self.x_in[k + 1])
             compact_meta(res.keep, res.n_keep, rows, self.B, self.B, self.rows_in[k + 1],
                          self.alive_in[k + 1], self.n_live[k:k + 1])
+            self.n_host[k:k + 1].copy_(self.n_live[k:k + 1], non_blocking=True)
 
     def _graph(self, k: int, bb: int):
         g = self.graphs.get((k, bb))
@@ -372,11 +384,8 @@ class CompactRunner:
                 return bb
         return self.B
 
-    def run(self, x=None) -> BatchResult:
+    def _reset(self):
         torch = nat.torch_cuda()
-        b = self.B
-        if x is not None:
-            self.x_in[0].copy_(x)
         self.slots.label.fill_(-1)
         self.slots.site.fill_(-1)
         self.slots.err.fill_(float("nan"))
@@ -384,16 +393,29 @@ class CompactRunner:
         self.ramp_label.fill_(-1)
         self.final_label.fill_(-1)
         self.alive_in[0].fill_(1)
-        torch.arange(b, dtype=torch.int32, device="cuda", out=self.rows_in[0])
-        bb = b
+        torch.arange(self.B, dtype=torch.int32, device="cuda", out=self.rows_in[0])
+
+    def run(self, x=None) -> BatchResult:
+        torch = nat.torch_cuda()
+        if x is not None:
+            self.x_in[0].copy_(x)
+        if self.graphs.get("reset") is None:  # the table resets as one graph too
+            self._reset()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=self.pool):
+                self._reset()
+            self.graphs["reset"] = g
+        self.graphs["reset"].replay()
+        bb = self.B
         for k in range(len(self.segments)):
+            if k >= 2:  # the count after segment k - 2 bounds segment k's live rows
+                self.done[k - 2].synchronize()
+                n = int(self.n_host[k - 2])
+                if n == 0:
+                    break
+                bb = self.bucket(n)
             self._graph(k, bb).replay()
-            if k == len(self.segments) - 1:
-                break
-            n = int(self.n_live[k].item())  # 4-byte read: the next bucket
-            if n == 0:
-                break
-            bb = self.bucket(n)
+            self.done[k].record()
         return self.out
 
 
@@ -431,16 +453,23 @@ def fold_batchnorm(model):
     return model
 
 
-def prepare_bf16(model, channels_last: bool):
+def prepare_bf16(model, channels_last: bool, route: bool = True):
     """The serving form of a backbone: bf16 weights and activations; CNNs
-    additionally channels_last with BatchNorm folded into the convolutions
-    (the layout cuDNN's tensor-core convolutions want). In place."""
+    additionally channels_last with BatchNorm folded into the convolutions.
+    route: a ResNet's blocks then run on the repo's kernels (convnet.py:
+    1x1 convolutions as tcgen05 GEMMs with bias / ReLU / shortcut fused, one
+    fused epilogue pass after each spatial convolution); False keeps the
+    library path (cuDNN convolutions + PyTorch elementwise kernels). In place."""
     import torch
 
     if channels_last:
         fold_batchnorm(model)
         model.to(memory_format=torch.channels_last)
     model.to(torch.bfloat16)
+    if channels_last and route and hasattr(model, "layer4"):
+        from paper_2312_05385_b200.convnet import route_resnet
+
+        route_resnet(model)
     return model
 
 

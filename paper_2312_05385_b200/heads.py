@@ -217,11 +217,12 @@ ACTS = {None: 0, "none": 0, "gelu": 1, "gelu_tanh": 2, "relu": 3}
 
 
 def gemm(x, weight, bias=None, *, act=None, out_bf16: bool = True, path: int = 0,
-         splits: int = 0, out=None):
+         splits: int = 0, out=None, res=None):
     """act(x bf16 [M, K] @ weight bf16 [N, K]^T + bias) on the tcgen05 kernels of
     csrc/gemm.cu (ee_gemm_bf16_ex): the persistent CTA-pair kernel for M > 256, the
     swap-AB weight-streaming kernel (cluster split-K) for M <= 256. `act` is fused
-    into the epilogue ("gelu" = erf form, "gelu_tanh", "relu"). x may have leading
+    into the epilogue ("gelu" = erf form, "gelu_tanh", "relu"), after adding the
+    optional bf16 residual `res` ([M, N] like the output). x may have leading
     batch dimensions; they are flattened into M."""
     torch = nat.torch_cuda()
     if x.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
@@ -252,8 +253,13 @@ def gemm(x, weight, bias=None, *, act=None, out_bf16: bool = True, path: int = 0
         _WORK_BYTES[key] = wb
     # split-K partials in torch's stream-ordered (and CUDA-graph-aware) allocator
     work = torch.empty(wb, dtype=torch.uint8, device=x.device) if wb else None
-    nat.check(lib.ee_gemm_bf16_ex(
-        nat.workspace(), x2.data_ptr(), weight.data_ptr(), nat.ptr(b), out.data_ptr(),
+    r = None
+    if res is not None:
+        r = res.reshape(-1, n)
+        if r.dtype != torch.bfloat16 or r.shape[0] != m or not r.is_contiguous():
+            raise ParameterError("res must be a contiguous bf16 [M, N] tensor")
+    nat.check(lib.ee_gemm_bf16_res(
+        nat.workspace(), x2.data_ptr(), weight.data_ptr(), nat.ptr(b), nat.ptr(r), out.data_ptr(),
         int(out_bf16), ACTS[act], m, n, k, splits, path, nat.ptr(work), wb,
         nat.stream_handle(torch)))
     return out.view(*lead, n)

@@ -113,6 +113,7 @@ PATH_CASES = [
     (2, 257, 256, 64), (2, 1000, 700, 136), (2, 8192, 2304, 768), (2, 2048, 4096, 4096),
     (4, 600, 776, 1000), (4, 8192, 768, 3072),
     (3, 777, 136, 72), (3, 4096, 1024, 512),
+    (5, 5000, 64, 576), (5, 300, 40, 128), (5, 1000, 200, 64),  # 64-wide tiles (one-chunk epilogue)
 ]
 
 
@@ -186,3 +187,24 @@ def test_gemm3_leading_dims_and_errors(cuda):
         gemm(x.float(), w)
     with pytest.raises(ParameterError):
         gemm(x, w, act="swish")
+
+
+@pytest.mark.parametrize("path,m,n,k,splits", [(0, 4000, 256, 64, 0), (3, 1000, 512, 128, 0),
+                                               (1, 100, 256, 512, 4), (1, 60, 1024, 256, 1)])
+@pytest.mark.parametrize("act", [None, "relu"])
+def test_gemm3_residual_epilogue(cuda, path, m, n, k, splits, act):
+    """act(A W^T + bias + R): a bottleneck's conv3 + shortcut + ReLU in one
+    kernel, on the pair kernel (TMA-store epilogue) and on the swap kernel
+    (unsplit stores and the split-K reduction)."""
+    from paper_2312_05385_b200.heads import gemm
+
+    g = torch.Generator().manual_seed(m + n + k)
+    a = torch.randn(m, k, generator=g).to(torch.bfloat16)
+    w = torch.randn(n, k, generator=g).to(torch.bfloat16) * 0.1
+    bias = torch.randn(n, generator=g)
+    r = torch.randn(m, n, generator=g).to(torch.bfloat16)
+    ref = a.float() @ w.float().t() + bias + r.float()
+    ref = torch.relu(ref) if act == "relu" else ref
+    got = gemm(a.cuda(), w.cuda(), bias.cuda(), act=act, path=path, splits=splits, res=r.cuda()).float().cpu()
+    scale = ref.abs().max().item()
+    assert (got - ref).abs().max().item() <= 8e-3 * scale
