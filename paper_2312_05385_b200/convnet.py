@@ -141,12 +141,13 @@ class Conv:
         (sh, sw), (ph, pw) = self.stride, self.padding
         if sh != sw or ph != pw:
             raise ParameterError("square strides and paddings only")
-        kp = (kh * kw * c + 63) // 64 * 64
+        seg = (kw * c + 7) // 8 * 8  # filter row r owns columns [r seg, r seg + kw c)
+        kp = (kh * seg + 63) // 64 * 64
         if getattr(self, "w_cols", None) is None or self.w_cols.shape[1] != kp:
             cout = self.w.shape[0]
-            wc = torch.zeros((cout, kp), dtype=torch.bfloat16, device=x.device)
-            wc[:, : kh * kw * c] = self.w.permute(0, 2, 3, 1).reshape(cout, -1)
-            self.w_cols = wc
+            wc = torch.zeros((cout, kh, seg), dtype=torch.bfloat16, device=x.device)
+            wc[:, :, : kw * c] = self.w.permute(0, 2, 3, 1).reshape(cout, kh, kw * c)
+            self.w_cols = torch.nn.functional.pad(wc.reshape(cout, kh * seg), (0, kp - kh * seg)).contiguous()
         ho, wo = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
         a = torch.empty((b * ho * wo, kp), dtype=torch.bfloat16, device=x.device)
         nat.check(nat.load_library().ee_im2col_bf16(

@@ -2653,15 +2653,18 @@ int ee_im2col_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, 
   if (n < 1 || h < 1 || w < 1 || c < 1 || kh < 1 || kw < 1 || stride < 1 || pad < 0 ||
       kh > h + 2 * pad || kw > w + 2 * pad)
     return fail(EE_ERR_ARG, "bad convolution shape");
-  if (kp % 64 || kp < kh * kw * c) return fail(EE_ERR_ARG, "kp must be a multiple of 64 >= kh*kw*c");
+  const int seg = (kw * c + 7) / 8 * 8;
+  if (kp % 64 || kp < kh * seg) return fail(EE_ERR_ARG, "kp must be a multiple of 64 >= kh * roundup8(kw * c)");
   if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
   if (reinterpret_cast<uintptr_t>(d_out) & 15) return fail(EE_ERR_ARG, "output must be 16-byte aligned");
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
-  const int64_t m = n * ho * wo;
-  const int64_t nv = m * (kp / 8);
-  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(nv, 256), (int64_t)sm_count() * 16);
-  convaux::k_im2col_nhwc<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<const uint16_t*>(d_x), h, w, c, kh, kw, stride, pad, ho, wo, m, kp,
+  const int64_t rows = n * ho;  // one CTA per output row
+  const size_t smem = (size_t)kh * (w + 2 * pad) * c * 2;
+  if (rows > 0x7fffffff || smem > 200 * 1024) return fail(EE_ERR_ARG, "im2col rows too large");
+  if (smem > 48 * 1024)
+    EE_CUDA(cudaFuncSetAttribute(convaux::k_im2col_nhwc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  convaux::k_im2col_nhwc<<<(unsigned)rows, convaux::IM2COL_THREADS, smem, (cudaStream_t)stream>>>(
+      static_cast<const uint16_t*>(d_x), h, w, c, kh, kw, stride, pad, ho, wo, kp, seg,
       static_cast<uint4*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;

@@ -58,6 +58,13 @@ def _worker(rank, world, port, q):
         res.append(eval_thresholds_host_sharded(
             np.ascontiguousarray(arrays.errs[lo:hi]), arrays.correct[lo:hi].astype(np.float64),
             evf.serve, evf.vanilla_ms, diag, n_total=arrays.n))
+        # two windows per rank, one all-reduce for both
+        from paper_2312_05385_b200.distributed import evaluate_windows
+
+        other = synth.config4_window(60_001, seed=7)
+        sw2 = ShardedSweep(other, sites, prof, rank=rank, world=world)
+        wa, ws = evaluate_windows([sw, sw2], rnd)
+        res += [(wa[0], ws[0]), (wa[1], ws[1])]
         q.put((rank, [(a.tolist(), s.tolist()) for a, s in res]))
     finally:
         dist.destroy_process_group()
@@ -78,6 +85,8 @@ def test_two_rank_sweep_matches_one_gpu(cuda):
     one = [ShardedSweep(arrays, sites, prof).evaluate_many(th) for th in (diag, rnd)]
     one += one + one[:1]  # the overlapped exchange: diag, rnd, diag
     one += one[:1]  # host shards through eval_thresholds_host_sharded: diag
+    other = synth.config4_window(60_001, seed=7)
+    one += [one[1], ShardedSweep(other, sites, prof).evaluate_many(rnd)]  # evaluate_windows
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
