@@ -291,6 +291,11 @@ int ee_conv_bf16(ee_workspace* ws, const void* d_x, int64_t n, int32_t h, int32_
                  const void* d_w, int32_t cout, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
                  const float* d_bias, const void* d_res, int32_t act, void* d_y, void* stream);
 
+/* The reference's sequential fp64 sum of each row of d_vals [rows, n]
+ * (((0 + v0) + v1) + ...), every addition rounded, as _exitcore.pyx:43-53
+ * folds serve times), bit for bit, one warp per row; the fold ee_tune uses. */
+int ee_sequential_sum(const double* d_vals, int32_t n, int32_t rows, double* d_out, void* stream);
+
 /* im2col of an NHWC bf16 map for a convolution with too few input channels
  * for ee_conv_bf16 (the 3-channel stem): out bf16 [n*ho*wo, kp]; filter row r
  * owns columns [r * seg, r * seg + kw * c) with seg = kw * c rounded up to 8

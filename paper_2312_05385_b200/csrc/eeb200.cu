@@ -497,6 +497,7 @@ __global__ void k_finalize(const unsigned long long* __restrict__ hist,
 #include "sweep_diag2.cuh"
 #include "sweep_diag3.cuh"
 #include "sweep_axis.cuh"
+#include "ordered_sum.cuh"
 #include "tune_device.cuh"
 #include "exit_controller.cuh"
 #include "pool.cuh"
@@ -2648,6 +2649,25 @@ __global__ void k_bias_act_bf16(const uint4* x, const float* __restrict__ bias,
 }
 
 extern "C" {
+}  // extern "C"
+// one warp per row: the reference's sequential sum of that row (osum)
+__global__ void k_sequential_sum(const double* __restrict__ v, int n, int rows, double* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const double* r = v + (int64_t)row * n;
+  const double s = osum::warp_ordered_sum(0.0, n, [&](int i) { return r[i]; });
+  if ((threadIdx.x & 31) == 0) out[row] = s;
+}
+extern "C" {
+int ee_sequential_sum(const double* d_vals, int32_t n, int32_t rows, double* d_out, void* stream) {
+  if (n < 0 || rows < 0) return fail(EE_ERR_ARG, "negative shape");
+  if (rows == 0) return EE_OK;
+  if (!d_out || (n > 0 && !d_vals)) return fail(EE_ERR_ARG, "null pointer");
+  k_sequential_sum<<<(unsigned)ceil_div(rows, 8), 256, 0, (cudaStream_t)stream>>>(d_vals, n, rows, d_out);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
 int ee_im2col_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, int32_t kh, int32_t kw,
                    int32_t stride, int32_t pad, int32_t kp, void* d_out, void* stream) {
   if (n < 1 || h < 1 || w < 1 || c < 1 || kh < 1 || kw < 1 || stride < 1 || pad < 0 ||

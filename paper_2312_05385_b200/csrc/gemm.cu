@@ -20,8 +20,8 @@
 //
 // k_gemm_swap  (M <= 256: decode steps, ramp heads on a batch)
 //   Weight streaming. The roles of the operands swap: W is the MMA's M side
-//   (128 output features per CTA) and up to 128 activation rows are its N side
-//   (32 / 64 / 128; more rows take more CTAs along z). The K range is split
+//   (128 output features per CTA) and up to 256 activation rows are its N side
+//   (32 / 64 / 128 / 256, so the weights stream once per call). The K range is split
 //   over a cluster of S CTAs along x: each CTA writes its fp32 partial tile to
 //   an L2-resident workspace slot, one cluster barrier (release/acquire at
 //   cluster scope), then rank s sums activation rows s, s + S, ... over the S
@@ -474,7 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
 // ===========================================================================
 template <int NP>
 struct SwapCfg {
-  static_assert(NP == 32 || NP == 64 || NP == 128, "activation rows per CTA");
+  static_assert(NP == 32 || NP == 64 || NP == 128 || NP == 256, "activation rows per CTA");
   static constexpr int W_BYTES = 128 * BK * 2;
   static constexpr int A_BYTES = NP * BK * 2;
   static constexpr int STAGE = W_BYTES + A_BYTES;
@@ -484,7 +484,7 @@ struct SwapCfg {
   static constexpr int STAGES_MAX = (SMEM_LIMIT / CTAS_PER_SM - 2048) / STAGE;
   static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
   static constexpr int SMEM = 1024 + STAGES * STAGE;
-  static constexpr int TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : 128;
+  static constexpr int TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
 };
 
 template <int NP, int ACT, bool OUT_BF16>
@@ -827,7 +827,7 @@ cudaError_t launch_conv(const void* x, const void* w, const float* bias, const u
 // how one call runs (host-side plan; the workspace query uses the same one)
 struct Plan {
   bool swap = false;
-  int np = 32;       // swap: activation rows per CTA (32 / 64 / 128)
+  int np = 32;       // swap: activation rows per CTA (32 / 64 / 128 / 256)
   int S = 1;         // swap: split count = cluster size
   int per = 1;       // swap: k-tiles per split
   int bn = 256;      // pair: tile width
@@ -846,7 +846,8 @@ Plan make_plan(int m, int n, int k, int splits, int path, bool bf) {
     p.bn = path == 3 ? 128 : path == 2 ? 256 : path == 4 ? 192 : path == 5 ? 64 : pick_bn(m, n, device_sms() / 2);
     return p;
   }
-  p.np = m <= 32 ? 32 : m <= 64 ? 64 : 128;
+  // one z tile up to 256 rows: the weights stream once per call
+  p.np = m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256;
   const int zt = (m + p.np - 1) / p.np;
   const int ft = (n + 127) / 128;
   const int kt_n = (k + gemm3::BK - 1) / gemm3::BK;
@@ -923,7 +924,8 @@ cudaError_t dispatch(const Plan& p, const void* a, const void* w, const float* b
   if (p.swap) {
     if (p.np == 32) return launch_swap<32, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);
     if (p.np == 64) return launch_swap<64, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);
-    return launch_swap<128, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);  // z tiles of 128 rows
+    if (p.np == 128) return launch_swap<128, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);
+    return launch_swap<256, ACT, BF>(p, a, w, bias, res, c, m, n, k, work, st);  // z tiles of 256 rows
   }
   if (p.bn == 256) return launch_pair<256, ACT, BF>(a, w, bias, res, c, m, n, k, st);
   if (p.bn == 192) return launch_pair<192, ACT, BF>(a, w, bias, res, c, m, n, k, st);

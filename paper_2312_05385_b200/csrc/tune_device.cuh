@@ -68,10 +68,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   // exact evaluation of rows cand[0..nc): every sample's first exit in parallel,
   // written as its serve value (the fold's addend) while the correct counts are
-  // summed with ballots (integer sums are order-free); then one thread per
-  // candidate folds the addends in index order (same order as
-  // _exitcore.pyx:43-53), a chain of n dependent adds with the next 8 addends
-  // always loaded ahead of it.
+  // summed with ballots (integer sums are order-free); then one warp per
+  // candidate folds the addends in index order (same order and the same
+  // roundings as _exitcore.pyx:43-53; osum::warp_ordered_sum).
   const int n8 = (n + 7) & ~7;
   __shared__ unsigned okc[MAXR + 1];  // n <= EE_TUNE_N_MAX: 32-bit counts, native shared atomics
   auto evaluate = [&](int nc) {
@@ -124,28 +123,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     }
     __syncthreads();
-    if (tid < nc) {
-      const double* vr = vals + (int64_t)tid * n8;
-      double ms = 0.0;
-      const int nfull = n & ~7;
-      double cur[8], nxt[8];
-      if (nfull > 0) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) cur[q] = vr[q];
+    // the fold: a warp per candidate sums the addends in index order, bit for
+    // bit the sequential chain, 128 at a time (osum::warp_ordered_sum)
+    for (int c = tid >> 5; c < nc; c += THREADS / 32) {
+      const double* vr = vals + (int64_t)c * n8;
+      const double ms = osum::warp_ordered_sum(0.0, n, [&](int i) { return vr[i]; });
+      if (lane == 0) {
+        const double dn = (double)n;
+        accs[c] = __ddiv_rn((double)okc[c], dn);
+        savs[c] = __dsub_rn(vanilla, __ddiv_rn(ms, dn));
       }
-      for (int i0 = 0; i0 < nfull; i0 += 8) {
-        const int i1 = i0 + 8 < nfull ? i0 + 8 : i0;  // loads ahead of the dependent adds
-#pragma unroll
-        for (int q = 0; q < 8; ++q) nxt[q] = vr[i1 + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) ms = __dadd_rn(ms, cur[q]);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
-      }
-      for (int i = nfull; i < n; ++i) ms = __dadd_rn(ms, vr[i]);
-      const double dn = (double)n;
-      accs[tid] = __ddiv_rn((double)okc[tid], dn);
-      savs[tid] = __dsub_rn(vanilla, __ddiv_rn(ms, dn));
     }
     __syncthreads();
   };

@@ -109,7 +109,7 @@ def _ref_act(y, act):
 # tile edge; k spans one to many k-tiles; several persistent tiles per pair.
 PATH_CASES = [
     (1, 1, 64, 64), (1, 32, 3072, 1024), (1, 33, 130, 200), (1, 100, 1000, 2048),
-    (1, 300, 777, 520), (1, 256, 50257, 256),
+    (1, 300, 777, 520), (1, 256, 50257, 256), (1, 160, 3072, 1024), (1, 200, 1024, 4096),
     (2, 257, 256, 64), (2, 1000, 700, 136), (2, 8192, 2304, 768), (2, 2048, 4096, 4096),
     (4, 600, 776, 1000), (4, 8192, 768, 3072),
     (3, 777, 136, 72), (3, 4096, 1024, 512),
