@@ -377,6 +377,12 @@ int ee_l2_flush(void* d_buf, int64_t bytes, void* stream);
  * last CTA, finalised). NULL turns it off. */
 int ee_diag_trace(ee_workspace* ws, uint64_t* d_trace);
 
+/* Profiling aid: while d_cycles (device i64 [8]) is set, ee_tune writes the
+ * clock64 cycles its thread 0 spent per phase over the whole hill climb:
+ * candidate rows, the exit scan, the ordered fold, the selection, the state
+ * update. NULL turns it off. */
+int ee_tune_profile(ee_workspace* ws, int64_t* d_cycles);
+
 /* Per-launch timing: while enabled, every kernel launched through `ws` is
  * bracketed by CUDA events on its stream. ee_profile_read synchronises, writes
  * {"kernel": {"launches": L, "ms": T}, ...} (JSON) into buf and resets. */

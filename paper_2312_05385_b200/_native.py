@@ -68,6 +68,7 @@ SIGNATURES = {
     "ee_eval_counts_host": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i32, _vp, _c_i64, _vp, _vp, _c_i32, _vp]),
     "ee_pack_correct_host": (ctypes.c_int, [_vp, _c_i64, _c_i32, _vp, _c_i32]),
     "ee_diag_trace": (ctypes.c_int, [_vp, _vp]),
+    "ee_tune_profile": (ctypes.c_int, [_vp, _vp]),
     "ee_l2_flush": (ctypes.c_int, [_vp, _c_i64, _vp]),
     "ee_profile_read": (ctypes.c_int, [_vp, ctypes.c_char_p, _c_i64]),
     "ee_tune": (

@@ -569,6 +569,7 @@ struct ee_workspace {
   unsigned long long* d_axis_tot = nullptr;  // [2][ncell]: counts, then deltas/corrects
   size_t axis_tot_cap = 0;
   unsigned long long* d_diag_trace = nullptr;  // set by ee_diag_trace (profiling)
+  long long* d_tune_prof = nullptr;             // set by ee_tune_profile (profiling)
   struct Mark {
     const char* name;
     cudaEvent_t a, b;
@@ -2014,6 +2015,13 @@ int ee_l2_flush(void* d_buf, int64_t bytes, void* stream) {
   return EE_OK;
 }
 
+int ee_tune_profile(ee_workspace* ws, int64_t* d_cycles) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  std::lock_guard<std::mutex> lock(ws->mu);
+  ws->d_tune_prof = reinterpret_cast<long long*>(d_cycles);
+  return EE_OK;
+}
+
 int ee_diag_trace(ee_workspace* ws, uint64_t* d_trace) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
   std::lock_guard<std::mutex> lock(ws->mu);
@@ -2096,7 +2104,7 @@ int ee_tune(ee_workspace* ws, const double* d_scores, const uint32_t* d_bits, in
   double* d_out = reinterpret_cast<double*>(hd);
   int* d_info = reinterpret_cast<int*>(hd + (size_t)(r + 2) * 8);
   double* d_trace = reinterpret_cast<double*>(hd + out_b);
-  tunedev::Params p{acc_loss_budget, init_step, min_step, max_rounds, trace_cap, {}};
+  tunedev::Params p{acc_loss_budget, init_step, min_step, max_rounds, trace_cap, {}, ws->d_tune_prof};
   for (int j = 0; j <= r; ++j) p.serve[j] = h_serve[j];
   const size_t n8 = (size_t)((n + 7) & ~7);
   const size_t rows_b = n8 * 4 + (size_t)(r + 1) * n8 * 8;

@@ -18,6 +18,7 @@ struct Params {
   int max_rounds;  // reference raises after 200000
   int trace_cap;   // rows of `trace` available (r doubles each)
   double serve[MAXR + 1];  // serve table (by value: no staging copy)
+  long long* prof;         // optional: clock64 cycles per phase [8] (ee_tune_profile)
 };
 
 // out_d: [0, r) thresholds, r: savings, r+1: accuracy
@@ -73,6 +74,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   // roundings as _exitcore.pyx:43-53; osum::warp_ordered_sum).
   const int n8 = (n + 7) & ~7;
   __shared__ unsigned okc[MAXR + 1];  // n <= EE_TUNE_N_MAX: 32-bit counts, native shared atomics
+  // optional phase profile (thread 0's clock): 0 candidates, 1 scan, 2 fold, 3 select, 4 update
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+  auto mark = [&](int k) {
+    if (p.prof && tid == 0) {
+      const long long t = clock64();
+      ph[k] += t - tc;
+      tc = t;
+    }
+  };
   auto evaluate = [&](int nc) {
     if (tid <= MAXR) okc[tid] = 0;
     __syncthreads();
@@ -123,6 +134,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     }
     __syncthreads();
+    mark(1);
     // the fold: a warp per candidate sums the addends in index order, bit for
     // bit the sequential chain, 128 at a time (osum::warp_ordered_sum)
     for (int c = tid >> 5; c < nc; c += THREADS / 32) {
@@ -135,6 +147,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     __syncthreads();
+    mark(2);
   };
 
   if (tid < r) cand[0][tid] = 0.0;
@@ -179,21 +192,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       cand[pos][j] = v;
     }
     __syncthreads();
+    mark(0);
     evaluate(nelig);
     __shared__ int s_best;
     __shared__ unsigned s_viol;
     __shared__ bool s_allmin;
     if (tid < 32) {
       // every eligible increment scored by its own lane; key (1, dsav, -i) when
-      // it loses no accuracy, else (0, dsav / dloss, dsav, -i); the warp keeps
-      // the lexicographic max (tuner.py:141-153). -i makes the max unique, so
-      // the reduction picks what the reference's in-order scan picks.
+      // it loses no accuracy, else (0, dsav / dloss, dsav, -i)
       const int pos = tid;
       const bool valid = pos < nelig;
       const int i = valid ? elig[pos] : 0;
       const bool viol_me = valid && accs[pos] < floor_eps;
       bool ok = valid && !viol_me;
-      int k0 = 0, k3 = -i;
+      int k0 = 0;
       double k1 = 0.0, k2 = 0.0;
       if (ok) {
         const double dsav = __dsub_rn(savs[pos], sav_cur);
@@ -206,28 +218,40 @@ __global__ void __launch_bounds__(THREADS, 1)
           k2 = dsav;
         }
       }
-      int best = ok ? pos : -1;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const bool ok2 = __shfl_xor_sync(0xffffffffu, ok, o);
-        const int a0 = __shfl_xor_sync(0xffffffffu, k0, o), a3 = __shfl_xor_sync(0xffffffffu, k3, o);
-        const double a1 = __shfl_xor_sync(0xffffffffu, k1, o), a2 = __shfl_xor_sync(0xffffffffu, k2, o);
-        const int b2 = __shfl_xor_sync(0xffffffffu, best, o);
-        bool take;
-        if (!ok2)
-          take = false;
-        else if (!ok)
-          take = true;
-        else if (a0 != k0)
-          take = a0 > k0;
-        else if (a1 != k1)
-          take = a1 > k1;
-        else if (k0 == 0 && a2 != k2)
-          take = a2 > k2;
-        else
-          take = a3 > k3;
-        if (take) ok = true, k0 = a0, k1 = a1, k2 = a2, k3 = a3, best = b2;
+      mark(5);
+      // lane 0 scans the keys in index order keeping the first maximum: the
+      // reference's in-order scan itself (tuner.py:141-153)
+      __shared__ double s_k1[MAXR], s_k2[MAXR];
+      __shared__ int s_k0[MAXR], s_ok[MAXR];
+      if (valid) {
+        s_ok[pos] = ok;
+        s_k0[pos] = k0;
+        s_k1[pos] = k1;
+        s_k2[pos] = k2;
       }
+      __syncwarp();
+      int best = -1;
+      if (pos == 0) {
+        int b0 = 0;
+        double b1 = 0.0, b2 = 0.0;
+        for (int q = 0; q < nelig; ++q) {
+          if (!s_ok[q]) continue;
+          const int c0 = s_k0[q];
+          const double c1 = s_k1[q], c2 = s_k2[q];
+          bool take = best < 0;
+          if (!take) {
+            if (c0 != b0)
+              take = c0 > b0;
+            else if (c1 != b1)
+              take = c1 > b1;
+            else if (c0 == 0 && c2 != b2)
+              take = c2 > b2;
+            // equal keys: the earlier index (larger -i) wins
+          }
+          if (take) best = q, b0 = c0, b1 = c1, b2 = c2;
+        }
+      }
+      mark(6);
       unsigned vm = viol_me ? 1u << i : 0u;
 #pragma unroll
       for (int o = 16; o; o >>= 1) vm |= __shfl_xor_sync(0xffffffffu, vm, o);
@@ -240,6 +264,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     __syncwarp();
+    mark(3);
     if (tid == 0) {
       n_evals += nelig;
       const int best = s_best;
@@ -271,8 +296,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     __syncthreads();
+    mark(4);
     if (done) break;
   }
+  if (p.prof && tid == 0)
+    for (int k = 0; k < 8; ++k) p.prof[k] = ph[k];
   if (tid == 0) {
     if (status == 0 && acc_cur < __dsub_rn(floor, 1e-9)) status = 1;
     out_i[0] = rounds;
