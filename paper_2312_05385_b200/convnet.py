@@ -91,7 +91,7 @@ class Conv:
         cin, cout = x.shape[1], self.w.shape[0]
         if cin % 64 == 0 and cout % 8 == 0 and not (self.pointwise and self.stride == (1, 1)):
             return self._implicit_gemm(x, act, res)
-        if cout % 8 == 0 and not self.pointwise:
+        if cout % 8 == 0 and not self.pointwise and (x.shape[3] * cin) % 8 == 0:
             return self._explicit_im2col(x, act, res)
         if self.pointwise and x.shape[1] % 8 == 0:
             if self.stride != (1, 1):

@@ -4,52 +4,70 @@
 // k_im2col_nhwc: a convolution whose input channels are too few for the
 //   implicit-GEMM kernel's 64-channel TMA im2col tiles (the 3-channel ImageNet
 //   stem) gets its A operand written out once: row m = output pixel (n, oh, ow),
-//   column (r, s, c) at r * seg + s * c + c (seg = kw * c rounded up to 8), zero
-//   in the gaps, past kh * seg up to kp (a multiple of 64) and outside the image.
+//   column (r, s, c) at r * seg + s * c + c (seg = kw * c rounded up to 8; the
+//   gap columns meet zero weights), zero past kh * seg up to kp (a multiple of
+//   64) and outside the image.
 // k_maxpool_nhwc: max pooling of an NHWC bf16 map, 8 channels per 16-byte
 //   vector per thread, padding = -inf (PyTorch's semantics).
 #pragma once
 
 namespace convaux {
 
-// One CTA per output row (n, oh): the kh input rows it needs (zero rows outside
-// the image, zero columns for the horizontal padding) are staged in shared
-// memory. Column layout: filter row r owns the `seg`-wide segment
-// [r * seg, r * seg + kw * c) (seg = kw * c rounded up to 8; the weight is laid
-// out the same way, zeros in the gaps), so every 16-byte output chunk copies up
-// to 8 CONTIGUOUS elements of one staged row: no division per element, and
-// the wo x kp block is written as consecutive coalesced chunks.
+// One CTA per output row (n, oh). The kh input rows it needs are staged in
+// shared memory with 16-byte copies, each behind lp >= pad * c zero elements
+// (lp a multiple of 8, so the copies stay aligned) and followed by zeros for
+// the right padding; rows outside the image stay zero. Column layout of the
+// output: filter row r owns the `seg`-wide segment [r * seg, r * seg + kw * c)
+// (seg = kw * c rounded up to 8; the weight is laid out the same way, zero in
+// the gaps), so each 16-byte output chunk is 8 CONTIGUOUS staged elements:
+// five 32-bit shared loads and a funnel shift, no per-element index math. The
+// gap columns pick up neighbouring (finite) staged values, which meet zero
+// weights. Thread t writes chunk t % chunks of pixels t / chunks, + PIX, ...:
+// consecutive threads write consecutive 16-byte chunks.
 constexpr int IM2COL_THREADS = 256;
 __global__ void __launch_bounds__(IM2COL_THREADS)
     k_im2col_nhwc(const uint16_t* __restrict__ x, int h, int w, int c, int kh, int kw, int stride,
-                  int pad, int ho, int wo, int kp, int seg, uint4* __restrict__ out) {
-  extern __shared__ uint16_t srow[];  // [kh][wp * c], wp = w + 2 pad (padded row)
-  const int wp = w + 2 * pad;
-  const int rowlen = wp * c;
+                  int pad, int ho, int wo, int kp, int seg, int lp, int rowlen,
+                  uint4* __restrict__ out) {
+  extern __shared__ __align__(16) uint16_t srow[];  // [kh][rowlen]
   const int64_t img = blockIdx.x / ho;
   const int oh = (int)(blockIdx.x - img * ho);
-  for (int q = threadIdx.x; q < kh * rowlen; q += IM2COL_THREADS) {
-    const int r = q / rowlen, col = q - r * rowlen;
+  uint4* s4 = reinterpret_cast<uint4*>(srow);
+  const int n4 = kh * rowlen / 8;
+  for (int q = threadIdx.x; q < n4; q += IM2COL_THREADS) s4[q] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  const int v_row = w * c / 8;  // 16-byte vectors per input row
+  for (int q = threadIdx.x; q < kh * v_row; q += IM2COL_THREADS) {
+    const int r = q / v_row, v = q - r * v_row;
     const int ih = oh * stride - pad + r;
-    const int iw = col / c - pad;
-    uint16_t v = 0;
-    if (ih >= 0 && ih < h && iw >= 0 && iw < w) v = __ldg(x + ((img * h + ih) * w) * c + (int64_t)iw * c + col % c);
-    srow[q] = v;
+    if (ih < 0 || ih >= h) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(x + (img * h + ih) * (int64_t)w * c);
+    s4[(r * rowlen + lp) / 8 + v] = __ldg(src + v);
   }
   __syncthreads();
-  const int chunks = kp / 8, segc = seg / 8, span = kw * c;
-  uint4* dst = out + (int64_t)blockIdx.x * wo * chunks;
-  for (int q = threadIdx.x; q < wo * chunks; q += IM2COL_THREADS) {
-    const int ow = q / chunks, ch = q - ow * chunks;
-    const int r = ch / segc, e0 = (ch - r * segc) * 8;  // filter row, first element in its segment
-    uint32_t o[4] = {0u, 0u, 0u, 0u};
+  const int chunks = kp / 8, segc = seg / 8;
+  const int PIX = IM2COL_THREADS / chunks;
+  const int ci = threadIdx.x % chunks, pix0 = threadIdx.x / chunks;
+  if (pix0 >= PIX) return;
+  const int r = ci / segc, e0 = (ci - r * segc) * 8;
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(srow);
+  const int obase = r * rowlen + lp - pad * c + e0;  // staged element of (ow = 0, this chunk)
+  uint4* dst = out + (int64_t)blockIdx.x * wo * chunks + ci;
+  for (int ow = pix0; ow < wo; ow += PIX) {
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
     if (r < kh) {
-      const uint16_t* src = srow + r * rowlen + ow * stride * c + e0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e0 + e < span) o[e >> 1] |= (uint32_t)src[e] << (16 * (e & 1));
+      const int e = obase + ow * stride * c;
+      const uint32_t* wp = s32 + (e >> 1);
+      const uint32_t a0 = wp[0], a1 = wp[1], a2 = wp[2], a3 = wp[3];
+      if (e & 1) {
+        const uint32_t a4 = wp[4];
+        o = make_uint4(__funnelshift_r(a0, a1, 16), __funnelshift_r(a1, a2, 16),
+                       __funnelshift_r(a2, a3, 16), __funnelshift_r(a3, a4, 16));
+      } else {
+        o = make_uint4(a0, a1, a2, a3);
+      }
     }
-    dst[q] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[(int64_t)ow * chunks] = o;
   }
 }
 

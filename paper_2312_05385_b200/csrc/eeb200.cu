@@ -2686,13 +2686,20 @@ int ee_im2col_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, 
   if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
   if (reinterpret_cast<uintptr_t>(d_out) & 15) return fail(EE_ERR_ARG, "output must be 16-byte aligned");
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  if ((w * c) % 8 || (reinterpret_cast<uintptr_t>(d_x) & 15))
+    return fail(EE_ERR_ARG, "im2col needs 16-byte input rows (w * c % 8 == 0, aligned x)");
+  if (kp / 8 > convaux::IM2COL_THREADS) return fail(EE_ERR_ARG, "kp too large");
   const int64_t rows = n * ho;  // one CTA per output row
-  const size_t smem = (size_t)kh * (w + 2 * pad) * c * 2;
+  // staged row: lp zeros (>= the left padding, 8-aligned), the input row, zeros for
+  // the right padding and 16 elements of slack for the last chunk's 5-word read
+  const int lp = (pad * c + 7) / 8 * 8;
+  const int rowlen = (lp + w * c + pad * c + 16 + 7) / 8 * 8;
+  const size_t smem = (size_t)kh * rowlen * 2;
   if (rows > 0x7fffffff || smem > 200 * 1024) return fail(EE_ERR_ARG, "im2col rows too large");
   if (smem > 48 * 1024)
     EE_CUDA(cudaFuncSetAttribute(convaux::k_im2col_nhwc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   convaux::k_im2col_nhwc<<<(unsigned)rows, convaux::IM2COL_THREADS, smem, (cudaStream_t)stream>>>(
-      static_cast<const uint16_t*>(d_x), h, w, c, kh, kw, stride, pad, ho, wo, kp, seg,
+      static_cast<const uint16_t*>(d_x), h, w, c, kh, kw, stride, pad, ho, wo, kp, seg, lp, rowlen,
       static_cast<uint4*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;

@@ -13,7 +13,7 @@ for r in rows[1:]:
     names[r[idi]] = r[ki]
 tot = collections.defaultdict(lambda: [0, 0.0, 0.0])
 scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
-bsc = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+bsc = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Kbyte ": 1e-3}
 for i, m in per.items():
     t, u = m["gpu__time_duration.sum"]
     t *= scale.get(u, 1.0)
@@ -26,4 +26,4 @@ all_t = sum(v[1] for v in tot.values())
 print(f"total {all_t:.1f} us over {sum(v[0] for v in tot.values())} launches")
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 for n, (c, t, mb) in sorted(tot.items(), key=lambda kv: -kv[1][1])[:top]:
-    print(f"{t:9.1f} us {100*t/all_t:5.1f}% x{c:3d}  {mb/max(t,1e-9)*1e-3*1e3:7.0f} GB/s  {n}")
+    print(f"{t:9.1f} us {100*t/all_t:5.1f}% x{c:3d}  {mb * 1e-3 / max(t * 1e-6, 1e-12):7.0f} GB/s  {n}")
