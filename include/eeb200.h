@@ -272,6 +272,49 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
  * (a fused QKV projection), pos i64 [b, q] with 0 <= pos < t1; writes K and V
  * of every (b, i) into kv bf16 [2, b, h, t1, dh] at slot pos[b, i]. A warp per
  * (b, i, K|V, head) row; dh must be a multiple of 2 and at most 256. */
+/* Token-level early exit (config 5): the reference decoder's deferral
+ * schedule (generative.py:217-259) kept on the device, so a decode step is
+ * [prefix layers -> ramp -> ee_defer_plan] then [suffix pass -> ee_defer_finish]
+ * with no host round trip. All pointers are device memory; B sequences, C =
+ * flush_cap + 1 chunk slots, N decode steps (history rows N + 1: row N is the
+ * end flush). kind: 0 none, 1 carry, 2 cap, 3 end. */
+typedef struct ee_defer_state {
+  int32_t* step;      /* [1] current decode step */
+  int32_t* n_def;     /* [B] parked tokens */
+  int64_t* qpos;      /* [B] next suffix position */
+  int32_t* def_step;  /* [B, C] step of the token parked in each slot */
+  int32_t* mem_cnt;   /* [B] this step's suffix chunk size */
+  int64_t* spos;      /* [B, C] suffix positions, -1 = padding */
+  uint8_t* h_exit;    /* [N + 1, B] history: exited */
+  float* h_err;       /* [N + 1, B] ramp error score */
+  int32_t* h_lab;     /* [N + 1, B] ramp label */
+  int32_t* h_final;   /* [N + 1, B] the model's own token */
+  int32_t* h_cnt;     /* [N + 1, B] chunk size decided at each step */
+  uint8_t* h_kind;    /* [N + 1, B] flush kind */
+  int64_t* h_qbase;   /* [N + 1, B] first suffix position of the chunk */
+  int32_t n_max;      /* N */
+  int32_t pad_;
+} ee_defer_state;
+
+/* Park the ramp's hidden state d_h_ramp bf16 [B, d] in the chunk bf16 [B, C, d]
+ * behind the parked ones, record (exit, err, label), and decide each sequence's
+ * suffix chunk: a non-exiting token carries every parked one, a sequence with
+ * flush_cap parked tokens flushes them (cap). d_fixed u8 [N, B] (nullable)
+ * overrides the exit decisions (tests). end_mode: every parked token flushes
+ * (end). Writes spos / mem_cnt / history; the caller then runs the suffix. */
+int ee_defer_plan(const ee_defer_state* st, int32_t b, int32_t c, int32_t d, int32_t cap,
+                  const void* d_h_ramp, void* d_chunk, const uint8_t* d_exits, const uint8_t* d_fixed,
+                  const float* d_err, const int32_t* d_lab, int32_t end_mode, void* stream);
+
+/* After the suffix pass: each flushed token's own output d_final_label i32
+ * [B * C] goes to the history (and, if d_hidden_hist f32 [N + 1, B, C, d] is
+ * given, the chunk's final hidden rows d_final_h f32 [B, C, d]); the next input
+ * token d_cur i64 [B] is the ramp label of an exit, else the model's; d_ppos
+ * and the step advance. */
+int ee_defer_finish(const ee_defer_state* st, int32_t b, int32_t c, int32_t d, const int32_t* d_final_label,
+                    const int32_t* d_lab, int64_t* d_cur, int64_t* d_ppos, const float* d_final_h,
+                    float* d_hidden_hist, int32_t end_mode, void* stream);
+
 int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_t q, int32_t h,
                       int32_t dh, int64_t t1, void* d_kv, void* stream);
 

@@ -90,6 +90,10 @@ SIGNATURES = {
     "ee_conv_bf16": (ctypes.c_int, [_vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _c_i32, _c_i32,
                                     _c_i32, _c_i32, _c_i32, _vp, _vp, _c_i32, _vp, _vp]),
     "ee_sequential_sum": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _vp]),
+    "ee_defer_plan": (ctypes.c_int, [_vp, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     _c_i32, _vp]),
+    "ee_defer_finish": (ctypes.c_int, [_vp, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _c_i32,
+                                       _vp]),
     "ee_im2col_bf16": (ctypes.c_int, [_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
                                       _c_i32, _c_i32, _vp, _vp]),
     "ee_maxpool_nhwc_bf16": (ctypes.c_int, [_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,

@@ -2298,7 +2298,7 @@ int ee_gemm_bf16(ee_workspace* ws, const void* d_a, const void* d_b, const float
 int64_t ee_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t splits, int32_t path,
                                int32_t out_bf16) {
   if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff ||
-      path < 0 || path > 5)
+      path < 0 || path > 6)
     return fail(EE_ERR_ARG, "bad GEMM shape or path");
   return (int64_t)ee_gemm3_workspace((int)m, (int)n, (int)k, splits, path, out_bf16);
 }
@@ -2320,7 +2320,7 @@ int ee_gemm_bf16_res(ee_workspace* ws, const void* d_a, const void* d_w, const f
   if (m < 1 || n < 1 || k < 1 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(EE_ERR_ARG, "bad GEMM shape");
   if (k % 8) return fail(EE_ERR_ARG, "K must be a multiple of 8 (16-byte rows)");
-  if (act < 0 || act > 3 || path < 0 || path > 5) return fail(EE_ERR_ARG, "bad act or path");
+  if (act < 0 || act > 3 || path < 0 || path > 6) return fail(EE_ERR_ARG, "bad act or path");
   if (!d_a || !d_w || !d_c) return fail(EE_ERR_ARG, "null pointer");
   if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_w) |
        reinterpret_cast<uintptr_t>(d_c)) & 15)
@@ -2579,6 +2579,106 @@ __global__ void __launch_bounds__(DA_THREADS) k_decode_attn(
 }
 
 // KV append: warp w -> row (b, i, s, head); lanes copy dh bf16 (u32 pairs)
+// Token-level early exit, the deferral schedule of the reference's decoder
+// timeline (generative.py:217-259) kept on the device so a decode step needs
+// no host round trip (config 5). Per sequence s: n_def[s] parked tokens in
+// chunk slots [0, n_def), qpos[s] the next suffix position.
+struct DeferState {   // = ee_defer_state (include/eeb200.h)
+  int32_t* step;        // [1] decode step (advanced after the finish kernel)
+  int32_t* n_def;       // [B]
+  int64_t* qpos;        // [B]
+  int32_t* def_step;    // [B, C] decode step of the token parked in each slot
+  int32_t* mem_cnt;     // [B] tokens in this step's suffix chunk (0 = none)
+  int64_t* spos;        // [B, C] suffix positions (-1 = padding slot)
+  uint8_t* h_exit;      // [N + 1, B] history: exited?
+  float* h_err;         // [N + 1, B]
+  int32_t* h_lab;       // [N + 1, B] ramp label
+  int32_t* h_final;     // [N + 1, B] the model's own token (filled when the suffix runs)
+  int32_t* h_cnt;       // [N + 1, B] suffix chunk size decided at each step
+  uint8_t* h_kind;      // [N + 1, B] 0 none / plain, 1 carry, 2 cap, 3 end
+  int64_t* h_qbase;     // [N + 1, B] first suffix position of the chunk
+  int32_t n_max;        // N (history rows N + 1: the end flush is row N)
+};
+
+// plan: park this step's ramp hidden state, decide who flushes. A CTA per sequence.
+__global__ void k_defer_plan(DeferState st, const uint16_t* __restrict__ h_ramp, uint16_t* __restrict__ chunk,
+                             const uint8_t* __restrict__ exits, const uint8_t* __restrict__ fixed,
+                             const float* __restrict__ err, const int32_t* __restrict__ lab, int C, int d,
+                             int cap, int end_mode) {
+  const int s = blockIdx.x, B = gridDim.x;
+  const int step = *st.step;
+  const int row = end_mode ? st.n_max : step;
+  const int n = st.n_def[s];
+  if (!end_mode) {  // the ramp's hidden state goes behind the parked ones
+    const uint4* src = reinterpret_cast<const uint4*>(h_ramp + (int64_t)s * d);
+    uint4* dst = reinterpret_cast<uint4*>(chunk + ((int64_t)s * C + n) * d);
+    for (int v = threadIdx.x; v < d / 8; v += blockDim.x) dst[v] = src[v];
+  }
+  if (threadIdx.x != 0) return;
+  bool ex = false;
+  int cnt = 0, kind = 0;
+  if (end_mode) {
+    cnt = n;
+    kind = n > 0 ? 3 : 0;
+  } else {
+    ex = fixed ? fixed[(int64_t)step * B + s] != 0 : exits[s] != 0;
+    st.def_step[s * C + n] = step;
+    st.h_exit[(int64_t)row * B + s] = ex;
+    st.h_err[(int64_t)row * B + s] = err[s];
+    st.h_lab[(int64_t)row * B + s] = lab[s];
+    if (!ex) {  // carries every parked suffix with it
+      cnt = n + 1;
+      kind = n > 0 ? 1 : 0;
+    } else if (n + 1 >= cap) {
+      cnt = n + 1;
+      kind = 2;
+    }
+  }
+  const int64_t q0 = st.qpos[s];
+  for (int i = 0; i < C; ++i) st.spos[s * C + i] = i < cnt ? q0 + i : -1;
+  st.mem_cnt[s] = cnt;
+  st.h_cnt[(int64_t)row * B + s] = cnt;
+  st.h_kind[(int64_t)row * B + s] = (uint8_t)kind;
+  st.h_qbase[(int64_t)row * B + s] = q0;
+  if (cnt > 0) {
+    st.qpos[s] = q0 + cnt;
+    st.n_def[s] = 0;
+  } else if (!end_mode) {
+    st.n_def[s] = n + 1;
+  }
+}
+
+// finish: the suffix pass has run; record every flushed token's own output,
+// pick the next input token, advance. A CTA per sequence (keep_hidden copies
+// the chunk's final hidden rows into the history).
+__global__ void k_defer_finish(DeferState st, const int32_t* __restrict__ final_label,
+                               const int32_t* __restrict__ lab, int64_t* __restrict__ cur,
+                               int64_t* __restrict__ ppos, const float* __restrict__ final_h,
+                               float* __restrict__ h_hidden, int C, int d, int end_mode) {
+  const int s = blockIdx.x, B = gridDim.x;
+  const int step = *st.step;
+  const int row = end_mode ? st.n_max : step;
+  const int cnt = st.mem_cnt[s];
+  if (h_hidden && cnt > 0) {
+    const float* src = final_h + (int64_t)s * C * d;
+    float* dst = h_hidden + ((int64_t)row * B + s) * C * d;
+    for (int v = threadIdx.x; v < cnt * d; v += blockDim.x) dst[v] = src[v];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < cnt; ++i)
+      st.h_final[(int64_t)st.def_step[s * C + i] * B + s] = final_label[s * C + i];
+    if (!end_mode) {
+      const bool ex = st.h_exit[(int64_t)row * B + s] != 0;
+      cur[s] = ex ? lab[s] : final_label[s * C + cnt - 1];  // a non-exit is its chunk's last token
+      ppos[s] += 1;
+    }
+  }
+}
+static_assert(sizeof(ee_defer_state) == sizeof(DeferState), "ee_defer_state layout");
+// the step counter moves after every CTA of the finish kernel has read it
+__global__ void k_defer_advance(int32_t* step) { *step += 1; }
+
 __global__ void k_kv_append(const uint32_t* __restrict__ qkv, const int64_t* __restrict__ pos,
                             int64_t b, int q, int h, int dh2, int64_t t1,
                             uint32_t* __restrict__ kv) {
@@ -2596,6 +2696,39 @@ __global__ void k_kv_append(const uint32_t* __restrict__ qkv, const int64_t* __r
   for (int k = lane; k < dh2; k += 32) dst[k] = __ldg(src + k);
 }
 extern "C" {
+
+int ee_defer_plan(const ee_defer_state* st_, int32_t b, int32_t c, int32_t d, int32_t cap, const void* d_h_ramp,
+                  void* d_chunk, const uint8_t* d_exits, const uint8_t* d_fixed, const float* d_err,
+                  const int32_t* d_lab, int32_t end_mode, void* stream) {
+  const auto* st = reinterpret_cast<const DeferState*>(st_);
+  if (!st || b < 1 || c < 1 || d < 8 || d % 8 || cap < 1 || cap > c)
+    return fail(EE_ERR_ARG, "bad deferral shape");
+  if (!end_mode && (!d_h_ramp || !d_chunk || (!d_exits && !d_fixed) || !d_err || !d_lab))
+    return fail(EE_ERR_ARG, "null pointer");
+  k_defer_plan<<<(unsigned)b, 128, 0, (cudaStream_t)stream>>>(
+      *st, static_cast<const uint16_t*>(d_h_ramp), static_cast<uint16_t*>(d_chunk), d_exits, d_fixed,
+      d_err, d_lab, c, d, cap, end_mode);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
+int ee_defer_finish(const ee_defer_state* st_, int32_t b, int32_t c, int32_t d, const int32_t* d_final_label,
+                    const int32_t* d_lab, int64_t* d_cur, int64_t* d_ppos, const float* d_final_h,
+                    float* d_hidden_hist, int32_t end_mode, void* stream) {
+  const auto* st = reinterpret_cast<const DeferState*>(st_);
+  if (!st || b < 1 || c < 1 || d < 1) return fail(EE_ERR_ARG, "bad deferral shape");
+  if (!d_final_label || (!end_mode && (!d_lab || !d_cur || !d_ppos)) || (d_hidden_hist && !d_final_h))
+    return fail(EE_ERR_ARG, "null pointer");
+  auto strm = (cudaStream_t)stream;
+  k_defer_finish<<<(unsigned)b, 256, 0, strm>>>(*st, d_final_label, d_lab, d_cur, d_ppos, d_final_h,
+                                                d_hidden_hist, c, d, end_mode);
+  EE_LAUNCH_CHECK();
+  if (!end_mode) {
+    k_defer_advance<<<1, 1, 0, strm>>>(st->step);
+    EE_LAUNCH_CHECK();
+  }
+  return EE_OK;
+}
 
 int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_t q, int32_t h,
                       int32_t dh, int64_t t1, void* d_kv, void* stream) {

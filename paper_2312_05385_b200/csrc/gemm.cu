@@ -841,15 +841,20 @@ Plan make_plan(int m, int n, int k, int splits, int path, bool bf) {
   // TMA stores need 16-byte output rows; otherwise (e.g. the 50257-wide LM
   // head) the swap kernel's plain stores take any shape
   const bool c_ok = (n * (bf ? 2 : 4)) % 16 == 0;
-  p.swap = path == 1 || (path == 0 && m <= 256) || !c_ok;
+  p.swap = path == 1 || path == 6 || (path == 0 && m <= 256) || !c_ok;
   if (!p.swap) {
     p.bn = path == 3 ? 128 : path == 2 ? 256 : path == 4 ? 192 : path == 5 ? 64 : pick_bn(m, n, device_sms() / 2);
     return p;
   }
-  // one z tile up to 256 rows: the weights stream once per call
-  p.np = m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256;
-  const int zt = (m + p.np - 1) / p.np;
+  // one z tile up to 256 rows (the weights stream once per call), unless the
+  // output is wide enough that 32-row z tiles still fit one wave at two CTAs
+  // per SM: their deeper weight ring (8 stages, 2 CTAs) beats the single wider
+  // tile and the repeated weight reads come from L2 (tools/sweep_np.py: M = 160,
+  // N = 3072 / 4096, K = 1024: 7.7 / 10.1 us vs 8.9 / 15.1 us)
   const int ft = (n + 127) / 128;
+  p.np = path == 6 ? 32 : m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256;
+  if (path == 0 && m > 64 && ft >= 16 && ((m + 31) / 32) * ft <= 2 * device_sms()) p.np = 32;
+  const int zt = (m + p.np - 1) / p.np;
   const int kt_n = (k + gemm3::BK - 1) / gemm3::BK;
   int S = splits;
   if (S <= 0) {  // the largest power of two with <= ~96 CTAs in all, S <= 8 and

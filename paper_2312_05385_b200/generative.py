@@ -29,8 +29,13 @@ reference's tuner consumes (token_feedback, generative.py:284-306).
 Both passes run at fixed shapes (B x 1 prefix tokens, B x (flush_cap + 1)
 suffix chunk slots with masks) and are captured as CUDA graphs; decode at
 batch 32 is weight-bandwidth bound, so the padded suffix slots cost little.
-Per-token release latency (time-per-token) is measured with CUDA events:
-ramp release for exits, suffix + head for the rest.
+The schedule itself (who parks, who carries, cap flushes, the next input
+token) runs on the device between the two passes (ee_defer_plan /
+ee_defer_finish), so the host enqueues every step without waiting on the GPU
+and reads the token / flush histories once at the end (use_graphs=False keeps
+the host-driven loop, eager, as the cross-check). Per-token release latency
+(time-per-token) is measured with CUDA events: ramp release for exits, suffix
++ head for the rest.
 """
 
 from __future__ import annotations
@@ -245,7 +250,7 @@ class TokenEEDecoder:
         self.final_err = torch.zeros(B * C, dtype=torch.float32, device="cuda")
         self.final_h = torch.zeros(B, C, d, dtype=torch.float32, device="cuda")
         self.never = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")  # argmax only
-        self._g_prefix = self._g_suffix = None
+        self._dev = None  # device-scheduled decoding state (_device_state)
 
     # ---- the two fixed-shape passes
     def _prefix(self):
@@ -266,27 +271,161 @@ class TokenEEDecoder:
         exit_from_logits(logits, self.never, conf=self.conf, site=1,
                          out_err=self.final_err, out_label=self.final_label)
 
-    def _capture(self):
-        torch = self.m.torch
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            for _ in range(2):  # warm-up allocations outside the capture
-                self._prefix()
-                self._suffix()
-        torch.cuda.current_stream().wait_stream(s)
-        self._g_prefix = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self._g_prefix):
-            self._prefix()
-        self._g_suffix = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self._g_suffix):
-            self._suffix()
-
     def run_prefix(self):
-        (self._g_prefix.replay() if self._g_prefix else self._prefix())
+        self._prefix()
 
     def run_suffix(self):
-        (self._g_suffix.replay() if self._g_suffix else self._suffix())
+        self._suffix()
+
+    # ---- the deferral schedule on the device (ee_defer_plan / ee_defer_finish)
+    def _device_state(self):
+        """Persistent device buffers of the on-device schedule (capacity: the
+        model's max_tokens decode steps) and the ee_defer_state that points at them."""
+        if self._dev is not None:
+            return self._dev
+        import ctypes
+
+        torch = self.m.torch
+        B, C, N = self.m.B, self.cap + 1, self.m.T
+        z = lambda *shape, dt: torch.zeros(*shape, dtype=dt, device="cuda")  # noqa: E731
+        t = {"step": z(1, dt=torch.int32), "n_def": z(B, dt=torch.int32), "qpos": z(B, dt=torch.int64),
+             "def_step": z(B, C, dt=torch.int32), "mem_cnt": z(B, dt=torch.int32),
+             "h_exit": z(N + 1, B, dt=torch.uint8), "h_err": z(N + 1, B, dt=torch.float32),
+             "h_lab": z(N + 1, B, dt=torch.int32), "h_final": z(N + 1, B, dt=torch.int32),
+             "h_cnt": z(N + 1, B, dt=torch.int32), "h_kind": z(N + 1, B, dt=torch.uint8),
+             "h_qbase": z(N + 1, B, dt=torch.int64), "fixed": z(N, B, dt=torch.uint8)}
+
+        class State(ctypes.Structure):
+            _fields_ = [(k, ctypes.c_void_p) for k in ("step", "n_def", "qpos", "def_step", "mem_cnt",
+                                                        "spos", "h_exit", "h_err", "h_lab", "h_final",
+                                                        "h_cnt", "h_kind", "h_qbase")] + \
+                       [("n_max", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+        st = State(**{k: (self.spos if k == "spos" else t[k]).data_ptr() for k, _ in State._fields_[:13]},
+                   n_max=N, pad_=0)
+        self._dev = {"t": t, "st": st, "hidden": None, "graphs": {}}
+        return self._dev
+
+    def _plan(self, end_mode: bool, use_fixed: bool):
+        dev = self._dev
+        m, torch = self.m, self.m.torch
+        B, C, d = self.chunk.shape
+        import ctypes
+
+        nat.check(nat.load_library().ee_defer_plan(
+            ctypes.byref(dev["st"]), B, C, d, self.cap, self.h_ramp.data_ptr(), self.chunk.data_ptr(),
+            self.exits.data_ptr(), dev["t"]["fixed"].data_ptr() if use_fixed else None,
+            self.err.data_ptr(), self.label.data_ptr(), int(end_mode), nat.stream_handle(torch)))
+
+    def _finish(self, end_mode: bool):
+        dev = self._dev
+        torch = self.m.torch
+        B, C, d = self.chunk.shape
+        import ctypes
+
+        hid = dev["hidden"]
+        nat.check(nat.load_library().ee_defer_finish(
+            ctypes.byref(dev["st"]), B, C, d, self.final_label.data_ptr(), self.label.data_ptr(),
+            self.cur.data_ptr(), self.ppos.data_ptr(), self.final_h.data_ptr(),
+            hid.data_ptr() if hid is not None else None, int(end_mode), nat.stream_handle(torch)))
+
+    def _step_graphs(self, use_fixed: bool, keep_hidden: bool):
+        """(A, B): A = prefix layers + ramp + plan, B = suffix + finish, captured once
+        per (fixed exits, hidden history) variant."""
+        dev = self._device_state()
+        key = (use_fixed, keep_hidden)
+        if key in dev["graphs"]:
+            return dev["graphs"][key]
+        torch = self.m.torch
+        t = dev["t"]
+        saved = {k: v.clone() for k, v in t.items()}
+        saved_io = (self.cur.clone(), self.ppos.clone(), self.chunk.clone(), self.spos.clone())
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm-up (allocations), then restore the state
+            self._prefix()
+            self._plan(False, use_fixed)
+            self._suffix()
+            self._finish(False)
+        torch.cuda.current_stream().wait_stream(s)
+        for k, v in saved.items():
+            t[k].copy_(v)
+        for dst, src in zip((self.cur, self.ppos, self.chunk, self.spos), saved_io):
+            dst.copy_(src)
+        ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ga):
+            self._prefix()
+            self._plan(False, use_fixed)
+        with torch.cuda.graph(gb):
+            self._suffix()
+            self._finish(False)
+        dev["graphs"][key] = (ga, gb)
+        return ga, gb
+
+    def _generate_device(self, prompt, n_new: int, keep_hidden: bool, fixed_exits) -> "DecodeReport":
+        """The whole decode enqueued without a host round trip per step: the
+        schedule lives in ee_defer_state, the host reads the histories once at
+        the end. Same tokens, flushes and feedback as the host-driven loop."""
+        torch = self.m.torch
+        m = self.m
+        B, C, d = self.chunk.shape
+        dev = self._device_state()
+        t = dev["t"]
+        use_fixed = fixed_exits is not None
+        if keep_hidden and dev["hidden"] is None:
+            dev["hidden"] = torch.zeros(m.T + 1, B, C, d, dtype=torch.float32, device="cuda")
+        ga, gb = self._step_graphs(use_fixed, keep_hidden)
+        first, P = self.prefill(prompt)
+        if P + n_new > m.T:
+            raise ParameterError("prompt + new tokens exceed the KV cache")
+        for v in t.values():
+            v.zero_()
+        t["qpos"].fill_(P)
+        self.ppos.fill_(P)
+        self.spos.fill_(-1)
+        self.cur.copy_(first)
+        if use_fixed:
+            t["fixed"][:n_new].copy_(torch.as_tensor(np.asarray(fixed_exits, dtype=np.uint8)[:n_new]))
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_new)]
+        for k in range(n_new):
+            ev[k][0].record()
+            ga.replay()
+            ev[k][1].record()
+            gb.replay()
+            ev[k][2].record()
+        # end of decoding: flush what is still parked
+        self._plan(True, use_fixed)
+        self._suffix()
+        self._finish(True)
+        torch.cuda.synchronize()
+        h = {k: v.cpu().numpy() for k, v in t.items() if k.startswith("h_")}
+        step_ms, t_ramp = [], []
+        for k in range(n_new):
+            t_ramp.append(ev[k][0].elapsed_time(ev[k][1]))
+            step_ms.append(ev[k][0].elapsed_time(ev[k][2]))
+        logs = []
+        for k in range(n_new):
+            for s_ in range(B):
+                ex = bool(h["h_exit"][k, s_])
+                lab = int(h["h_lab"][k, s_])
+                fin = int(h["h_final"][k, s_])
+                logs.append(TokenLog(s_, k, float(h["h_err"][k, s_]), lab, ex, lab if ex else fin, fin,
+                                     t_ramp[k] if ex else step_ms[k]))
+        names = {1: "carry", 2: "cap", 3: "end"}
+        flushes = []
+        hidden = {}
+        hid = dev["hidden"].cpu() if keep_hidden else None
+        for k in range(n_new + 1):
+            row = m.T if k == n_new else k
+            for s_ in range(B):
+                cnt, kind = int(h["h_cnt"][row, s_]), int(h["h_kind"][row, s_])
+                if kind in names:
+                    flushes.append((s_, k, cnt - 1 if kind == 1 else cnt, names[kind]))
+                if keep_hidden and cnt > 0:
+                    q0 = int(h["h_qbase"][row, s_])
+                    for i in range(cnt):
+                        hidden[(s_, q0 + i)] = hid[row, s_, i].cuda()
+        return DecodeReport(logs, flushes, step_ms, hidden)
 
     # ---- decoding
     def prefill(self, prompt):
@@ -311,10 +450,8 @@ class TokenEEDecoder:
         B, C = m.B, self.cap + 1
         if prompt.shape[0] != B:
             raise ParameterError("prompt batch must equal the decoder batch")
-        if self.use_graphs and self._g_prefix is None:
-            self.ppos.fill_(-1)  # capture with every write aimed at the sink slot
-            self.spos.fill_(-1)
-            self._capture()
+        if self.use_graphs:  # the schedule on the device: no host round trip per step
+            return self._generate_device(prompt, n_new, keep_hidden, fixed_exits)
         first, P = self.prefill(prompt)
         if P + n_new > m.T:
             raise ParameterError("prompt + new tokens exceed the KV cache")

@@ -48,7 +48,12 @@ def _oracle_check(rep, B, cap, threshold):
         assert all(t.final >= 0 for t in toks)  # every token's suffix ran (feedback)
 
 
-def _kv_check(torch, model, rep, prompt, first_inputs, n_new, tol=3e-2):
+def _kv_check(torch, model, rep, prompt, first_inputs, n_new, tol=5e-2):
+    """bf16 model, 24 layers: the decode passes and the teacher-forced forward run
+    the same math at different GEMM tilings (decode chunks vs one long chunk:
+    other split-K / z-tile plans, other fp32 accumulation orders), so final
+    hidden states agree to bf16 noise (measured worst 2-4 % of the row's max);
+    a missing or misplaced KV entry shows up as an O(1) error."""
     B, P = prompt.shape
     inputs = np.zeros((B, n_new), dtype=np.int64)
     for t in rep.tokens:
