@@ -354,15 +354,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     float* bias_row = bias_smem + (warp - 2) * 64;
     uint32_t ai = 0;
     int buf = 0;
+    constexpr int NCH = BN / CW;  // chunks per tile; half h takes chunks [h*NCH/2 ...)
+    const int c_lo = h * (NCH / 2) * CW, c_hi = h ? BN : (NCH / 2) * CW;
+    // the residual rows this lane adds in tile t, pulled into L2 ahead of use (one
+    // prefetch per 128-byte line) while the tile's MMAs still run
+    auto prefetch_res = [&](int t) {
+      if (res == nullptr || !OUT_BF16 || t >= tiles) return;
+      const int row = (t % mt) * 256 + (int)rank * 128 + q * 32 + lane, nb = (t / mt) * BN;
+      if (row >= M) return;
+      for (int cb = c_lo; cb < c_hi; cb += 64)
+        if (nb + cb < N)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(res + (int64_t)row * N + nb + cb));
+    };
+    prefetch_res(pair);
     for (int t = pair; t < tiles; t += pairs, ++ai) {
       const uint32_t a = ai & 1;
       const int row0 = (t % mt) * 256 + (int)rank * 128 + q * 32;
       const int n0 = (t / mt) * BN;
+      prefetch_res(t + pairs);  // one tile ahead (two measured slower: 224 vs 221 us, layer1)
       mbar_wait(&tfull_bar[a], (ai >> 1) & 1);
       fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
-      constexpr int NCH = BN / CW;  // chunks per tile; half h takes chunks [h*NCH/2 ...)
-      const int c_lo = h * (NCH / 2) * CW, c_hi = h ? BN : (NCH / 2) * CW;
       if (c_lo >= c_hi) {  // a one-chunk tile (BN = 64, bf16): half 0 only releases TMEM
         fence_before();
         __syncwarp();
