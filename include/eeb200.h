@@ -344,7 +344,7 @@ int ee_sequential_sum(const double* d_vals, int32_t n, int32_t rows, double* d_o
  * owns columns [r * seg, r * seg + kw * c) with seg = kw * c rounded up to 8
  * (column r * seg + s * c + ch = tap (r, s), channel ch); the gap columns
  * hold neighbouring finite input values and need ZERO weights; zeros past
- * kh * seg (kp % 64 == 0, kp / 8 <= 256) and outside the image. w * c % 8 == 0
+ * kh * seg (kp % 8 == 0, kp / 8 <= 256) and outside the image. w * c % 8 == 0
  * and x 16-byte aligned. The GEMM (weights laid out the same way) then runs on
  * ee_gemm_bf16_res. */
 int ee_im2col_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, int32_t kh, int32_t kw,

@@ -16,7 +16,7 @@ row-major [B*H*W, C] matrix, so
     padding done by the TMA unit), with the same fused epilogue;
   * a convolution whose input channels are not a multiple of 64 (the
     3-channel stem) gets its A operand written out once (ee_im2col_bf16, K
-    padded to a multiple of 64) and runs on the same GEMM with the same
+    padded to a multiple of 8) and runs on the same GEMM with the same
     epilogue; the stem's max pool is one NHWC pass (ee_maxpool_nhwc_bf16);
   * anything else (output channels not a multiple of 8) stays on cuDNN without
     a bias and takes bias / ReLU / shortcut in ONE fused NHWC pass
@@ -142,7 +142,7 @@ class Conv:
         if sh != sw or ph != pw:
             raise ParameterError("square strides and paddings only")
         seg = (kw * c + 7) // 8 * 8  # filter row r owns columns [r seg, r seg + kw c)
-        kp = (kh * seg + 63) // 64 * 64
+        kp = kh * seg  # a multiple of 8: the GEMM's last k-tile is zero-filled by TMA
         if getattr(self, "w_cols", None) is None or self.w_cols.shape[1] != kp:
             cout = self.w.shape[0]
             wc = torch.zeros((cout, kh, seg), dtype=torch.bfloat16, device=x.device)

@@ -6,7 +6,7 @@
 //   stem) gets its A operand written out once: row m = output pixel (n, oh, ow),
 //   column (r, s, c) at r * seg + s * c + c (seg = kw * c rounded up to 8; the
 //   gap columns meet zero weights), zero past kh * seg up to kp (a multiple of
-//   64) and outside the image.
+//   8) and outside the image.
 // k_maxpool_nhwc: max pooling of an NHWC bf16 map, 8 channels per 16-byte
 //   vector per thread, padding = -inf (PyTorch's semantics).
 #pragma once

@@ -2815,7 +2815,7 @@ int ee_im2col_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c, 
       kh > h + 2 * pad || kw > w + 2 * pad)
     return fail(EE_ERR_ARG, "bad convolution shape");
   const int seg = (kw * c + 7) / 8 * 8;
-  if (kp % 64 || kp < kh * seg) return fail(EE_ERR_ARG, "kp must be a multiple of 64 >= kh * roundup8(kw * c)");
+  if (kp % 8 || kp < kh * seg) return fail(EE_ERR_ARG, "kp must be a multiple of 8 >= kh * roundup8(kw * c)");
   if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
   if (reinterpret_cast<uintptr_t>(d_out) & 15) return fail(EE_ERR_ARG, "output must be 16-byte aligned");
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
