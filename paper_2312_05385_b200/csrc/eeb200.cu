@@ -2875,6 +2875,78 @@ int ee_bias_act_bf16(const void* d_x, const float* d_bias, const void* d_res, in
 }
 }  // extern "C"
 
+// A warp per row for d <= 256 * VPL... (VPL 16-byte vectors per lane): no block
+// barriers, 8 rows per CTA, so a [8192, 768] call is one wave of warps instead
+// of 8192 three-warp CTAs with four __syncthreads each. Same operations as
+// k_add_layernorm (the torch-rounded bf16 add, two-pass fp32 statistics); the
+// sums reduce in a different order.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_add_layernorm_warp(
+    uint16_t* __restrict__ h, const uint16_t* __restrict__ y, const uint16_t* __restrict__ gamma,
+    const uint16_t* __restrict__ beta, float eps, int d, int64_t rows, uint16_t* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nv = d / 8;
+  const uint4* hr = reinterpret_cast<const uint4*>(h + row * d);
+  float v[VPL][8];
+  uint4 hv[VPL], yv[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int t = lane + 32 * i;
+    hv[i] = t < nv ? hr[t] : make_uint4(0u, 0u, 0u, 0u);
+    if (y) yv[i] = t < nv ? reinterpret_cast<const uint4*>(y + row * d)[t] : make_uint4(0u, 0u, 0u, 0u);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int t = lane + 32 * i;
+    const uint32_t hw[4] = {hv[i].x, hv[i].y, hv[i].z, hv[i].w};
+    if (y) {
+      const uint32_t yw[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        o[k] = bf_round(bf_lo(hw[k]) + bf_lo(yw[k])) | (bf_round(bf_hi(hw[k]) + bf_hi(yw[k])) << 16);
+      if (t < nv) reinterpret_cast<uint4*>(h + row * d)[t] = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[i][2 * k] = bf_lo(o[k]), v[i][2 * k + 1] = bf_hi(o[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[i][2 * k] = bf_lo(hw[k]), v[i][2 * k + 1] = bf_hi(hw[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[i][k];  // padding lanes hold zeros
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i)
+    if (lane + 32 * i < nv)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) q += (v[i][k] - mean) * (v[i][k] - mean);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / (float)d + eps);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int t = lane + 32 * i;
+    if (t >= nv) continue;
+    const uint4 gv = reinterpret_cast<const uint4*>(gamma)[t], bv = reinterpret_cast<const uint4*>(beta)[t];
+    const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float a = (v[i][2 * k] - mean) * rstd * bf_lo(gw[k]) + bf_lo(bw[k]);
+      const float b = (v[i][2 * k + 1] - mean) * rstd * bf_hi(gw[k]) + bf_hi(bw[k]);
+      o[k] = bf_round(a) | (bf_round(b) << 16);
+    }
+    reinterpret_cast<uint4*>(x + row * d)[t] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 extern "C" {
 int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const void* d_beta,
                           double eps, int64_t rows, int32_t d, void* d_x, void* stream) {
@@ -2884,6 +2956,25 @@ int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const
        reinterpret_cast<uintptr_t>(d_gamma) | reinterpret_cast<uintptr_t>(d_beta) |
        reinterpret_cast<uintptr_t>(d_x)) % 16)
     return fail(EE_ERR_ARG, "misaligned rows");
+  if (d <= 2048 && rows >= 64) {  // a warp per row (the BERT / GPT-2 widths)
+    const unsigned blocks = (unsigned)ceil_div(rows, 8);
+    auto* hh = static_cast<uint16_t*>(d_h);
+    const auto* yy = static_cast<const uint16_t*>(d_y);
+    const auto* g = static_cast<const uint16_t*>(d_gamma);
+    const auto* bb = static_cast<const uint16_t*>(d_beta);
+    auto* xx = static_cast<uint16_t*>(d_x);
+    const int vpl = (d / 8 + 31) / 32;
+    if (vpl <= 1)
+      k_add_layernorm_warp<1><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
+    else if (vpl <= 2)
+      k_add_layernorm_warp<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
+    else if (vpl <= 4)
+      k_add_layernorm_warp<4><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
+    else
+      k_add_layernorm_warp<8><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
+    EE_LAUNCH_CHECK();
+    return EE_OK;
+  }
   k_add_layernorm<<<(unsigned)rows, (unsigned)((d / 8 + 31) / 32 * 32), 0, (cudaStream_t)stream>>>(
       static_cast<uint16_t*>(d_h), static_cast<const uint16_t*>(d_y),
       static_cast<const uint16_t*>(d_gamma), static_cast<const uint16_t*>(d_beta), (float)eps, d,

@@ -142,7 +142,8 @@ def test_add_layernorm_matches_torch(cuda):
     from paper_2312_05385_b200 import _native as nat
 
     g = torch.Generator(device="cuda").manual_seed(4)
-    for rows, d in ((32, 1024), (7, 64), (160, 1024)):
+    # rows >= 64 and d <= 2048 take the warp-per-row kernel (BERT 8192 x 768)
+    for rows, d in ((32, 1024), (7, 64), (160, 1024), (8192, 768), (100, 2048), (70, 24), (65, 4096)):
         h = torch.randn(rows, d, generator=g, device="cuda").to(torch.bfloat16)
         y = torch.randn(rows, d, generator=g, device="cuda").to(torch.bfloat16)
         gamma = (1 + 0.1 * torch.randn(d, generator=g, device="cuda")).to(torch.bfloat16)
@@ -154,6 +155,14 @@ def test_add_layernorm_matches_torch(cuda):
             h.data_ptr(), y.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1e-5, rows, d,
             x.data_ptr(), nat.stream_handle(torch)))
         assert torch.equal(h, h_ref)
+        assert torch.allclose(x.float(), x_ref, rtol=2 ** -7, atol=2 ** -7)
+        # LayerNorm only (no residual): h untouched
+        h0 = h.clone()
+        nat.check(nat.load_library().ee_add_layernorm_bf16(
+            h.data_ptr(), None, gamma.data_ptr(), beta.data_ptr(), 1e-5, rows, d,
+            x.data_ptr(), nat.stream_handle(torch)))
+        assert torch.equal(h, h0)
+        x_ref = torch.nn.functional.layer_norm(h0.float(), (d,), gamma.float(), beta.float(), eps=1e-5)
         assert torch.allclose(x.float(), x_ref, rtol=2 ** -7, atol=2 ** -7)
 
 
