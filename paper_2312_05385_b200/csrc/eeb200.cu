@@ -2264,8 +2264,11 @@ int ee_conv_bf16(ee_workspace* ws, const void* d_x, int64_t n, int32_t h, int32_
                  const void* d_w, int32_t cout, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
                  const float* d_bias, const void* d_res, int32_t act, void* d_y, void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  // the TMA im2col window corners of a 4D map must lie in [-128, 127] (pad and
+  // pad - (k - 1)), traversal strides in [1, 8]
   if (n < 1 || h < 1 || w < 1 || c < 1 || cout < 1 || kh < 1 || kw < 1 || stride < 1 || stride > 8 ||
-      pad < 0 || pad >= std::min(kh, kw) + 8 || kh > h + 2 * pad || kw > w + 2 * pad)
+      pad < 0 || pad > 127 || kh - 1 - pad > 128 || kw - 1 - pad > 128 || kh > h + 2 * pad ||
+      kw > w + 2 * pad)
     return fail(EE_ERR_ARG, "bad convolution shape");
   if (c % 64) return fail(EE_ERR_ARG, "input channels must be a multiple of 64");
   if (cout % 8) return fail(EE_ERR_ARG, "output channels must be a multiple of 8");
