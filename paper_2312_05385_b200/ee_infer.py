@@ -271,6 +271,22 @@ class GraphRunner:
         return self.out
 
 
+def compaction_segments(ramp_order, n_stages: int):
+    """[(first stage, last stage)] of a compacted batch: each segment ends at a
+    ramp site, the last one at the final classifier (stage n_stages - 1)."""
+    ends = list(ramp_order) + [n_stages - 1]
+    starts = [0] + [e + 1 for e in ends[:-1]]
+    return list(zip(starts, ends))
+
+
+def compaction_buckets(b: int):
+    """Batch buckets of a compacted segment: multiples of B/16 and the powers of
+    two below B/16 (every live count maps to the smallest bucket >= it)."""
+    granule = max(1, b // 16)
+    return sorted({min(b, 1 << k) for k in range(granule.bit_length() + 1)}
+                  | set(range(granule, b + 1, granule)) | {b})
+
+
 class CompactRunner:
     """Compaction mode (north star (2): downstream blocks run only on the rows
     that have not exited) without per-stage host work.
@@ -302,12 +318,8 @@ class CompactRunner:
         self.B = b = example.shape[0]
         self.R = R = pipe.n_ramps
         self.th = torch.tensor([float(t) for t in thresholds], dtype=torch.float64, device="cuda")
-        ends = list(pipe.ramp_order) + [len(pipe.stages) - 1]
-        starts = [0] + [e + 1 for e in ends[:-1]]
-        self.segments = list(zip(starts, ends))
-        granule = max(1, b // 16)
-        self.buckets = sorted({min(b, 1 << k) for k in range(granule.bit_length() + 1)}
-                              | set(range(granule, b + 1, granule)) | {b})
+        self.segments = compaction_segments(pipe.ramp_order, len(pipe.stages))
+        self.buckets = compaction_buckets(b)
         dev = "cuda"
         # result tables: B request slots + one dummy slot for padding rows
         self.slots = SlotTable(torch.empty(b + 1, dtype=torch.int32, device=dev),
