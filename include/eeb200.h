@@ -113,6 +113,19 @@ int ee_eval_thresholds_windows(ee_workspace* ws, const double* const* d_scores_l
                                int32_t r, const double* h_serve, double vanilla, const double* h_th,
                                int64_t c, double* d_acc, double* d_sav, void* stream);
 
+/* The counting half of ee_eval_thresholds_windows, for a caller that reduces
+ * across ranks first (one all-reduce per K windows): exact
+ * per-window totals into d_accw int64 [nwin, EE_WINDOW_ACC_WORDS] (zeroed here;
+ * the all-reduce sums them), then ee_windows_finalize on the reduced totals
+ * with the global sample count. */
+#define EE_WINDOW_ACC_WORDS 2178
+int ee_windows_counts(ee_workspace* ws, const double* const* d_scores_list,
+                      const uint32_t* const* d_bits_list, int32_t nwin, int64_t n, int32_t r,
+                      const double* h_th, int64_t c, int64_t* d_accw, void* stream);
+int ee_windows_finalize(ee_workspace* ws, const int64_t* d_accw, int32_t nwin, int64_t n_total, int32_t r,
+                        const double* h_serve, double vanilla, const double* h_th, int64_t c,
+                        double* d_acc, double* d_sav, void* stream);
+
 /* The same evaluation from HOST buffers (the reference's own calling
  * convention: numpy arrays in, numpy arrays out, engine.py:165-170):
  * h_scores f64 [n, r], h_correct_ext f64 [n, r+1] (0.0/1.0, else

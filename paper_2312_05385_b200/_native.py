@@ -117,6 +117,9 @@ SIGNATURES = {
     "ee_classify_candidates": (ctypes.c_int, [_vp, _c_i64, _c_i32, _vp, _vp, _vp]),
     "ee_kv_append_bf16": (ctypes.c_int, [_vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _vp, _vp]),
     "ee_add_layernorm_bf16": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_double, _c_i64, _c_i32, _vp, _vp]),
+    "ee_windows_counts": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i64, _c_i32, _vp, _c_i64, _vp, _vp]),
+    "ee_windows_finalize": (ctypes.c_int, [_vp, _vp, _c_i32, _c_i64, _c_i32, _vp, ctypes.c_double, _vp,
+                                           _c_i64, _vp, _vp, _vp]),
     "ee_eval_thresholds_windows": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i64, _c_i32, _vp, ctypes.c_double,
                                                   _vp, _c_i64, _vp, _vp, _vp]),
     "ee_decode_attention_bf16": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i64, _vp, _vp]),

@@ -1425,26 +1425,63 @@ static int eval_axis(ee_workspace* ws, const double* d_scores, const uint32_t* d
 
 }  // extern "C"
 template <int R>
-static cudaError_t launch_windows(const diag2::Params& p, const double* const* sl,
-                                 const uint32_t* const* bl, int nwin, long long* accw,
-                                 double* acc, double* sav, cudaStream_t st, ee_workspace* ws) {
-  constexpr int smem = diag3::Big::smem_bytes<R>();
-  constexpr int fsmem = diag3::Big::fin_bytes<R>();
-  {
-    cudaError_t e = ensure_smem(diag3::k_diag3_windows<R>, smem);
-    if (e != cudaSuccess) return e;
-  }
-  const unsigned grid = diag_grid(ws, p.n);
-  {
-    ProfScope ps(ws, st, "k_diag3_windows");
-    diag3::k_diag3_windows<R><<<grid, 1024, smem, st>>>(p, sl, bl, nwin, accw);
-  }
-  cudaError_t e = cudaGetLastError();
+static cudaError_t launch_windows_counts(const diag2::Params& p, const double* const* sl,
+                                        const uint32_t* const* bl, int nwin, long long* accw,
+                                        cudaStream_t st, ee_workspace* ws) {
+  constexpr int smem = diag3::dbw::smem_bytes<R>();
+  cudaError_t e = ensure_smem(diag3::k_diag3_windows_db<R>, smem);
   if (e != cudaSuccess) return e;
+  const unsigned grid = diag_grid(ws, p.n);
+  ProfScope ps(ws, st, "k_diag3_windows_db");
+  diag3::k_diag3_windows_db<R><<<grid, diag3::dbw::THREADS, smem, st>>>(p, sl, bl, nwin, accw);
+  return cudaGetLastError();
+}
+template <int R>
+static cudaError_t launch_windows_fin(const diag2::Params& p, long long* accw, int nwin, double* acc,
+                                     double* sav, cudaStream_t st, ee_workspace* ws) {
+  constexpr int fsmem = diag3::Big::fin_bytes<R>();
   ProfScope ps(ws, st, "k_diag3_windows_fin");
   diag3::k_diag3_windows_fin<R><<<(unsigned)nwin, 1024, fsmem, st>>>(p, accw, acc, sav);
   return cudaGetLastError();
 }
+// the planned parameters of a windows sweep (diagonal candidate rows)
+static int windows_params(ee_workspace* ws, int32_t nwin, int64_t n, int32_t r, const double* h_serve,
+                          double vanilla, const double* h_th, int64_t c, diag2::Params* p) {
+  if (nwin < 1 || n < 1 || c < 1 || c > diag2::MAX_POS || r < 2 || r > diag2::RMAX || (r & 1))
+    return fail(EE_ERR_ARG, "windows: nwin, n, c >= 1, c <= 512, even r <= 16");
+  if (!h_th) return fail(EE_ERR_ARG, "null thresholds");
+  std::vector<double> u;
+  if (!diagonal_rows(h_th, c, r, u) || u.empty() || (int)u.size() > diag3::MAX_M)
+    return fail(EE_ERR_ARG, "windows: candidate rows must be diagonal with <= 64 distinct values");
+  *p = diag2::Params{};
+  if (!plan_bins(u, &p->a, &p->c0, p->tab)) return fail(EE_ERR_ARG, "windows: thresholds do not fit the bin grid");
+  const int m = (int)u.size();
+  p->n = n;
+  p->m = m;
+  p->C = c;
+  p->vanilla = vanilla;
+  if (h_serve)
+    for (int j = 0; j <= r; ++j) p->serve[j] = h_serve[j];
+  for (int i = 0; i < m; ++i) p->u[i] = u[i];
+  for (int64_t k = 0; k < c; ++k) {
+    const double v = h_th[k * r];
+    p->pos[k] = v == v ? (unsigned char)(std::lower_bound(u.begin(), u.end(), canon(v)) - u.begin())
+                       : (unsigned char)255;
+  }
+  (void)ws;
+  return EE_OK;
+}
+#define EE_WIN_DISPATCH(call)                                                              \
+  switch (r) {                                                                             \
+    case 2: { constexpr int RR = 2; e = call; } break;                                     \
+    case 4: { constexpr int RR = 4; e = call; } break;                                     \
+    case 6: { constexpr int RR = 6; e = call; } break;                                     \
+    case 8: { constexpr int RR = 8; e = call; } break;                                     \
+    case 10: { constexpr int RR = 10; e = call; } break;                                   \
+    case 12: { constexpr int RR = 12; e = call; } break;                                   \
+    case 14: { constexpr int RR = 14; e = call; } break;                                   \
+    default: { constexpr int RR = 16; e = call; } break;                                   \
+  }
 extern "C" {
 
 int ee_eval_thresholds_windows(ee_workspace* ws, const double* const* d_scores_list,
@@ -1452,32 +1489,16 @@ int ee_eval_thresholds_windows(ee_workspace* ws, const double* const* d_scores_l
                                int32_t r, const double* h_serve, double vanilla, const double* h_th,
                                int64_t c, double* d_acc, double* d_sav, void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
-  if (nwin < 1 || n < 1 || c < 1 || c > diag2::MAX_POS || r < 2 || r > diag2::RMAX || (r & 1))
-    return fail(EE_ERR_ARG, "windows: nwin, n, c >= 1, c <= 512, even r <= 16");
   if (!d_scores_list || !d_bits_list || !h_serve || !h_th || !d_acc || !d_sav)
     return fail(EE_ERR_ARG, "null pointer");
-  std::vector<double> u;
-  if (!diagonal_rows(h_th, c, r, u) || u.empty() || (int)u.size() > diag3::MAX_M)
-    return fail(EE_ERR_ARG, "windows: candidate rows must be diagonal with <= 64 distinct values");
+  diag2::Params p;
+  int rc = windows_params(ws, nwin, n, r, h_serve, vanilla, h_th, c, &p);
+  if (rc) return rc;
   std::lock_guard<std::mutex> lock(ws->mu);
   auto st = (cudaStream_t)stream;
   ws->resident = false;
-  if (ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n)) > diag3::Big::MAX_CTA_CHUNKS)
+  if (ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n)) > diag3::dbw::MAX_CTA_CHUNKS)
     return fail(EE_ERR_ARG, "windows: window too large for the packed cell counters");
-  diag2::Params p{};
-  if (!plan_bins(u, &p.a, &p.c0, p.tab)) return fail(EE_ERR_ARG, "windows: thresholds do not fit the bin grid");
-  const int m = (int)u.size();
-  p.n = n;
-  p.m = m;
-  p.C = c;
-  p.vanilla = vanilla;
-  for (int j = 0; j <= r; ++j) p.serve[j] = h_serve[j];
-  for (int i = 0; i < m; ++i) p.u[i] = u[i];
-  for (int64_t k = 0; k < c; ++k) {
-    const double v = h_th[k * r];
-    p.pos[k] = v == v ? (unsigned char)(std::lower_bound(u.begin(), u.end(), canon(v)) - u.begin())
-                      : (unsigned char)255;
-  }
   const size_t acc_b = (size_t)nwin * diag2::ACC_WORDS * 8;
   if (acc_b > ws->accw_cap) {
     if (ws->d_accw) EE_CUDA(cudaFree(ws->d_accw));
@@ -1486,14 +1507,50 @@ int ee_eval_thresholds_windows(ee_workspace* ws, const double* const* d_scores_l
     ws->accw_cap = acc_b;
   }
   EE_CUDA(cudaMemsetAsync(ws->d_accw, 0, acc_b, st));
+  auto* accw = static_cast<long long*>(ws->d_accw);
   cudaError_t e;
-  switch (r) {
-#define EE_WIN_CASE(K) case K: e = launch_windows<K>(p, d_scores_list, d_bits_list, nwin, static_cast<long long*>(ws->d_accw), d_acc, d_sav, st, ws); break;
-    EE_WIN_CASE(2) EE_WIN_CASE(4) EE_WIN_CASE(6) EE_WIN_CASE(8) EE_WIN_CASE(10) EE_WIN_CASE(12)
-    EE_WIN_CASE(14) default: e = launch_windows<16>(p, d_scores_list, d_bits_list, nwin, static_cast<long long*>(ws->d_accw), d_acc, d_sav, st, ws); break;
-#undef EE_WIN_CASE
-  }
-  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_diag3_windows: ") + cudaGetErrorString(e));
+  EE_WIN_DISPATCH(launch_windows_counts<RR>(p, d_scores_list, d_bits_list, nwin, accw, st, ws))
+  if (e == cudaSuccess) EE_WIN_DISPATCH(launch_windows_fin<RR>(p, accw, nwin, d_acc, d_sav, st, ws))
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_diag3_windows_db: ") + cudaGetErrorString(e));
+  return EE_OK;
+}
+
+static_assert(EE_WINDOW_ACC_WORDS == diag2::ACC_WORDS, "window accumulator layout");
+int ee_windows_counts(ee_workspace* ws, const double* const* d_scores_list,
+                      const uint32_t* const* d_bits_list, int32_t nwin, int64_t n, int32_t r,
+                      const double* h_th, int64_t c, int64_t* d_accw, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (!d_scores_list || !d_bits_list || !d_accw) return fail(EE_ERR_ARG, "null pointer");
+  diag2::Params p;
+  int rc = windows_params(ws, nwin, n, r, nullptr, 0.0, h_th, c, &p);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  ws->resident = false;
+  if (ceil_div(ceil_div(n, 32), (int64_t)diag_grid(ws, n)) > diag3::dbw::MAX_CTA_CHUNKS)
+    return fail(EE_ERR_ARG, "windows: window too large for the packed cell counters");
+  EE_CUDA(cudaMemsetAsync(d_accw, 0, (size_t)nwin * diag2::ACC_WORDS * 8, st));
+  cudaError_t e;
+  EE_WIN_DISPATCH(launch_windows_counts<RR>(p, d_scores_list, d_bits_list, nwin,
+                                           reinterpret_cast<long long*>(d_accw), st, ws))
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_diag3_windows_db: ") + cudaGetErrorString(e));
+  return EE_OK;
+}
+
+int ee_windows_finalize(ee_workspace* ws, const int64_t* d_accw, int32_t nwin, int64_t n_total, int32_t r,
+                        const double* h_serve, double vanilla, const double* h_th, int64_t c,
+                        double* d_acc, double* d_sav, void* stream) {
+  if (!ws) return fail(EE_ERR_ARG, "null workspace");
+  if (!d_accw || !h_serve || !d_acc || !d_sav) return fail(EE_ERR_ARG, "null pointer");
+  diag2::Params p;
+  int rc = windows_params(ws, nwin, n_total, r, h_serve, vanilla, h_th, c, &p);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(ws->mu);
+  auto st = (cudaStream_t)stream;
+  cudaError_t e;
+  EE_WIN_DISPATCH(launch_windows_fin<RR>(p, const_cast<long long*>(reinterpret_cast<const long long*>(d_accw)),
+                                         nwin, d_acc, d_sav, st, ws))
+  if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_diag3_windows_fin: ") + cudaGetErrorString(e));
   return EE_OK;
 }
 

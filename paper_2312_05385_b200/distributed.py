@@ -141,6 +141,67 @@ class ShardedSweep:
         return acc, sav
 
 
+WINDOW_ACC_WORDS = 2178  # EE_WINDOW_ACC_WORDS (include/eeb200.h)
+
+
+class WindowStream:
+    """A stream of config-4 sweeps over resident, sample-sharded windows as ONE
+    persistent counting launch per call (k_diag3_windows_db: tables built once,
+    each window's fold overlapped with the next window's stream), ONE
+    all-reduce of the K per-window totals (K x 2178 int64) when the group has
+    more than one rank, and one finalisation with the global sample count
+    (ee_windows_counts / ee_windows_finalize). Every buffer is allocated here,
+    so a call can be captured in a CUDA graph. Diagonal candidate rows only
+    (<= 64 distinct thresholds, even r <= 16). Results equal evaluating each
+    full window on its own, bit for bit."""
+
+    def __init__(self, sweeps: Sequence["ShardedSweep"], order=None, *, group=None):
+        import torch
+
+        if not sweeps:
+            raise ParameterError("no windows")
+        s0 = sweeps[0].local
+        for sw in sweeps[1:]:
+            e = sw.local
+            if e.n != s0.n or e.r != s0.r or not np.array_equal(e.serve, s0.serve) or \
+                    e.vanilla_ms != s0.vanilla_ms or sw.n_total != sweeps[0].n_total:
+                raise ParameterError("windows must share n, r, serve table and vanilla latency")
+        order = list(range(len(sweeps))) if order is None else [int(i) for i in order]
+        if not order or any(i < 0 or i >= len(sweeps) for i in order):
+            raise ParameterError("bad window order")
+        self.sweeps, self.order, self.group = list(sweeps), order, group
+        self.n, self.r, self.n_total = s0.n, s0.r, sweeps[0].n_total
+        self.serve, self.vanilla = s0.serve, float(s0.vanilla_ms)
+        self.sl = torch.tensor([nat.ptr(sweeps[i].local.d_scores) for i in order], dtype=torch.int64,
+                               device="cuda")
+        self.bl = torch.tensor([sweeps[i].local.d_bits.data_ptr() for i in order], dtype=torch.int64,
+                               device="cuda")
+        self.accw = torch.zeros((len(order), WINDOW_ACC_WORDS), dtype=torch.int64, device="cuda")
+        self.acc = self.sav = None
+
+    def run(self, thresholds):
+        """acc, sav [K, C] (CUDA f64) for the candidate rows `thresholds` (C, r)."""
+        import torch
+        import torch.distributed as dist
+
+        th = np.ascontiguousarray(thresholds, dtype=np.float64)
+        if th.ndim != 2 or th.shape[1] != self.r:
+            raise ParameterError(f"thresholds must be (C, {self.r})")
+        c, k = th.shape[0], len(self.order)
+        if self.acc is None or self.acc.shape != (k, c):
+            self.acc = torch.empty((k, c), dtype=torch.float64, device="cuda")
+            self.sav = torch.empty((k, c), dtype=torch.float64, device="cuda")
+        lib, st = nat.load_library(), nat.stream_handle(torch)
+        nat.check(lib.ee_windows_counts(nat.workspace(), self.sl.data_ptr(), self.bl.data_ptr(), k,
+                                        self.n, self.r, th.ctypes.data, c, self.accw.data_ptr(), st))
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(self.accw, op=dist.ReduceOp.SUM, group=self.group)
+        nat.check(lib.ee_windows_finalize(nat.workspace(), self.accw.data_ptr(), k, self.n_total, self.r,
+                                          self.serve.ctypes.data, self.vanilla, th.ctypes.data, c,
+                                          self.acc.data_ptr(), self.sav.data_ptr(), st))
+        return self.acc, self.sav
+
+
 def evaluate_windows(sweeps: Sequence["ShardedSweep"], thresholds: np.ndarray, *, group=None,
                      to_host: bool = True):
     """acc, sav [K, C] for K windows sharded the same way (one ShardedSweep per

@@ -65,6 +65,13 @@ def _worker(rank, world, port, q):
         sw2 = ShardedSweep(other, sites, prof, rank=rank, world=world)
         wa, ws = evaluate_windows([sw, sw2], rnd)
         res += [(wa[0], ws[0]), (wa[1], ws[1])]
+        # the persistent multi-window sweep over this rank's shards, one all-reduce
+        from paper_2312_05385_b200.distributed import WindowStream
+
+        wsr = WindowStream([sw, sw2], order=[0, 1, 1, 0])
+        da, dsv = wsr.run(diag)
+        da, dsv = da.cpu().numpy(), dsv.cpu().numpy()
+        res += [(da[q], dsv[q]) for q in range(4)]
         q.put((rank, [(a.tolist(), s.tolist()) for a, s in res]))
     finally:
         dist.destroy_process_group()
@@ -87,6 +94,8 @@ def test_two_rank_sweep_matches_one_gpu(cuda):
     one += one[:1]  # host shards through eval_thresholds_host_sharded: diag
     other = synth.config4_window(60_001, seed=7)
     one += [one[1], ShardedSweep(other, sites, prof).evaluate_many(rnd)]  # evaluate_windows
+    d_other = ShardedSweep(other, sites, prof).evaluate_many(diag)
+    one += [one[0], d_other, d_other, one[0]]  # WindowStream order 0, 1, 1, 0 (diagonal rows)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

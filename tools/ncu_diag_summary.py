@@ -66,12 +66,15 @@ for row in hot:
                f"{int(f(row, 'Instructions Executed'))} exec  {row[ix['Source']].strip()[:70]}")
 print("\n".join(out))
 if "--traffic" in sys.argv:
-    rd = num("dram__bytes_read.sum") * mb[u["dram__bytes_read.sum"]] * 1e6
-    wr = num("dram__bytes_write.sum") * mb[u["dram__bytes_write.sum"]] * 1e6
+    # --windows K: the capture is one persistent launch over K windows (per step = / K)
+    kw = int(sys.argv[sys.argv.index("--windows") + 1]) if "--windows" in sys.argv else 1
+    rd = num("dram__bytes_read.sum") * mb[u["dram__bytes_read.sum"]] * 1e6 / kw
+    wr = num("dram__bytes_write.sum") * mb[u["dram__bytes_write.sum"]] * 1e6 / kw
     alg = 8 * 1_000_000 * 12 + 1_000_000 * 12 // 8 + 8 * 64 * 12 + 16 * 64
     json.dump({"source": f"{os.path.basename(rep)} (ncu --set full --clock-control none, "
-                         "tools/profile_sweep.py diagonal)",
-               "kernel": name + " (the whole config-4 sweep is this one launch)",
+                         + ("tools/profile_windows.py" if kw > 1 else "tools/profile_sweep.py diagonal") + ")",
+               "kernel": name + (f" (one launch over {kw} config-4 windows; bytes per window)" if kw > 1
+                                 else " (the whole config-4 sweep is this one launch)"),
                "dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
                "sweep_dram_bytes_per_step": int(rd + wr), "algorithmic_bytes_per_step": alg,
                "note": "read = 96 MB f64 scores + 4 MB u32 correctness rows (4 B/sample vs the "
