@@ -423,15 +423,18 @@ def test_axis_family_path_matches_generic_and_oracle(cuda, r, n, nan_base):
     assert np.array_equal(hist2, hist_a) and np.array_equal(ok2, ok_a)
 
 
-def test_windows_batch_matches_per_window_sweeps(cuda):
-    """ee_eval_thresholds_windows (one persistent sweep over several resident
-    windows + one finalisation) returns, per window, the bits a per-window
-    sweep returns; windows repeated in the order are independent results."""
+@pytest.mark.parametrize("r,n,nwin", [(12, 40001, 5), (2, 33, 3), (16, 100003, 7), (6, 4099, 1), (8, 1, 2)])
+def test_windows_batch_matches_per_window_sweeps(cuda, r, n, nwin):
+    """ee_eval_thresholds_windows (k_diag3_windows_db: one persistent sweep over
+    several resident windows, folds overlapped by dedicated warps, + one
+    finalisation) returns, per window, the bits a per-window sweep returns;
+    windows repeated in the order are independent results. Ragged tails, tiny
+    windows (fewer chunks than stream warps), every even R up to 16, odd window
+    counts (both cell buffers in turn)."""
     import torch
 
     from paper_2312_05385_b200 import kernels as K
 
-    r, n = 12, 40001
     prof = make_chain(r + 1)
     sites = find_feasible_sites(prof)[:r]
     evs = []
@@ -443,7 +446,7 @@ def test_windows_batch_matches_per_window_sweeps(cuda):
                                                mode="hist"))
     vals = np.concatenate([np.arange(60) / 59.0, [np.nan, -np.inf]])
     th = np.repeat(vals[:, None], r, axis=1)
-    order = [0, 1, 2, 1, 0]
+    order = [(2 * i + 1) % 3 for i in range(nwin)]  # 1, 0, 2, 1, 0, ...
     acc, sav = K.eval_thresholds_windows(evs, th, order)
     torch.cuda.synchronize()
     for row, wi in enumerate(order):
