@@ -342,10 +342,18 @@ int ee_kv_append_bf16(const void* d_qkv, const int64_t* d_pos, int64_t b, int32_
  * wo); act 0 none / 3 ReLU. The A operand is never materialised: each k-tile
  * is one TMA im2col load (128 consecutive output pixels x 64 channels of one
  * filter tap, zero padding by the TMA unit). c % 64 == 0, cout % 8 == 0,
- * 16-byte aligned pointers. (A ResNet's spatial convolutions.) */
+ * 16-byte aligned pointers; d_work / work_bytes: ee_conv_workspace_size bytes
+ * (nullable when that is 0). (A ResNet's spatial convolutions.) */
 int ee_conv_bf16(ee_workspace* ws, const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c,
                  const void* d_w, int32_t cout, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
-                 const float* d_bias, const void* d_res, int32_t act, void* d_y, void* stream);
+                 const float* d_bias, const void* d_res, int32_t act, void* d_y, void* d_work,
+                 int64_t work_bytes, void* stream);
+
+/* Bytes of device workspace ee_conv_bf16 needs for this shape: > 0 when the
+ * convolution has too few output tiles for the SMs and splits K (fp32
+ * partials [splits, m, cout], summed in order by one epilogue pass), else 0. */
+int64_t ee_conv_workspace_size(int64_t n, int32_t h, int32_t w, int32_t c, int32_t cout, int32_t kh,
+                               int32_t kw, int32_t stride, int32_t pad);
 
 /* The reference's sequential fp64 sum of each row of d_vals [rows, n]
  * (((0 + v0) + v1) + ...), every addition rounded, as _exitcore.pyx:43-53

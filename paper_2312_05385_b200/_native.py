@@ -88,7 +88,9 @@ SIGNATURES = {
     ),
     "ee_compact_rows": (ctypes.c_int, [_vp, _c_i64, _vp, _vp, _c_i64, _vp, _vp]),
     "ee_conv_bf16": (ctypes.c_int, [_vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _c_i32, _c_i32,
-                                    _c_i32, _c_i32, _c_i32, _vp, _vp, _c_i32, _vp, _vp]),
+                                    _c_i32, _c_i32, _c_i32, _vp, _vp, _c_i32, _vp, _vp, _c_i64, _vp]),
+    "ee_conv_workspace_size": (_c_i64, [_c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
+                                        _c_i32]),
     "ee_sequential_sum": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _vp]),
     "ee_defer_plan": (ctypes.c_int, [_vp, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
                                      _c_i32, _vp]),

@@ -36,6 +36,7 @@ from paper_2312_05385_b200.errors import ParameterError
 from paper_2312_05385_b200.heads import gemm
 
 ACT = {None: 0, "relu": 3}
+_CONV_WORK: dict = {}  # conv shape -> ee_conv_workspace_size
 
 
 def _rows(x):
@@ -126,9 +127,19 @@ class Conv:
         if res is not None:
             r = res if res.is_contiguous(memory_format=torch.channels_last) else \
                 res.contiguous(memory_format=torch.channels_last)
-        nat.check(nat.load_library().ee_conv_bf16(
+        lib = nat.load_library()
+        key = (b, h, w, c, cout, kh, kw, sh, ph)
+        wb = _CONV_WORK.get(key)
+        if wb is None:
+            wb = int(lib.ee_conv_workspace_size(*key))
+            nat.check(min(wb, 0))
+            _CONV_WORK[key] = wb
+        # split-K partials in torch's stream-ordered (CUDA-graph-aware) allocator
+        work = torch.empty(wb, dtype=torch.uint8, device=x.device) if wb else None
+        nat.check(lib.ee_conv_bf16(
             nat.workspace(), x.data_ptr(), b, h, w, c, self.w.data_ptr(), cout, kh, kw, sh, ph,
-            self.bias.data_ptr(), nat.ptr(r), ACT[act], y.data_ptr(), nat.stream_handle(torch)))
+            self.bias.data_ptr(), nat.ptr(r), ACT[act], y.data_ptr(), nat.ptr(work), wb,
+            nat.stream_handle(torch)))
         return y.permute(0, 3, 1, 2)
 
 

@@ -2314,12 +2314,22 @@ cudaError_t ee_gemm3_launch(const void* a, const void* w, const float* bias, con
 size_t ee_gemm3_workspace(int m, int n, int k, int splits, int path, int out_bf16);
 cudaError_t ee_conv3_launch(const void* x, const void* w, const float* bias, const void* res, void* y,
                             int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad,
-                            int act, cudaStream_t st);
+                            int act, void* work, size_t work_bytes, cudaStream_t st);
+size_t ee_conv3_workspace(int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad);
 extern "C" {
+
+int64_t ee_conv_workspace_size(int64_t n, int32_t h, int32_t w, int32_t c, int32_t cout, int32_t kh,
+                               int32_t kw, int32_t stride, int32_t pad) {
+  if (n < 1 || h < 1 || w < 1 || c < 1 || cout < 1 || kh < 1 || kw < 1 || stride < 1 || pad < 0 ||
+      kh > h + 2 * pad || kw > w + 2 * pad || n > 0x7fffffff)
+    return fail(EE_ERR_ARG, "bad convolution shape");
+  return (int64_t)ee_conv3_workspace((int)n, h, w, c, cout, kh, kw, stride, pad);
+}
 
 int ee_conv_bf16(ee_workspace* ws, const void* d_x, int64_t n, int32_t h, int32_t w, int32_t c,
                  const void* d_w, int32_t cout, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
-                 const float* d_bias, const void* d_res, int32_t act, void* d_y, void* stream) {
+                 const float* d_bias, const void* d_res, int32_t act, void* d_y, void* d_work,
+                 int64_t work_bytes, void* stream) {
   if (!ws) return fail(EE_ERR_ARG, "null workspace");
   // the TMA im2col window corners of a 4D map must lie in [-128, 127] (pad and
   // pad - (k - 1)), traversal strides in [1, 8]
@@ -2342,7 +2352,8 @@ int ee_conv_bf16(ee_workspace* ws, const void* d_x, int64_t n, int32_t h, int32_
   cudaError_t e;
   {
     ProfScope ps(ws, st, "k_conv3");
-    e = ee_conv3_launch(d_x, d_w, d_bias, d_res, d_y, (int)n, h, w, c, cout, kh, kw, stride, pad, act, st);
+    e = ee_conv3_launch(d_x, d_w, d_bias, d_res, d_y, (int)n, h, w, c, cout, kh, kw, stride, pad, act, d_work,
+                        (size_t)std::max<int64_t>(0, work_bytes), st);
   }
   if (e != cudaSuccess) return fail(EE_ERR_CUDA, std::string("k_conv3: ") + cudaGetErrorString(e));
   return EE_OK;

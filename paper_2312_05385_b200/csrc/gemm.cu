@@ -60,6 +60,10 @@ struct ConvGeom {
   int kw;       // filter width
   int cblocks;  // C / 64
   int stride, pad;
+  // split-K (both the plain and the implicit GEMM): tile t covers k-tile range
+  // split t / (mt * nt) and writes fp32 partials to rows split * m_pad + m of
+  // the output map; ee_splitk_epilogue sums the splits in order
+  int ksplit, m_pad;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -270,8 +274,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int mt = (M + 255) / 256, nt = (N + BN - 1) / BN;
-  const int tiles = mt * nt;
   const int kt_n = (K + BK - 1) / BK;
+  const int nsplit = G.ksplit > 1 ? G.ksplit : 1;
+  const int mn = mt * nt, tiles = mn * nsplit;
+  const int kpt = (kt_n + nsplit - 1) / nsplit;  // k-tiles per split (every split non-empty: host)
+  // tile t -> (m tile, n tile, k-tile range, output row offset)
+  auto tile_m = [&](int t) { return (t % mn) % mt; };
+  auto tile_n = [&](int t) { return (t % mn) / mt; };
+  auto tile_k0 = [&](int t) { return (t / mn) * kpt; };
+  auto tile_k1 = [&](int t) { return min(kt_n, (t / mn) * kpt + kpt); };
+  auto tile_rowoff = [&](int t) { return (t / mn) * G.m_pad; };
   const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
@@ -299,8 +311,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     if (lane == 0) {  // ===== TMA producer (both CTAs; bytes land on the leader's barrier)
       uint32_t it = 0;
       for (int t = pair; t < tiles; t += pairs) {
-        const int m0 = (t % mt) * 256 + (int)rank * 128;
-        const int n0 = (t / mt) * BN + (int)rank * (BN / 2);
+        const int m0 = tile_m(t) * 256 + (int)rank * 128;
+        const int n0 = tile_n(t) * BN + (int)rank * (BN / 2);
         // implicit GEMM: the input window corner of this CTA's first output pixel
         int img = 0, hb = 0, wb = 0;
         if constexpr (IM2COL) {
@@ -310,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           hb = oh * G.stride - G.pad;
           wb = (rem - oh * G.wo) * G.stride - G.pad;
         }
-        for (int kt = 0; kt < kt_n; ++kt, ++it) {
+        for (int kt = tile_k0(t); kt < tile_k1(t); ++kt, ++it) {
           const int s = it % ST;
           mbar_wait(&empty_bar[s], ((it / ST) & 1) ^ 1);
           if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * Cfg::STAGE);
@@ -335,14 +347,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         mbar_wait(&tempty_bar[a], ((ai >> 1) & 1) ^ 1);
         fence_after();
         const uint32_t d = tmem + a * BN;
-        for (int kt = 0; kt < kt_n; ++kt, ++it) {
+        const int k0 = tile_k0(t);
+        for (int kt = k0; kt < tile_k1(t); ++kt, ++it) {
           const int s = it % ST;
           mbar_wait(&full_bar[s], (it / ST) & 1);
           fence_after();
           const uint32_t a0 = smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma<2>(d, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32), id, (kt | k) ? 1u : 0u);
+            umma<2>(d, desc_sw128(a0 + k * 32), desc_sw128(b0 + k * 32), id, (kt != k0 || k) ? 1u : 0u);
           umma_commit<2>(&empty_bar[s]);
         }
         umma_commit<2>(&tfull_bar[a]);
@@ -360,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     // prefetch per 128-byte line) while the tile's MMAs still run
     auto prefetch_res = [&](int t) {
       if (res == nullptr || !OUT_BF16 || t >= tiles) return;
-      const int row = (t % mt) * 256 + (int)rank * 128 + q * 32 + lane, nb = (t / mt) * BN;
+      const int row = tile_m(t) * 256 + (int)rank * 128 + q * 32 + lane, nb = tile_n(t) * BN;
       if (row >= M) return;
       for (int cb = c_lo; cb < c_hi; cb += 64)
         if (nb + cb < N)
@@ -369,8 +382,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     prefetch_res(pair);
     for (int t = pair; t < tiles; t += pairs, ++ai) {
       const uint32_t a = ai & 1;
-      const int row0 = (t % mt) * 256 + (int)rank * 128 + q * 32;
-      const int n0 = (t / mt) * BN;
+      const int row0 = tile_m(t) * 256 + (int)rank * 128 + q * 32;
+      const int n0 = tile_n(t) * BN;
+      const int rowoff = tile_rowoff(t);  // split-K: this split's region of the partial map
       prefetch_res(t + pairs);  // one tile ahead (two measured slower: 224 vs 221 us, layer1)
       mbar_wait(&tfull_bar[a], (ai >> 1) & 1);
       fence_after();
@@ -467,7 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          tma_store(&tmC, stage0 + buf * 4096, n0 + c0, row0);
+          tma_store(&tmC, stage0 + buf * 4096, n0 + c0, rowoff + row0);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         buf ^= 1;
@@ -810,30 +824,102 @@ cudaError_t launch_pair(const void* a, const void* w, const float* bias, const u
   const int tiles = ((m + 255) / 256) * ((n + BN - 1) / BN);
   const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
   kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, res, m, n, k,
-                                                                 gemm3::ConvGeom{});
+                                                                 gemm3::ConvGeom{0, 0, 0, 0, 0, 0, 1, 0});
   return cudaGetLastError();
+}
+
+// split-K epilogue: y[m, n] = act(sum_s part[s * m_pad + m, n] + bias[n] (+ res[m, n]))
+// in bf16, the splits summed in order (deterministic); 8 columns per thread
+__global__ void k_splitk_epilogue(const float* __restrict__ part, int S, int64_t m_pad, int64_t M,
+                                  int N, const float* __restrict__ bias, const uint16_t* __restrict__ res,
+                                  int act, uint16_t* __restrict__ y) {
+  const int nv = N / 8;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M * nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = v / nv;
+    const int c0 = (int)(v - m * nv) * 8;
+    float f[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = 0.f;
+    for (int s = 0; s < S; ++s) {
+      const float4* src = reinterpret_cast<const float4*>(part + (s * m_pad + m) * N + c0);
+      const float4 a = __ldcs(src), b = __ldcs(src + 1);
+      f[0] += a.x, f[1] += a.y, f[2] += a.z, f[3] += a.w, f[4] += b.x, f[5] += b.y, f[6] += b.z, f[7] += b.w;
+    }
+    uint32_t rw[4] = {0u, 0u, 0u, 0u};
+    if (res) {
+      const uint4 r4 = *reinterpret_cast<const uint4*>(res + m * N + c0);
+      rw[0] = r4.x, rw[1] = r4.y, rw[2] = r4.z, rw[3] = r4.w;
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float lo = f[2 * e] + (res ? __uint_as_float(rw[e] << 16) : 0.f);
+      float hi = f[2 * e + 1] + (res ? __uint_as_float(rw[e] & 0xffff0000u) : 0.f);
+      if (bias) lo += __ldg(bias + c0 + 2 * e), hi += __ldg(bias + c0 + 2 * e + 1);
+      if (act == gemm3::ACT_RELU) lo = fmaxf(lo, 0.f), hi = fmaxf(hi, 0.f);
+      o[e] = gemm3::bf16x2(lo, hi);
+    }
+    *reinterpret_cast<uint4*>(y + m * N + c0) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Few output tiles over a long K (late layers of a small batch): split K so the
+// tiles x splits fill the SM pairs (fp32 partials, then one epilogue pass), when
+// at least 3 splits fit (below that the extra pass costs what the split saves)
+int conv_splits(int m, int cout, int k, int bn, int avail) {
+  const int tiles = ((m + 255) / 256) * ((cout + bn - 1) / bn);
+  const int kt_n = (k + gemm3::BK - 1) / gemm3::BK;
+  if (kt_n < 12 || tiles * 3 > avail) return 1;
+  int S = std::min({avail / tiles, kt_n / 4, 8});
+  const int kpt = (kt_n + S - 1) / S;
+  S = (kt_n + kpt - 1) / kpt;  // no empty split
+  return S >= 3 ? S : 1;
 }
 
 template <int BN, int ACT>
 cudaError_t launch_conv(const void* x, const void* w, const float* bias, const uint16_t* res, void* y,
                         int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad,
-                        cudaStream_t st) {
+                        void* work, size_t work_bytes, cudaStream_t st) {
   using Cfg = gemm3::PairCfg<BN>;
-  auto kern = gemm3::k_gemm_pair<BN, ACT, true, true>;
-  cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
-  if (e != cudaSuccess) return e;
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (wd + 2 * pad - kw) / stride + 1;
   const int m = n * ho * wo, k = kh * kw * c;
+  const int mt = (m + 255) / 256, tiles = mt * ((cout + BN - 1) / BN);
+  const int S = conv_splits(m, cout, k, BN, device_sms() / 2);
   CUtensorMap ta, tb, tc;
   if (!make_im2col_map(&ta, x, n, h, wd, c, kh, kw, stride, pad) ||
-      !make_map(&tb, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cout, k, gemm3::BK, BN / 2) ||
-      !make_map(&tc, y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, cout, 64, 32))
+      !make_map(&tb, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cout, k, gemm3::BK, BN / 2))
     return cudaErrorInvalidValue;
-  const gemm3::ConvGeom g{ho * wo, wo, kw, c / gemm3::BK, stride, pad};
-  const int tiles = ((m + 255) / 256) * ((cout + BN - 1) / BN);
-  const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
-  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, res, m, cout, k, g);
-  return cudaGetLastError();
+  const gemm3::ConvGeom g{ho * wo, wo, kw, c / gemm3::BK, stride, pad, S, mt * 256};
+  if (S == 1) {
+    auto kern = gemm3::k_gemm_pair<BN, ACT, true, true>;
+    cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    if (!make_map(&tc, y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, cout, 64, 32)) return cudaErrorInvalidValue;
+    const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
+    kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, res, m, cout, k, g);
+    return cudaGetLastError();
+  }
+  auto kern = gemm3::k_gemm_pair<BN, 0, false, true>;  // fp32 partials, no epilogue math
+  cudaError_t e = set_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM);
+  if (e != cudaSuccess) return e;
+  // the caller's workspace (ee_conv_workspace_size bytes)
+  float* part = static_cast<float*>(work);
+  const size_t part_b = (size_t)S * mt * 256 * cout * 4;
+  if (!part || work_bytes < part_b) return cudaErrorInvalidValue;
+  if (!make_map(&tc, part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (int64_t)S * mt * 256, cout, 32, 32))
+    return cudaErrorInvalidValue;
+  const int pairs = std::max(1, std::min(tiles * S, max_pairs(kern, Cfg::SMEM)));
+  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, nullptr, nullptr, m, cout, k, g);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    const int64_t nv = (int64_t)m * (cout / 8);
+    const unsigned blocks = (unsigned)std::min<int64_t>((nv + 255) / 256, (int64_t)device_sms() * 8);
+    k_splitk_epilogue<<<blocks, 256, 0, st>>>(part, S, (int64_t)mt * 256, m, cout, bias, res, ACT,
+                                              static_cast<uint16_t*>(y));
+    e = cudaGetLastError();
+  }
+  return e;
 }
 
 // how one call runs (host-side plan; the workspace query uses the same one)
@@ -955,22 +1041,30 @@ cudaError_t dispatch(const Plan& p, const void* a, const void* w, const float* b
 // Implicit-GEMM convolution entry (ee_conv_bf16, eeb200.cu): NHWC bf16 x
 // [n, h, w, c], weight [cout, kh, kw, c], y [n, ho, wo, cout] = act(conv + bias
 // (+ res)); c % 64 == 0, cout % 8 == 0, act 0 or 3.
+size_t ee_conv3_workspace(int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad) {
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (wd + 2 * pad - kw) / stride + 1;
+  const int m = n * ho * wo;
+  const int bn = pick_bn(m, cout, device_sms() / 2);
+  const int S = conv_splits(m, cout, kh * kw * c, bn, device_sms() / 2);
+  return S > 1 ? (size_t)S * ((m + 255) / 256) * 256 * cout * 4 : 0;
+}
+
 cudaError_t ee_conv3_launch(const void* x, const void* w, const float* bias, const void* res, void* y,
                             int n, int h, int wd, int c, int cout, int kh, int kw, int stride, int pad,
-                            int act, cudaStream_t st) {
+                            int act, void* work, size_t work_bytes, cudaStream_t st) {
   const auto* r = static_cast<const uint16_t*>(res);
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (wd + 2 * pad - kw) / stride + 1;
   const int bn = pick_bn(n * ho * wo, cout, device_sms() / 2);
   if (act == 3) {
-    if (bn == 256) return launch_conv<256, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
-    if (bn == 192) return launch_conv<192, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
-    if (bn == 64) return launch_conv<64, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
-    return launch_conv<128, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+    if (bn == 256) return launch_conv<256, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
+    if (bn == 192) return launch_conv<192, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
+    if (bn == 64) return launch_conv<64, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
+    return launch_conv<128, 3>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
   }
-  if (bn == 256) return launch_conv<256, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
-  if (bn == 192) return launch_conv<192, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
-  if (bn == 64) return launch_conv<64, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
-  return launch_conv<128, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, st);
+  if (bn == 256) return launch_conv<256, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
+  if (bn == 192) return launch_conv<192, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
+  if (bn == 64) return launch_conv<64, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
+  return launch_conv<128, 0>(x, w, bias, r, y, n, h, wd, c, cout, kh, kw, stride, pad, work, work_bytes, st);
 }
 
 // Internal entries used by ee_gemm_bf16_ex / ee_gemm_workspace_size

@@ -45,6 +45,9 @@ def _ref_conv(x, conv, act, res):
     (3, 1, 512, 512, 7, 5),     # layer4: 7x7 maps, tiles straddle images
     (3, 2, 64, 128, 32, 2),     # CIFAR downsampling block
     (1, 2, 64, 128, 32, 2),     # its strided 1x1 shortcut (implicit GEMM, traversal stride 2)
+    (3, 1, 512, 512, 4, 32),    # CIFAR layer4 at B=32: 8 tiles over K=4608 -> split-K + epilogue pass
+    (3, 1, 256, 256, 8, 32),    # CIFAR layer3: split-K
+    (3, 2, 256, 512, 8, 3),     # tiny M, strided, split-K with a ragged last tile
     (7, 2, 3, 64, 224, 2),      # the ImageNet stem: explicit im2col (K 147 -> 192) + GEMM
     (3, 1, 3, 64, 32, 4),       # the CIFAR stem
     (3, 1, 24, 40, 15, 3),      # odd channels: im2col K 216 -> 256, ragged M
