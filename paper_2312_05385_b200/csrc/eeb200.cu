@@ -71,7 +71,9 @@ int sm_count() {
 // a second GPU driven from the same process, or two threads racing on a first
 // call, still set the attribute before launching.
 static cudaError_t ensure_smem_fn(const void* fn, size_t smem) {
-  if (smem <= 48 * 1024) return cudaSuccess;
+  // (the 48 KB default covers static + dynamic shared memory together; no
+  // kernel here has more than 24 KB static, so smaller requests always fit)
+  if (smem <= 24 * 1024) return cudaSuccess;
   static std::mutex mu;
   static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;
   int dev = 0;

@@ -43,10 +43,14 @@ def _check(res, feat, w, bias, conf, thr, alive=None, check_logits=True):
     return int(near.sum())
 
 
-@pytest.mark.parametrize("layout", ["nchw", "nhwc", "pooled"])
+HEAD_SHAPES = [(64, 96, 7), (32, 64, 32), (32, 128, 16), (16, 512, 4), (8, 24, 57)]
+# pooled rows have no spatial split: one pooled shape
+HEAD_CASES = [(lay, sh) for lay in ("nchw", "nhwc") for sh in HEAD_SHAPES] + [("pooled", (64, 96, 7))]
+
+
+@pytest.mark.parametrize("layout,shape", HEAD_CASES)
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("conf", ["maxprob", "entropy"])
-@pytest.mark.parametrize("shape", [(64, 96, 7), (32, 64, 32), (32, 128, 16), (16, 512, 4), (8, 24, 57)])
 def test_fused_head_matches_torch(cuda, layout, dtype, conf, shape):
     """Every pooling path, including the cluster-split ones (a row's map split
     over 2-8 CTAs of one cluster when it is >= 16 KB: the CIFAR ResNet-18 ramp
@@ -55,8 +59,6 @@ def test_fused_head_matches_torch(cuda, layout, dtype, conf, shape):
     b, c, hw = shape
     k = 10
     if layout == "pooled":
-        if hw != 7:
-            pytest.skip("pooled rows have no spatial split")
         feat = torch.randn(b, c, generator=g)
     else:
         feat = torch.randn(b, c, hw, hw, generator=g)
