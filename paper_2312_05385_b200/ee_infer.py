@@ -137,7 +137,9 @@ class EEPipeline:
         if dev_th:
             thresholds = [thresholds[r : r + 1] for r in range(R)]
         alive = torch.ones(b, dtype=torch.uint8, device=dev)
-        rows = torch.arange(b, dtype=torch.int32, device=dev)  # request slot of each live row
+        # request slot of each live row (feedback mode: the identity, which the
+        # kernels take as a null slot map)
+        rows = torch.arange(b, dtype=torch.int32, device=dev) if mode == "compact" else None
         if mode == "feedback":
             # every row reaches every ramp (each writes err/label for all rows) and
             # is released exactly once (at a ramp or by the final model), so the
@@ -214,10 +216,16 @@ class EEPipeline:
                 if side is not None:  # join: every ramp has decided
                     main.wait_stream(side)
                     held.clear()
-                final_label.index_copy_(0, rows.long(), torch.argmax(logits, dim=1).to(torch.int32))
                 # every still-alive row is released with the final model's label
-                exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=R, alive=alive,
-                                 slot=rows, slots=slots, compact=(mode != "feedback"))
+                # (argmax, first maximum: torch.argmax's rule); feedback mode
+                # takes every row's label straight from the kernel
+                if mode == "feedback":
+                    exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=R, alive=alive,
+                                     slots=slots, out_label=final_label, compact=False)
+                else:
+                    final_label.index_copy_(0, rows.long(), torch.argmax(logits, dim=1).to(torch.int32))
+                    exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=R, alive=alive,
+                                     slot=rows, slots=slots, compact=True)
         if side is not None:
             main.wait_stream(side)
         out = BatchResult(slots.label, slots.site, slots.err, ramp_err, ramp_label, final_label,
