@@ -25,5 +25,7 @@ for i, m in per.items():
 all_t = sum(v[1] for v in tot.values())
 print(f"total {all_t:.1f} us over {sum(v[0] for v in tot.values())} launches")
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+has_bytes = any(v[2] > 0 for v in tot.values())  # only when the list carries dram__bytes
 for n, (c, t, mb) in sorted(tot.items(), key=lambda kv: -kv[1][1])[:top]:
-    print(f"{t:9.1f} us {100*t/all_t:5.1f}% x{c:3d}  {mb * 1e-3 / max(t * 1e-6, 1e-12):7.0f} GB/s  {n}")
+    bw = f"{mb * 1e-3 / max(t * 1e-6, 1e-12):7.0f} GB/s  " if has_bytes else ""
+    print(f"{t:9.1f} us {100*t/all_t:5.1f}% x{c:3d}  {bw}{n}")
