@@ -400,6 +400,18 @@ int ee_decode_attention_bf16(const void* d_qkv, const void* d_kv, const int64_t*
 int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
                     const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream);
 
+/* In-place compaction of d_buf [rows, row_bytes] (rows <= 8192, row_bytes % 16
+ * == 0, 16-byte aligned) to the *d_nkeep survivors d_keep lists (ascending, as
+ * the exit controller writes it): survivors below *d_nkeep stay in place and
+ * the survivors at or above it move, ascending, into the exited rows' places
+ * below it, so only those rows are copied. d_rows_out[p] = d_rows_in[source
+ * row of p] (the source row index if d_rows_in is NULL) for p < *d_nkeep, else
+ * `dummy`; d_alive_out[p] = p < *d_nkeep; *d_n_out = *d_nkeep when given. All
+ * on the device, so it can sit inside a CUDA graph. */
+int ee_compact_fill(void* d_buf, int64_t row_bytes, const int32_t* d_keep, const int32_t* d_nkeep,
+                    int64_t rows, const int32_t* d_rows_in, int32_t dummy, int32_t* d_rows_out,
+                    uint8_t* d_alive_out, int32_t* d_n_out, void* stream);
+
 /* Compaction bookkeeping for the next stage of a compacted batch (capacity cap
  * rows): d_rows_out[i] = d_rows_in[d_keep[i]] (d_keep[i] if d_rows_in is NULL)
  * for i < *d_nkeep, else `dummy`; d_alive_out[i] = i < *d_nkeep; *d_n_out =

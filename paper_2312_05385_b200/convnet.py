@@ -85,14 +85,16 @@ class Conv:
         self.w2d = w.reshape(w.shape[0], -1).contiguous() if self.pointwise else None
         self.w = w.contiguous(memory_format=torch.channels_last)
 
-    def __call__(self, x, act=None, res=None):
+    def __call__(self, x, act=None, res=None, out=None):
+        """`out`: optional channels_last bf16 [B, C_out, H_out, W_out] the result is
+        written into (the GEMM paths; e.g. a compacted batch's next input buffer)."""
         import torch
         import torch.nn.functional as F
 
         cin, cout = x.shape[1], self.w.shape[0]
         if cin % 64 == 0 and cout % 8 == 0 and not (self.pointwise and self.stride == (1, 1)):
-            return self._implicit_gemm(x, act, res)
-        if cout % 8 == 0 and not self.pointwise and (x.shape[3] * cin) % 8 == 0:
+            return self._implicit_gemm(x, act, res, out)
+        if out is None and cout % 8 == 0 and not self.pointwise and (x.shape[3] * cin) % 8 == 0:
             return self._explicit_im2col(x, act, res)
         if self.pointwise and x.shape[1] % 8 == 0:
             if self.stride != (1, 1):
@@ -100,8 +102,15 @@ class Conv:
                     memory_format=torch.channels_last)
             a, (b, _, h, w) = _rows(x)
             r = _rows(res)[0] if res is not None else None
-            y = gemm(a, self.w2d, self.bias, act=act, res=r)
+            o = None
+            if out is not None:
+                if not out.is_contiguous(memory_format=torch.channels_last):
+                    raise ParameterError("out must be channels_last")
+                o = out.permute(0, 2, 3, 1).reshape(b * h * w, cout)  # a view: dense NHWC rows
+            y = gemm(a, self.w2d, self.bias, act=act, res=r, out=o)
             return _unrows(y, b, h, w)
+        if out is not None:
+            raise ParameterError("this convolution has no direct-output path")
         y = F.conv2d(x, self.w, None, self.stride, self.padding)
         if y.shape[1] % 8:
             y = y + self.bias.to(y.dtype).view(1, -1, 1, 1)
@@ -111,7 +120,7 @@ class Conv:
         return bias_act(y, self.bias, act, res, out=None)
 
 
-    def _implicit_gemm(self, x, act, res):
+    def _implicit_gemm(self, x, act, res, out=None):
         torch = nat.torch_cuda()
         if not x.is_contiguous(memory_format=torch.channels_last):
             x = x.contiguous(memory_format=torch.channels_last)
@@ -122,7 +131,12 @@ class Conv:
             raise ParameterError("square strides and paddings only")
         ho, wo = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
         cout = self.w.shape[0]
-        y = torch.empty((b, ho, wo, cout), dtype=torch.bfloat16, device=x.device)
+        if out is not None:
+            if tuple(out.shape) != (b, cout, ho, wo) or not out.is_contiguous(memory_format=torch.channels_last):
+                raise ParameterError("out must be a channels_last [B, C_out, H_out, W_out] map")
+            y = out.permute(0, 2, 3, 1)
+        else:
+            y = torch.empty((b, ho, wo, cout), dtype=torch.bfloat16, device=x.device)
         r = None
         if res is not None:
             r = res if res.is_contiguous(memory_format=torch.channels_last) else \
@@ -187,11 +201,11 @@ class BottleneckTC:
         self.c1, self.c2, self.c3 = Conv(blk.conv1), Conv(blk.conv2), Conv(blk.conv3)
         self.ds = Conv(blk.downsample[0]) if blk.downsample is not None else None
 
-    def __call__(self, x):
-        out = self.c1(x, act="relu")
-        out = self.c2(out, act="relu")
+    def __call__(self, x, out=None):
+        y = self.c1(x, act="relu")
+        y = self.c2(y, act="relu")
         idt = self.ds(x) if self.ds is not None else x
-        return self.c3(out, act="relu", res=idt)
+        return self.c3(y, act="relu", res=idt, out=out)
 
 
 class BasicBlockTC:
@@ -201,10 +215,36 @@ class BasicBlockTC:
         self.c1, self.c2 = Conv(blk.conv1), Conv(blk.conv2)
         self.ds = Conv(blk.downsample[0]) if blk.downsample is not None else None
 
-    def __call__(self, x):
-        out = self.c1(x, act="relu")
+    def __call__(self, x, out=None):
+        y = self.c1(x, act="relu")
         idt = self.ds(x) if self.ds is not None else x
-        return self.c2(out, act="relu", res=idt)
+        return self.c2(y, act="relu", res=idt, out=out)
+
+
+def run_into(stage, x, out):
+    """stage(x) with its result written into `out` when the stage ends in a
+    routed residual block (else None: the caller falls back to a copy)."""
+    import torch
+
+    if isinstance(stage, torch.nn.Sequential) and len(stage):
+        last = stage[len(stage) - 1]
+        if not isinstance(getattr(last, "forward", None), (BottleneckTC, BasicBlockTC)):
+            return None
+        for j in range(len(stage) - 1):
+            x = stage[j](x)
+        stage = last
+    fwd = getattr(stage, "forward", None)
+    if not isinstance(fwd, (BottleneckTC, BasicBlockTC)):
+        return None
+    return fwd(x, out=out)
+
+
+def can_run_into(stage) -> bool:
+    import torch
+
+    if isinstance(stage, torch.nn.Sequential) and len(stage):
+        stage = stage[len(stage) - 1]
+    return isinstance(getattr(stage, "forward", None), (BottleneckTC, BasicBlockTC))
 
 
 def route_resnet(model):

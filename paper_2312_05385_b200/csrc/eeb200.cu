@@ -3070,6 +3070,25 @@ int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
   return EE_OK;
 }
 
+int ee_compact_fill(void* d_buf, int64_t row_bytes, const int32_t* d_keep, const int32_t* d_nkeep,
+                    int64_t rows, const int32_t* d_rows_in, int32_t dummy, int32_t* d_rows_out,
+                    uint8_t* d_alive_out, int32_t* d_n_out, void* stream) {
+  if (row_bytes <= 0 || row_bytes % 16) return fail(EE_ERR_ARG, "row_bytes must be a positive multiple of 16");
+  if (rows > exitc::FILL_MAX_ROWS) return fail(EE_ERR_ARG, "more rows than ee_compact_fill supports");
+  if (!d_buf || !d_keep || !d_nkeep || !d_rows_out || !d_alive_out) return fail(EE_ERR_ARG, "null pointer");
+  if (reinterpret_cast<uintptr_t>(d_buf) & 15) return fail(EE_ERR_ARG, "buffer must be 16-byte aligned");
+  if (rows < 1) return EE_OK;
+  // enough CTAs for a few moved rows to stream at full bandwidth
+  const int64_t words = rows * (row_bytes / 16);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(words, 256 * 4),
+                                                                            (int64_t)sm_count() * 2));
+  exitc::k_compact_fill<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<uint8_t*>(d_buf), row_bytes, d_keep, d_nkeep, (int)rows, d_rows_in, dummy, d_rows_out,
+      d_alive_out, d_n_out);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
 int ee_compact_meta(const int32_t* d_keep, const int32_t* d_nkeep, const int32_t* d_rows_in,
                     int64_t cap, int32_t dummy, int32_t* d_rows_out, uint8_t* d_alive_out,
                     int32_t* d_n_out, void* stream) {

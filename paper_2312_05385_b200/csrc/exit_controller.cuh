@@ -483,4 +483,82 @@ __global__ void k_compact_meta(const int32_t* __restrict__ keep, const int32_t* 
   }
 }
 
+// In-place compaction of a batch buffer: the survivors already below n_keep
+// stay where they are and only the survivors at or above n_keep move, in
+// ascending order, into the exited rows' places below n_keep (ascending), so
+// a batch where few rows exited moves only those few rows instead of copying
+// every survivor (the stable gather of k_compact_rows). Every CTA rebuilds the
+// (hole, source) pairing from `keep` in shared memory (rows <= FILL_MAX_ROWS),
+// then the CTAs copy 16-byte words of the pairs' rows; CTA 0 writes the new
+// row -> request slot map and alive bytes. Sources (>= n_keep) and holes
+// (< n_keep) never overlap.
+constexpr int FILL_MAX_ROWS = 8192;
+__global__ void __launch_bounds__(256)
+    k_compact_fill(uint8_t* __restrict__ buf, int64_t row_bytes, const int32_t* __restrict__ keep,
+                   const int32_t* __restrict__ n_keep, int rows, const int32_t* __restrict__ rows_in,
+                   int32_t dummy, int32_t* __restrict__ rows_out, uint8_t* __restrict__ alive_out,
+                   int32_t* __restrict__ n_out) {
+  __shared__ uint8_t mark[FILL_MAX_ROWS];
+  __shared__ int16_t hole[FILL_MAX_ROWS];  // hole rank -> position (< n_keep <= FILL_MAX_ROWS)
+  __shared__ int wsum[8];
+  __shared__ int s_m;
+  const int nk = min(*n_keep, rows);
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) mark[i] = 0;
+  if (threadIdx.x == 0) s_m = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int t = threadIdx.x; t < nk; t += blockDim.x)
+    if (keep[t] < nk) mark[keep[t]] = 1, ++mine;
+  atomicAdd(&s_m, mine);
+  __syncthreads();
+  const int m = s_m;  // survivors below n_keep: keep[0 .. m), the rest keep[m .. nk)
+  // rank the holes (positions < nk not marked), 256 positions per step
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int base = 0;
+  for (int p0 = 0; p0 < nk; p0 += 256) {
+    const int p = p0 + threadIdx.x;
+    const bool h = p < nk && !mark[p];
+    const unsigned b = __ballot_sync(0xffffffffu, h);
+    if (lane == 0) wsum[wid] = __popc(b);
+    __syncthreads();
+    int off = base;
+    for (int w = 0; w < wid; ++w) off += wsum[w];
+    if (h) hole[off + __popc(b & ((1u << lane) - 1))] = (int16_t)p;
+    int tot = 0;
+    for (int w = 0; w < 8; ++w) tot += wsum[w];
+    base += tot;
+    __syncthreads();
+  }
+  const int npairs = nk - m;
+  if (blockIdx.x == 0) {
+    // new order: position p < nk holds p itself (a survivor) or the source its hole got
+    for (int p = threadIdx.x; p < rows; p += blockDim.x) {
+      if (p < nk) {
+        rows_out[p] = rows_in ? rows_in[p] : p;
+        alive_out[p] = 1;
+      } else {
+        rows_out[p] = dummy;
+        alive_out[p] = 0;
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
+      const int src = keep[m + t];
+      rows_out[hole[t]] = rows_in ? rows_in[src] : src;
+    }
+    if (threadIdx.x == 0 && n_out) *n_out = nk;
+  }
+  // the copies: (pair, 16-byte word) items over the whole grid
+  const int64_t words = row_bytes / 16;
+  const int64_t items = (int64_t)npairs * words;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(it / words);
+    const int64_t w = it - (int64_t)t * words;
+    const uint4* src = reinterpret_cast<const uint4*>(buf + (int64_t)keep[m + t] * row_bytes) + w;
+    uint4* dst = reinterpret_cast<uint4*>(buf + (int64_t)hole[t] * row_bytes) + w;
+    *dst = __ldcs(src);
+  }
+}
+
 }  // namespace exitc

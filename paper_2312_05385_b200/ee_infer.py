@@ -30,7 +30,8 @@ import numpy as np
 
 from paper_2312_05385_b200 import _native as nat
 from paper_2312_05385_b200.errors import ParameterError
-from paper_2312_05385_b200.heads import (ExitController, LargeRampHead, SlotTable, compact_meta, compact_rows,
+from paper_2312_05385_b200.convnet import can_run_into, run_into
+from paper_2312_05385_b200.heads import (ExitController, LargeRampHead, SlotTable, compact_fill, compact_meta, compact_rows,
                                         exit_from_logits, gemm)
 
 # North star: a sample whose confidence lies within 1e-5 of a threshold is a
@@ -350,6 +351,10 @@ class CompactRunner:
                 for j in range(a, e + 1):
                     h = pipe.stages[j](h)
         self.x_in[0].copy_(example)  # run() without an input replays the example
+        # segments whose last stage ends in a routed residual block compact in place
+        self.fill = [k < len(self.segments) - 1 and b <= 8192 and can_run_into(pipe.stages[e])
+                     and self.x_in[k + 1].is_contiguous(memory_format=torch.channels_last)
+                     for k, (a, e) in enumerate(self.segments)]
         self.graphs = {}
         self.pool = torch.cuda.graph_pool_handle()
         self.out = BatchResult(self.slots.label[:b], self.slots.site[:b], self.slots.err[:b],
@@ -367,7 +372,7 @@ class CompactRunner:
         alive, rows = self.alive_in[k][:bb], self.rows_in[k][:bb]
         last = k == len(self.segments) - 1
         with torch.no_grad():
-            for j in range(a, e + 1 if not last else e):
+            for j in range(a, e):
                 h = self.pipe.stages[j](h)
             if last:
                 logits = self.pipe.stages[e](h).float()
@@ -375,12 +380,23 @@ class CompactRunner:
                 exit_from_logits(logits.contiguous(), 2.0, conf="maxprob", site=self.R, alive=alive,
                                  slot=rows, slots=self.slots, compact=False)
                 return
+            if self.fill[k]:
+                # the segment's last block writes straight into the next segment's
+                # input buffer, which is then compacted in place: only survivors
+                # above the live count move (a few rows), not every survivor
+                h = run_into(self.pipe.stages[e], h, self.x_in[k + 1][:bb])
+            else:
+                h = self.pipe.stages[e](h)
             res = self.pipe.ramps[e](h, self.th[k:k + 1], alive=alive, slot=rows, slots=self.slots)
             self.ramp_err[k].index_copy_(0, rows.long(), res.err)
             self.ramp_label[k].index_copy_(0, rows.long(), res.label)
-            compact_rows(h, res.keep, res.n_keep, out=self.x_in[k + 1])
-            compact_meta(res.keep, res.n_keep, rows, self.B, self.B, self.rows_in[k + 1],
-                         self.alive_in[k + 1], self.n_live[k:k + 1])
+            if self.fill[k]:
+                compact_fill(self.x_in[k + 1], res.keep, res.n_keep, bb, rows, self.B, self.rows_in[k + 1],
+                             self.alive_in[k + 1], self.n_live[k:k + 1])
+            else:
+                compact_rows(h, res.keep, res.n_keep, out=self.x_in[k + 1])
+                compact_meta(res.keep, res.n_keep, rows, self.B, self.B, self.rows_in[k + 1],
+                             self.alive_in[k + 1], self.n_live[k:k + 1])
             self.n_host[k:k + 1].copy_(self.n_live[k:k + 1], non_blocking=True)
 
     def _graph(self, k: int, bb: int):

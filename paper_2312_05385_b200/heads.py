@@ -207,6 +207,22 @@ def compact_meta(keep, n_keep, rows_in, cap: int, dummy: int, rows_out, alive_ou
         rows_out.data_ptr(), alive_out.data_ptr(), nat.ptr(n_out), nat.stream_handle(torch)))
 
 
+def compact_fill(buf, keep, n_keep, rows: int, rows_in, dummy: int, rows_out, alive_out, n_out=None):
+    """In-place compaction of buf's first `rows` rows ([B, ...], contiguous or
+    channels_last) to the survivors `keep` lists: survivors below n_keep stay,
+    the ones above move into the exited rows' places (ee_compact_fill), and
+    rows_out / alive_out / n_out describe the new order like compact_meta."""
+    torch = nat.torch_cuda()
+    if not _rows_dense(buf):
+        raise ParameterError("compact_fill needs a dense row layout")
+    row_bytes = buf.numel() // max(buf.shape[0], 1) * buf.element_size()
+    if rows_in is not None and rows_in.data_ptr() == rows_out.data_ptr():
+        raise ParameterError("rows_out must not alias rows_in")
+    nat.check(nat.load_library().ee_compact_fill(
+        buf.data_ptr(), row_bytes, keep.data_ptr(), n_keep.data_ptr(), int(rows), nat.ptr(rows_in),
+        int(dummy), rows_out.data_ptr(), alive_out.data_ptr(), nat.ptr(n_out), nat.stream_handle(torch)))
+
+
 def linear_tc(x, weight, bias=None, *, splits: int = 0, out_bf16: bool = False):
     """[M, N] = x bf16 [M, K] @ weight bf16 [N, K]^T + bias, fp32 out by default
     (ramp-head logits): `gemm` with no activation."""

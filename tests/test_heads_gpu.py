@@ -149,3 +149,43 @@ def test_wide_head_epilogue_matches_torch(cuda, k, conf):
     assert int(res.label[5]) == 17
     assert torch.allclose(res.err.double().cpu(), err_ref.cpu(), atol=2e-5, rtol=0)
     assert torch.equal(res.exits.bool().cpu(), (res.err.double() < thr).cpu())
+
+
+@pytest.mark.parametrize("rows,row_elems,seed", [(256, 3136 * 8, 0), (48, 8 * 8 * 256, 1), (7, 64, 2),
+                                                 (1000, 16, 3), (32, 16, 4)])
+def test_compact_fill_in_place(cuda, rows, row_elems, seed):
+    """ee_compact_fill (CompactRunner's in-place compaction) against a host
+    restatement: survivors below n_keep stay, the ones above move ascending into
+    the exited rows' places below n_keep, request slots follow their rows,
+    padding rows read alive = 0 and the dummy slot."""
+    from paper_2312_05385_b200.heads import compact_fill
+
+    rng = np.random.default_rng(seed)
+    for frac in (0.0, 0.05, 0.5, 0.97, 1.0):
+        alive = rng.random(rows) >= frac
+        keep = np.flatnonzero(alive).astype(np.int32)
+        nk = keep.size
+        data = torch.randn(rows, row_elems, device="cuda").to(torch.bfloat16)
+        orig = data.clone()
+        d_keep = torch.zeros(rows, dtype=torch.int32, device="cuda")
+        d_keep[:nk] = torch.from_numpy(keep).cuda()
+        d_nk = torch.tensor([nk], dtype=torch.int32, device="cuda")
+        rows_in = torch.from_numpy(rng.permutation(rows).astype(np.int32) + 5).cuda()
+        rows_out = torch.full((rows,), -7, dtype=torch.int32, device="cuda")
+        alive_out = torch.full((rows,), 9, dtype=torch.uint8, device="cuda")
+        n_out = torch.zeros(1, dtype=torch.int32, device="cuda")
+        compact_fill(data, d_keep, d_nk, rows, rows_in, 12345, rows_out, alive_out, n_out)
+        # host restatement of the pairing
+        src = np.arange(rows)
+        stay = keep[keep < nk]
+        holes = np.setdiff1d(np.arange(nk), stay)
+        movers = keep[keep >= nk]
+        assert holes.size == movers.size
+        src[holes] = movers
+        ri = rows_in.cpu().numpy()
+        want_rows = np.where(np.arange(rows) < nk, ri[src], 12345)
+        assert np.array_equal(rows_out.cpu().numpy(), want_rows)
+        assert np.array_equal(alive_out.cpu().numpy(), (np.arange(rows) < nk).astype(np.uint8))
+        assert int(n_out.item()) == nk
+        got = data[:nk].cpu()
+        assert torch.equal(got, orig.cpu()[torch.from_numpy(src[:nk]).long()])
