@@ -400,6 +400,12 @@ int ee_decode_attention_bf16(const void* d_qkv, const void* d_kv, const int64_t*
 int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
                     const int32_t* d_nkeep, int64_t max_rows, void* d_dst, void* stream);
 
+/* Per-request signal tables of a compacted batch: d_err_table[d_rows[i]] =
+ * d_err[i], d_label_table[d_rows[i]] = d_label[i] for i < n (one launch; the
+ * padding rows' dummy slot is a valid table entry). */
+int ee_scatter_signals(const float* d_err, const int32_t* d_label, const int32_t* d_rows, int64_t n,
+                       float* d_err_table, int32_t* d_label_table, void* stream);
+
 /* In-place compaction of d_buf [rows, row_bytes] (rows <= 8192, row_bytes % 16
  * == 0, 16-byte aligned) to the *d_nkeep survivors d_keep lists (ascending, as
  * the exit controller writes it): survivors below *d_nkeep stay in place and

@@ -3070,6 +3070,17 @@ int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
   return EE_OK;
 }
 
+int ee_scatter_signals(const float* d_err, const int32_t* d_label, const int32_t* d_rows, int64_t n,
+                       float* d_err_table, int32_t* d_label_table, void* stream) {
+  if (n < 1) return EE_OK;
+  if (!d_err || !d_label || !d_rows || !d_err_table || !d_label_table) return fail(EE_ERR_ARG, "null pointer");
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 256), 256);
+  exitc::k_scatter_signals<<<blocks, 256, 0, (cudaStream_t)stream>>>(d_err, d_label, d_rows, n, d_err_table,
+                                                                      d_label_table);
+  EE_LAUNCH_CHECK();
+  return EE_OK;
+}
+
 int ee_compact_fill(void* d_buf, int64_t row_bytes, const int32_t* d_keep, const int32_t* d_nkeep,
                     int64_t rows, const int32_t* d_rows_in, int32_t dummy, int32_t* d_rows_out,
                     uint8_t* d_alive_out, int32_t* d_n_out, void* stream) {

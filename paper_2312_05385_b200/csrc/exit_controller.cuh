@@ -483,6 +483,18 @@ __global__ void k_compact_meta(const int32_t* __restrict__ keep, const int32_t* 
   }
 }
 
+// a compacted batch's ramp signals into the per-request tables (one launch for
+// both, no index conversion): table[rows[i]] = value[i]
+__global__ void k_scatter_signals(const float* __restrict__ err, const int32_t* __restrict__ label,
+                                  const int32_t* __restrict__ rows, int64_t n, float* __restrict__ err_tab,
+                                  int32_t* __restrict__ label_tab) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = rows[i];
+    err_tab[s] = err[i];
+    label_tab[s] = label[i];
+  }
+}
+
 // In-place compaction of a batch buffer: the survivors already below n_keep
 // stay where they are and only the survivors at or above n_keep move, in
 // ascending order, into the exited rows' places below n_keep (ascending), so

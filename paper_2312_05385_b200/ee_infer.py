@@ -31,8 +31,8 @@ import numpy as np
 from paper_2312_05385_b200 import _native as nat
 from paper_2312_05385_b200.errors import ParameterError
 from paper_2312_05385_b200.convnet import can_run_into, run_into
-from paper_2312_05385_b200.heads import (ExitController, LargeRampHead, SlotTable, compact_fill, compact_meta, compact_rows,
-                                        exit_from_logits, gemm)
+from paper_2312_05385_b200.heads import (ExitController, LargeRampHead, SlotTable, compact_fill, compact_meta,
+                                        compact_rows, exit_from_logits, gemm, scatter_signals)
 
 # North star: a sample whose confidence lies within 1e-5 of a threshold is a
 # near-tie — its exit decision may legitimately differ from an fp64 CPU oracle,
@@ -198,8 +198,7 @@ class EEPipeline:
                                out_err=ramp_err[r], out_label=ramp_label[r], compact=False)
                 else:
                     res = head(h, th, alive=alive, slot=rows, slots=slots)
-                    ramp_err[r].index_copy_(0, rows.long(), res.err)
-                    ramp_label[r].index_copy_(0, rows.long(), res.label)
+                    scatter_signals(res.err, res.label, rows, ramp_err[r], ramp_label[r])
                 if timed:
                     ev = torch.cuda.Event(enable_timing=True)
                     ev.record()
@@ -388,8 +387,7 @@ class CompactRunner:
             else:
                 h = self.pipe.stages[e](h)
             res = self.pipe.ramps[e](h, self.th[k:k + 1], alive=alive, slot=rows, slots=self.slots)
-            self.ramp_err[k].index_copy_(0, rows.long(), res.err)
-            self.ramp_label[k].index_copy_(0, rows.long(), res.label)
+            scatter_signals(res.err, res.label, rows, self.ramp_err[k], self.ramp_label[k])
             if self.fill[k]:
                 compact_fill(self.x_in[k + 1], res.keep, res.n_keep, bb, rows, self.B, self.rows_in[k + 1],
                              self.alive_in[k + 1], self.n_live[k:k + 1])

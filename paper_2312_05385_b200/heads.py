@@ -207,6 +207,20 @@ def compact_meta(keep, n_keep, rows_in, cap: int, dummy: int, rows_out, alive_ou
         rows_out.data_ptr(), alive_out.data_ptr(), nat.ptr(n_out), nat.stream_handle(torch)))
 
 
+def scatter_signals(err, label, rows, err_table, label_table):
+    """err_table[rows[i]] = err[i], label_table[rows[i]] = label[i] (one launch:
+    ee_scatter_signals; rows int32 request slots)."""
+    torch = nat.torch_cuda()
+    n = rows.numel()
+    if err.dtype != torch.float32 or label.dtype != torch.int32 or rows.dtype != torch.int32:
+        raise ParameterError("scatter_signals takes fp32 err, int32 label and int32 rows")
+    if err.numel() < n or label.numel() < n:
+        raise ParameterError("fewer signals than rows")
+    nat.check(nat.load_library().ee_scatter_signals(
+        err.data_ptr(), label.data_ptr(), rows.data_ptr(), n, err_table.data_ptr(), label_table.data_ptr(),
+        nat.stream_handle(torch)))
+
+
 def compact_fill(buf, keep, n_keep, rows: int, rows_in, dummy: int, rows_out, alive_out, n_out=None):
     """In-place compaction of buf's first `rows` rows ([B, ...], contiguous or
     channels_last) to the survivors `keep` lists: survivors below n_keep stay,
