@@ -486,6 +486,22 @@ int ee_synth_columns(const uint64_t* raw, int64_t n_raw, int64_t* io_pos, int32_
                      double miscal_late, int32_t n_labels, double* errs, int32_t* labels,
                      int32_t* finals);
 
+/* Device-scheduled compaction: one executable graph that runs a compacted
+ * batch's segments back to back with no host round trip. Segment 0 runs
+ * graphs[nb - 1] (bucket h_buckets[nb - 1] = the full batch); before segment
+ * k >= 1 a one-thread kernel reads d_n_live[k - 1] (the live rows segment
+ * k - 1 left, written on the device) and sets a SWITCH conditional node to the
+ * smallest bucket >= it, whose body is graphs[k * nb + j] as a child graph
+ * (no body when no row is live: the rest of the chain does nothing).
+ * graphs: cudaGraph_t [nseg * nb] (NULL = never needed); reset: an optional
+ * graph run first. The graphs may contain kernels, memsets and device-to-
+ * device copies only (CUDA conditional-body rules); they are cloned. */
+typedef struct ee_seg_chain ee_seg_chain;
+int ee_seg_chain_create(void* const* graphs, int32_t nseg, int32_t nb, const int32_t* h_buckets,
+                        const int32_t* d_n_live, void* reset, ee_seg_chain** out);
+int ee_seg_chain_launch(ee_seg_chain* chain, void* stream);
+void ee_seg_chain_destroy(ee_seg_chain* chain);
+
 #ifdef __cplusplus
 }
 #endif

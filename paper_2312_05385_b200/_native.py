@@ -101,6 +101,9 @@ SIGNATURES = {
     "ee_maxpool_nhwc_bf16": (ctypes.c_int, [_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
                                             _vp, _vp]),
     "ee_bias_act_bf16": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i64, _c_i32, _vp, _vp]),
+    "ee_seg_chain_create": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _vp, _vp, _vp]),
+    "ee_seg_chain_launch": (ctypes.c_int, [_vp, _vp]),
+    "ee_seg_chain_destroy": (None, [_vp]),
     "ee_scatter_signals": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _vp, _vp, _vp]),
     "ee_compact_fill": (ctypes.c_int, [_vp, _c_i64, _vp, _vp, _c_i64, _vp, _c_i32, _vp, _vp, _vp, _vp]),
     "ee_compact_meta": (ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i32, _vp, _vp, _vp, _vp]),

@@ -3070,6 +3070,114 @@ int ee_compact_rows(const void* d_src, int64_t row_bytes, const int32_t* d_keep,
   return EE_OK;
 }
 
+}  // extern "C"
+
+// before segment k: the smallest bucket >= the live rows segment k - 1 left
+// (nb = no body: nothing is live)
+__global__ void k_seg_select(cudaGraphConditionalHandle h, const int32_t* __restrict__ n_live,
+                             const int32_t* __restrict__ buckets, int nb) {
+  const int n = *n_live;
+  unsigned v = (unsigned)nb;
+  if (n > 0) {
+    v = (unsigned)(nb - 1);
+    for (int j = 0; j < nb; ++j)
+      if (buckets[j] >= n) {
+        v = (unsigned)j;
+        break;
+      }
+  }
+  cudaGraphSetConditional(h, v);
+}
+
+struct ee_seg_chain {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int32_t* d_buckets = nullptr;
+};
+
+extern "C" {
+void ee_seg_chain_destroy(ee_seg_chain* c) {
+  if (!c) return;
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->d_buckets) cudaFree(c->d_buckets);
+  delete c;
+}
+
+int ee_seg_chain_create(void* const* graphs, int32_t nseg, int32_t nb, const int32_t* h_buckets,
+                        const int32_t* d_n_live, void* reset, ee_seg_chain** out) {
+  if (!out || !graphs || !h_buckets || !d_n_live || nseg < 1 || nb < 1) return fail(EE_ERR_ARG, "bad chain");
+  if (!graphs[nb - 1]) return fail(EE_ERR_ARG, "segment 0 needs the full-batch graph");
+  *out = nullptr;
+  auto* c = new ee_seg_chain();
+  auto bail = [&](cudaError_t e, const char* what) {
+    ee_seg_chain_destroy(c);
+    return fail(EE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaMalloc(&c->d_buckets, (size_t)nb * 4);
+  if (e != cudaSuccess) return bail(e, "bucket table");
+  e = cudaMemcpy(c->d_buckets, h_buckets, (size_t)nb * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return bail(e, "bucket table");
+  e = cudaGraphCreate(&c->graph, 0);
+  if (e != cudaSuccess) return bail(e, "graph");
+  cudaGraphNode_t prev = nullptr;
+  auto dep = [&]() { return prev ? 1 : 0; };
+  if (reset) {
+    e = cudaGraphAddChildGraphNode(&prev, c->graph, nullptr, 0, static_cast<cudaGraph_t>(reset));
+    if (e != cudaSuccess) return bail(e, "reset node");
+  }
+  {
+    cudaGraphNode_t n0;
+    e = cudaGraphAddChildGraphNode(&n0, c->graph, prev ? &prev : nullptr, dep(),
+                                   static_cast<cudaGraph_t>(graphs[nb - 1]));
+    if (e != cudaSuccess) return bail(e, "segment 0");
+    prev = n0;
+  }
+  for (int k = 1; k < nseg; ++k) {
+    cudaGraphConditionalHandle h;
+    e = cudaGraphConditionalHandleCreate(&h, c->graph, 0, 0);
+    if (e != cudaSuccess) return bail(e, "conditional handle");
+    cudaKernelNodeParams kp{};
+    const int32_t* nl = d_n_live + (k - 1);
+    const int32_t* bk = c->d_buckets;
+    int nbv = nb;
+    void* args[] = {&h, &nl, &bk, &nbv};
+    kp.func = reinterpret_cast<void*>(k_seg_select);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    cudaGraphNode_t sel;
+    e = cudaGraphAddKernelNode(&sel, c->graph, &prev, 1, &kp);
+    if (e != cudaSuccess) return bail(e, "selector node");
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeSwitch;
+    cp.conditional.size = (unsigned)nb;
+    cudaGraphNode_t sw;
+    e = cudaGraphAddNode(&sw, c->graph, &sel, 1, &cp);
+    if (e != cudaSuccess) return bail(e, "switch node");
+    for (int j = 0; j < nb; ++j) {
+      void* g = graphs[(size_t)k * nb + j];
+      if (!g) continue;
+      cudaGraphNode_t body;
+      e = cudaGraphAddChildGraphNode(&body, cp.conditional.phGraph_out[j], nullptr, 0, static_cast<cudaGraph_t>(g));
+      if (e != cudaSuccess) return bail(e, "switch body");
+    }
+    prev = sw;
+  }
+  e = cudaGraphInstantiate(&c->exec, c->graph, 0);
+  if (e != cudaSuccess) return bail(e, "instantiate");
+  *out = c;
+  return EE_OK;
+}
+
+int ee_seg_chain_launch(ee_seg_chain* c, void* stream) {
+  if (!c || !c->exec) return fail(EE_ERR_ARG, "null chain");
+  EE_CUDA(cudaGraphLaunch(c->exec, (cudaStream_t)stream));
+  return EE_OK;
+}
+
 int ee_scatter_signals(const float* d_err, const int32_t* d_label, const int32_t* d_rows, int64_t n,
                        float* d_err_table, int32_t* d_label_table, void* stream) {
   if (n < 1) return EE_OK;

@@ -363,7 +363,7 @@ class CompactRunner:
     def set_thresholds(self, thresholds):
         self.th.copy_(self.th.new_tensor([float(t) for t in thresholds]))
 
-    def _segment(self, k: int, bb: int):
+    def _segment(self, k: int, bb: int, host_count: bool = True):
         """Segment k at bucket bb: the eager body the graphs capture."""
         torch = nat.torch_cuda()
         a, e = self.segments[k]
@@ -395,7 +395,8 @@ class CompactRunner:
                 compact_rows(h, res.keep, res.n_keep, out=self.x_in[k + 1])
                 compact_meta(res.keep, res.n_keep, rows, self.B, self.B, self.rows_in[k + 1],
                              self.alive_in[k + 1], self.n_live[k:k + 1])
-            self.n_host[k:k + 1].copy_(self.n_live[k:k + 1], non_blocking=True)
+            if host_count:
+                self.n_host[k:k + 1].copy_(self.n_live[k:k + 1], non_blocking=True)
 
     def _graph(self, k: int, bb: int):
         g = self.graphs.get((k, bb))
@@ -412,6 +413,67 @@ class CompactRunner:
             self.graphs[(k, bb)] = g
         return g
 
+    def device_chain(self):
+        """Schedule the whole batch on the device (ee_seg_chain): every (segment,
+        bucket) graph is captured once, and one executable graph runs segment 0
+        at the full batch, then before each later segment a one-thread kernel
+        reads the live count the previous segment left and a SWITCH node runs
+        that segment at the smallest bucket >= it. No host round trip and no
+        lag: each segment runs at the bucket of its own live rows."""
+        if getattr(self, "_chain", None) is not None:
+            return self._chain
+        import ctypes
+
+        torch = nat.torch_cuda()
+        lib = nat.load_library()
+        keep, ptrs = [], []
+
+        def capture(body):
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                body()  # warm-up (idempotent on the live state)
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(g, pool=self.pool):
+                body()
+            keep.append(g)
+            return g.raw_cuda_graph()
+
+        reset = capture(self._reset)
+        nb = len(self.buckets)
+        for k in range(len(self.segments)):
+            for bb in self.buckets:
+                if k == 0 and bb != self.B:
+                    ptrs.append(None)
+                    continue
+                ptrs.append(capture(lambda k=k, bb=bb: self._segment(k, bb, host_count=False)))
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        bk = (ctypes.c_int32 * nb)(*self.buckets)
+        chain = ctypes.c_void_p()
+        nat.check(lib.ee_seg_chain_create(arr, len(self.segments), nb, bk, self.n_live.data_ptr(), reset,
+                                          ctypes.byref(chain)))
+        self._chain_graphs = keep  # their memory pool backs the chain
+        self._chain = chain
+        return chain
+
+    def run_device(self, x=None) -> BatchResult:
+        """One compacted batch through device_chain(): a single graph launch."""
+        torch = nat.torch_cuda()
+        chain = self.device_chain()
+        if x is not None:
+            self.x_in[0].copy_(x)
+        nat.check(nat.load_library().ee_seg_chain_launch(chain, nat.stream_handle(torch)))
+        return self.out
+
+    def __del__(self):
+        chain = getattr(self, "_chain", None)
+        if chain is not None:
+            try:
+                nat.load_library().ee_seg_chain_destroy(chain)
+            except Exception:
+                pass
+
     def bucket(self, n: int) -> int:
         for bb in self.buckets:
             if bb >= n:
@@ -420,6 +482,7 @@ class CompactRunner:
 
     def _reset(self):
         torch = nat.torch_cuda()
+        self.n_live.zero_()  # a skipped segment reads as no live rows (device_chain)
         self.slots.label.fill_(-1)
         self.slots.site.fill_(-1)
         self.slots.err.fill_(float("nan"))

@@ -212,3 +212,53 @@ def test_overlapped_ramps_equal_serial_ramps(cuda):
         for f in ("released_site", "released_label", "released_err", "ramp_err", "ramp_label", "final_label"):
             assert torch.equal(getattr(a, f), getattr(ser, f)), f
     assert np.all(over.release_ms > 0)
+
+
+@pytest.mark.parametrize("config", ["resnet18_bf16", "resnet50_bf16", "bert_bf16"])
+def test_device_scheduled_compaction_matches_host_schedule(cuda, config):
+    """CompactRunner.run_device (one graph: SWITCH nodes pick each segment's
+    bucket from the device's live count) releases what the host-scheduled
+    runner and feedback mode release off the margin, censors later ramps, and
+    skips the remaining segments once every row has exited."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    if config == "resnet18_bf16":
+        pipe, m = ee_infer.resnet18_cifar()
+        b, shape = 32, (3, 32, 32)
+    elif config == "resnet50_bf16":
+        pipe, m = ee_infer.resnet50_imagenet()
+        b, shape = 32, (3, 224, 224)
+    else:
+        pipe, m = ee_infer.bert_base()
+        b = 16
+    ee_infer.prepare_bf16(m, channels_last=not config.startswith("bert"))
+
+    def make(n):
+        if config.startswith("bert"):
+            return torch.randint(0, 30522, (n, 128), generator=g, device="cuda")
+        return torch.randn(n, *shape, generator=g, device="cuda").to(torch.bfloat16).contiguous(
+            memory_format=torch.channels_last)
+
+    th = _thresholds(pipe, make(64))
+    x = make(b)
+    runner = pipe.capture_compact(x, th)
+    for trial, xx in enumerate([x, make(b), x]):
+        dev = runner.run_device(xx)
+        site_d = dev.released_site.cpu().numpy().copy()
+        err_d = dev.ramp_err.cpu().numpy().copy()
+        host = runner.run(xx)
+        fb = pipe.run(xx, th)
+        near = _near(fb, th, 2e-3)
+        assert (site_d >= 0).all()
+        assert np.array_equal(site_d[~near], host.released_site.cpu().numpy()[~near]), trial
+        assert np.array_equal(site_d[~near], fb.released_site.cpu().numpy()[~near]), trial
+        for i in range(b):
+            s = site_d[i]
+            assert np.isfinite(err_d[: min(s + 1, pipe.n_ramps), i]).all(), (trial, i)
+            assert np.isnan(err_d[s + 1:, i]).all(), (trial, i)
+    runner.set_thresholds([2.0] * pipe.n_ramps)
+    out = runner.run_device(x)
+    assert (out.released_site.cpu() == 0).all()
+    runner.set_thresholds(th)
+    out = runner.run_device(x)
+    assert np.array_equal(out.released_site.cpu().numpy()[~_near(pipe.run(x, th), th, 2e-3)],
+                          pipe.run(x, th).released_site.cpu().numpy()[~_near(pipe.run(x, th), th, 2e-3)])

@@ -90,6 +90,17 @@ def bench(name, pipe, make_input, batch, iters, warmup=5):
         ev1.synchronize()
         ts.append(ev0.elapsed_time(ev1))
         exits.append(float((crun.out.released_site < pipe.n_ramps).float().mean().item()))
+    # the same compaction scheduled on the device: one graph launch per batch
+    # (SWITCH nodes pick each segment's bucket from the live count, no lag)
+    for _ in range(warmup):
+        crun.run_device()
+    tsd = []
+    for _ in range(iters):
+        ev0.record()
+        crun.run_device()
+        ev1.record()
+        ev1.synchronize()
+        tsd.append(ev0.elapsed_time(ev1))
     fb = pipe.run(x, th)
     margin = 2e-3
     e = fb.ramp_err.float()
@@ -103,6 +114,11 @@ def bench(name, pipe, make_input, batch, iters, warmup=5):
                             "graphs_captured": len(crun.graphs),
                             "matches_feedback_off_margin": agree,
                             "rows_within_margin": int(near.sum().item())}
+    dsite = crun.run_device().released_site
+    out["compact_device_graph"] = {"samples_per_s": batch / (np.mean(tsd) / 1e3),
+                                   "p50_batch_ms": float(np.percentile(tsd, 50)),
+                                   "matches_feedback_off_margin": bool(torch.equal(dsite[~near], fb.released_site[~near])),
+                                   "schedule": "one graph launch: SWITCH nodes choose each segment's bucket on the device"}
     # vanilla: the same stages, no ramps
     x = make_input(batch)
     with torch.no_grad():
