@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __shared__ double th[MAXR], steps[MAXR], cand[MAXR + 1][MAXR], accs[MAXR + 1], savs[MAXR + 1];
   __shared__ double sserve[MAXR + 1];
-  __shared__ int elig[MAXR], nelig, done;
+  __shared__ int elig[MAXR], posof[MAXR], nelig, done;
   __shared__ double acc_cur, sav_cur;
   __shared__ int n_evals, n_rows, status;
   const int tid = threadIdx.x;
@@ -84,7 +84,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc = t;
     }
   };
-  auto evaluate = [&](int nc) {
+  // delta: candidate c is the current thresholds th with only ramp elig[c]
+  // raised (every round after the first), so its exit site is the current one
+  // unless that ramp now fires first: site_c = (site0 > i && x_i < up_i) ? i : site0
+  auto evaluate = [&](int nc, bool delta) {
     if (tid <= MAXR) okc[tid] = 0;
     __syncthreads();
     const int lane = tid & 31;
@@ -100,11 +103,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int j = 0; j < RB; ++j) x[j] = (valid && j < r) ? win[(int64_t)i * wsi + j * wsj] : 0.0;
         const uint32_t wb = valid ? wbits[i] : 0u;
-        for (int c = 0; c < nc; ++c) {
-          int site = r;
-#pragma unroll
-          for (int j = RB - 1; j >= 0; --j)
-            if (j < r && x[j] < cand[c][j]) site = j;
+        auto emit = [&](int c, int site) {
           unsigned hit = 0;
           if (valid) {
             vals[(int64_t)c * n8 + i] = sserve[site];
@@ -112,6 +111,29 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           const unsigned b = __ballot_sync(0xffffffffu, hit);
           if (lane == 0 && b) atomicAdd(&okc[c], (unsigned)__popc(b));
+        };
+        if (delta) {
+          int site0 = r;
+#pragma unroll
+          for (int j = RB - 1; j >= 0; --j)
+            if (j < r && x[j] < th[j]) site0 = j;
+          // one candidate per eligible ramp: loop over the ramps (static
+          // register indices), candidate slot posof[j] (-1: not eligible)
+#pragma unroll
+          for (int j = 0; j < RB; ++j) {
+            if (j >= r) break;
+            const int c = posof[j];
+            if (c < 0) continue;
+            emit(c, (site0 > j && x[j] < cand[c][j]) ? j : site0);
+          }
+        } else {
+          for (int c = 0; c < nc; ++c) {
+            int site = r;
+#pragma unroll
+            for (int j = RB - 1; j >= 0; --j)
+              if (j < r && x[j] < cand[c][j]) site = j;
+            emit(c, site);
+          }
         }
       }
     } else {
@@ -152,7 +174,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (tid < r) cand[0][tid] = 0.0;
   __syncthreads();
-  evaluate(1);
+  evaluate(1, false);
   const double floor = __dsub_rn(1.0, p.budget);
   const double floor_eps = __dsub_rn(floor, ACC_EPS);
   if (tid == 0) {
@@ -176,7 +198,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid < 32) {  // eligible ramps in index order (r <= 31: one warp)
       const bool e = tid < r && th[tid] < 1.0;
       const unsigned m = __ballot_sync(0xffffffffu, e);
-      if (e) elig[__popc(m & ((1u << tid) - 1))] = tid;
+      const int pos = __popc(m & ((1u << tid) - 1));
+      if (e) elig[pos] = tid;
+      if (tid < MAXR) posof[tid] = e ? pos : -1;
       if (tid == 0) nelig = __popc(m);
     }
     __syncthreads();
@@ -193,7 +217,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
     mark(0);
-    evaluate(nelig);
+    evaluate(nelig, true);
     __shared__ int s_best;
     __shared__ unsigned s_viol;
     __shared__ bool s_allmin;
