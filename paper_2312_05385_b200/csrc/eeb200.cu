@@ -21,6 +21,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <atomic>
+#include <memory>
 #include <limits>
 #include <mutex>
 #include <string>
@@ -558,6 +561,10 @@ struct ee_workspace {
     cudaStream_t stream = nullptr;
   };
   std::vector<Stager> stagers;
+  // packed correctness rows go up chunk by chunk on their own stream while the
+  // scores are still streaming (stage_host_window)
+  cudaStream_t bits_stream = nullptr;
+  cudaEvent_t bits_start = nullptr, bits_done = nullptr;
   long long* d_diag_acc = nullptr;
   bool diag_acc_dirty = true;
   void* d_exit_done = nullptr;  // exit controllers' completion counter (self-resetting)
@@ -773,6 +780,9 @@ int ee_workspace_destroy(ee_workspace* ws) {
   }
   if (ws->h_stage) cudaFreeHost(ws->h_stage);
   if (ws->staged) cudaEventDestroy(ws->staged);
+  if (ws->bits_start) cudaEventDestroy(ws->bits_start);
+  if (ws->bits_done) cudaEventDestroy(ws->bits_done);
+  if (ws->bits_stream) cudaStreamDestroy(ws->bits_stream);
   delete ws;
   return EE_OK;
 }
@@ -1885,6 +1895,19 @@ static cudaError_t copy_to_device(ee_workspace* ws, void* dst, const void* src, 
 // scores stream to the device; `extra` bytes of output space follow the bits.
 // Returns with the copies queued on st (the caller synchronises before it
 // hands the host buffers back).
+// EEB200_TRACE_HOST=1: host timestamps (us since the call's entry) of the
+// host-buffer entry points' steps, on stderr (diagnostics)
+static bool trace_host() {
+  static const bool on = [] {
+    const char* e = std::getenv("EEB200_TRACE_HOST");
+    return e && *e == '1';
+  }();
+  return on;
+}
+static double trace_us(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+}
+
 static int stage_host_window(ee_workspace* ws, const double* h_scores, const double* h_correct_ext,
                              int64_t n, int32_t r, size_t extra, int32_t n_threads, cudaStream_t st,
                              double** d_scores, uint32_t** d_bits, unsigned char** d_extra) {
@@ -1907,27 +1930,85 @@ static int stage_host_window(ee_workspace* ws, const double* h_scores, const dou
   *d_scores = reinterpret_cast<double*>(base);
   *d_bits = reinterpret_cast<uint32_t*>(base + s_b);
   *d_extra = base + s_b + b_b;
-  int prc = EE_OK;
-  std::string perr;
+  if (r + 1 > EE_MAX_RAMPS + 1) return fail(EE_ERR_RAMPS, "more than 31 ramps");
+  if (!ws->bits_stream) {
+    EE_CUDA(cudaStreamCreateWithFlags(&ws->bits_stream, cudaStreamNonBlocking));
+    EE_CUDA(cudaEventCreateWithFlags(&ws->bits_start, cudaEventDisableTiming));
+    EE_CUDA(cudaEventCreateWithFlags(&ws->bits_done, cudaEventDisableTiming));
+  }
+  // the bit rows' device buffer may still be read by work queued on st
+  EE_CUDA(cudaEventRecord(ws->bits_start, st));
+  EE_CUDA(cudaStreamWaitEvent(ws->bits_stream, ws->bits_start, 0));
   // leave kStagers cores to the score copy threads when the scores are pageable
   const bool staged = n > 0 && r > 0 && (size_t)n * r * 8 > kChunk && !host_pinned(h_scores);
-  const int pack_threads =
-      n_threads > 0 ? n_threads
-      : staged      ? std::max(1, (int)std::thread::hardware_concurrency() - kStagers)
-                    : 0;
+  int pack_threads = n_threads > 0 ? n_threads
+                     : staged      ? std::max(1, (int)std::thread::hardware_concurrency() - kStagers)
+                                   : (int)std::max(1u, std::thread::hardware_concurrency());
+  pack_threads = (int)std::min<int64_t>(pack_threads, std::max<int64_t>(1, n / 4096));
+  // The pack runs in K row chunks: every worker packs its slice of chunk 0,
+  // then of chunk 1, ...; the issuing thread sends a chunk's H2D on
+  // bits_stream as soon as all workers have finished it, so only the last
+  // chunk's copy trails the pack (a single 4 MB copy of freshly written host
+  // lines ran at ~17 GB/s after the scores had gone up).
+  const int K = n >= (int64_t)1 << 18 ? 16 : 1;
+  std::vector<int> bad((size_t)pack_threads, 0);
+  std::unique_ptr<std::atomic<int>[]> chunk_done(new std::atomic<int>[K]);
+  for (int i = 0; i < K; ++i) chunk_done[i].store(0);
+  cudaError_t bce = cudaSuccess;
+  uint32_t* dbits = *d_bits;
+  auto worker = [&, h_correct_ext, n, r](int t) {
+    for (int i = 0; i < K; ++i) {
+      const int64_t lo = n * i / K, len = n * (i + 1) / K - lo;
+      pack_rows_host(h_correct_ext, lo + len * t / pack_threads, lo + len * (t + 1) / pack_threads, r + 1,
+                     ws->h_bits, &bad[(size_t)t]);
+      chunk_done[i].fetch_add(1, std::memory_order_acq_rel);
+    }
+  };
   std::thread packer([&] {
-    prc = ee_pack_correct_host(h_correct_ext, n, r + 1, ws->h_bits, pack_threads);
-    if (prc) perr = g_err;  // thread-local
+    std::vector<std::thread> pool;
+    for (int t = 0; t < pack_threads; ++t) pool.emplace_back(worker, t);
+    for (int i = 0; i < K; ++i) {  // the issuer: each chunk's copy as soon as it is packed
+      while (chunk_done[i].load(std::memory_order_acquire) < pack_threads) std::this_thread::yield();
+      const int64_t lo = n * i / K, len = n * (i + 1) / K - lo;
+      if (len > 0 && bce == cudaSuccess)
+        bce = cudaMemcpyAsync(dbits + lo, ws->h_bits + lo, (size_t)len * 4, cudaMemcpyHostToDevice,
+                              ws->bits_stream);
+    }
+    for (auto& th : pool) th.join();
   });
   cudaError_t ce = cudaSuccess;
-  if (n > 0 && r > 0) ce = copy_to_device(ws, *d_scores, h_scores, (size_t)n * r * 8, st);
-  packer.join();
-  if (prc) {
-    cudaStreamSynchronize(st);  // the caller's buffers stay in use until the copy is done
-    return fail(prc, perr);
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+  if (trace_host()) {
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[0], st);
   }
+  if (n > 0 && r > 0) ce = copy_to_device(ws, *d_scores, h_scores, (size_t)n * r * 8, st);
+  if (tev[1]) cudaEventRecord(tev[1], st);
+  const double t_issued = trace_us(t0);
+  packer.join();
+  if (trace_host())
+    std::fprintf(stderr, "[eeb200] stage: scores H2D issued %.1f us, pack joined %.1f us\n", t_issued,
+                 trace_us(t0));
+  EE_CUDA(cudaEventRecord(ws->bits_done, ws->bits_stream));
+  EE_CUDA(cudaStreamWaitEvent(st, ws->bits_done, 0));
+  for (int b : bad)
+    if (b) {
+      cudaStreamSynchronize(st);  // the caller's buffers stay in use until the copy is done
+      return fail(EE_ERR_NOT_BINARY, "correct_ext must contain only 0.0 and 1.0");
+    }
   if (ce != cudaSuccess) return fail(EE_ERR_CUDA, std::string("scores H2D: ") + cudaGetErrorString(ce));
-  if (n > 0) EE_CUDA(cudaMemcpyAsync(*d_bits, ws->h_bits, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+  if (bce != cudaSuccess) return fail(EE_ERR_CUDA, std::string("bits H2D: ") + cudaGetErrorString(bce));
+  if (tev[2]) {
+    cudaEventRecord(tev[2], st);
+    cudaEventSynchronize(tev[2]);
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, tev[0], tev[1]);
+    cudaEventElapsedTime(&b, tev[1], tev[2]);
+    std::fprintf(stderr, "[eeb200] stage (device): scores H2D %.1f us, bits H2D %.1f us (synchronised for tracing)\n",
+                 1e3 * a, 1e3 * b);
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
   return EE_OK;
 }
 
@@ -1955,8 +2036,10 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
   double* d_scores;
   uint32_t* d_bits;
   unsigned char* d_out;
+  const auto t0 = std::chrono::steady_clock::now();
   rc = stage_host_window(ws, h_scores, h_correct_ext, n, r, 2 * o_b, n_threads, st, &d_scores, &d_bits, &d_out);
   if (rc) return rc;
+  const double t_staged = trace_us(t0);
   double* d_acc = reinterpret_cast<double*>(d_out);
   double* d_sav = reinterpret_cast<double*>(d_out + o_b);
   rc = eval_dispatch(ws, d_scores, d_bits, n, r, h_serve, vanilla, h_th, c, mode, nullptr,
@@ -1965,9 +2048,18 @@ int ee_eval_thresholds_host(ee_workspace* ws, const double* h_scores, const doub
     cudaStreamSynchronize(st);
     return rc;
   }
+  const double t_eval = trace_us(t0);
+  if (trace_host()) {
+    EE_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[eeb200] sweep done %.1f us\n", trace_us(t0));
+  }
   EE_CUDA(cudaMemcpyAsync(h_acc, d_acc, (size_t)c * 8, cudaMemcpyDeviceToHost, st));
   EE_CUDA(cudaMemcpyAsync(h_sav, d_sav, (size_t)c * 8, cudaMemcpyDeviceToHost, st));
+  const double t_d2h = trace_us(t0);
   EE_CUDA(cudaStreamSynchronize(st));
+  if (trace_host())
+    std::fprintf(stderr, "[eeb200] eval_thresholds_host: staged %.1f us, sweep issued %.1f us, D2H issued %.1f us, done %.1f us\n",
+                 t_staged, t_eval, t_d2h, trace_us(t0));
   return EE_OK;
 }
 

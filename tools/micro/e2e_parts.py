@@ -36,3 +36,9 @@ out = {
     "cores": os.cpu_count(),
 }
 print(json.dumps(out))
+
+# the two together, as the call overlaps them: H2D issued, then the host pack
+def both():
+    d.copy_(hs, non_blocking=True)
+    nat.check(lib.ee_pack_correct_host(cext.ctypes.data, 1_000_000, 13, bits.data_ptr(), 0))
+print(json.dumps({"h2d_and_pack_overlapped_ms": med(both)}))
