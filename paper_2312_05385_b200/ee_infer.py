@@ -51,6 +51,7 @@ class BatchResult:
     release_ms: np.ndarray | None = None  # per request, from batch start (host, if timed)
     batch_ms: float | None = None
     thresholds: "object" = None  # the thresholds this batch was decided under (host list or CUDA f64 [R])
+    events: "object" = None  # (start, per-ramp marks, end) CUDA events of a graph-captured timed batch
 
     def near_ties(self, thresholds=None, eps: float = NEAR_TIE_EPS):
         """bool [B] (CUDA): rows with |err_j - t_j| < eps at some active ramp j the
@@ -113,10 +114,11 @@ class EEPipeline:
     def n_ramps(self) -> int:
         return len(self.ramp_order)
 
-    def capture(self, example, thresholds) -> "GraphRunner":
+    def capture(self, example, thresholds, *, timed: bool = False) -> "GraphRunner":
         """Capture one feedback-mode batch into a CUDA graph (static shapes; the
-        thresholds live in device memory, so retuning needs no re-capture)."""
-        return GraphRunner(self, example, thresholds)
+        thresholds live in device memory, so retuning needs no re-capture).
+        timed: every replay fills batch_ms / release_ms from event nodes."""
+        return GraphRunner(self, example, thresholds, timed=timed)
 
     def capture_compact(self, example, thresholds) -> "CompactRunner":
         """Compaction mode as CUDA graphs, one per (segment, batch bucket)."""
@@ -155,8 +157,15 @@ class EEPipeline:
             ramp_label = torch.full((R, b), -1, dtype=torch.int32, device=dev)
             final_label = torch.full((b,), -1, dtype=torch.int32, device=dev)
         marks = []
+        # timed="graph": inside a CUDA graph capture; the events become record
+        # nodes (external) and GraphRunner reads them after each replay
+        ext = timed == "graph"
+
+        def event():
+            return torch.cuda.Event(enable_timing=True, external=ext)
+
         if timed:
-            start = torch.cuda.Event(enable_timing=True)
+            start = event()
             start.record()
         main = torch.cuda.current_stream()
         side = None
@@ -188,7 +197,7 @@ class EEPipeline:
                         head(h, th, alive=alive, slot=rows, slots=slots,
                              out_err=ramp_err[r], out_label=ramp_label[r], compact=False)
                         if timed:
-                            ev = torch.cuda.Event(enable_timing=True)
+                            ev = event()
                             ev.record()
                             marks.append(ev)
                     r += 1
@@ -200,7 +209,7 @@ class EEPipeline:
                     res = head(h, th, alive=alive, slot=rows, slots=slots)
                     scatter_signals(res.err, res.label, rows, ramp_err[r], ramp_label[r])
                 if timed:
-                    ev = torch.cuda.Event(enable_timing=True)
+                    ev = event()
                     ev.record()
                     marks.append(ev)
                 if mode == "compact":
@@ -230,8 +239,12 @@ class EEPipeline:
             main.wait_stream(side)
         out = BatchResult(slots.label, slots.site, slots.err, ramp_err, ramp_label, final_label,
                           thresholds=th_record)
-        if timed:
-            end = torch.cuda.Event(enable_timing=True)
+        if timed == "graph":
+            end = event()
+            end.record()
+            out.events = (start, marks, end)
+        elif timed:
+            end = event()
             end.record()
             end.synchronize()
             t = [start.elapsed_time(m) for m in marks] + [start.elapsed_time(end)]
@@ -254,11 +267,12 @@ class GraphRunner:
     backbone + every ramp head / exit controller + scatter in one launch from
     the host (the per-ramp Python and launch overhead disappears)."""
 
-    def __init__(self, pipe: EEPipeline, example, thresholds):
+    def __init__(self, pipe: EEPipeline, example, thresholds, *, timed: bool = False):
         torch = nat.torch_cuda()
         self.pipe = pipe
         self.x = example.clone()
         self.th = torch.tensor([float(t) for t in thresholds], dtype=torch.float64, device="cuda")
+        self.timed = timed
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -267,7 +281,10 @@ class GraphRunner:
         torch.cuda.current_stream().wait_stream(s)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.out = pipe.run(self.x, self.th)
+            # timed: the batch start, every ramp's decision and the end are event
+            # record NODES of the graph (external events), so a replay is timed on
+            # the device exactly like an eager timed run
+            self.out = pipe.run(self.x, self.th, timed="graph" if timed else False)
 
     def set_thresholds(self, thresholds):
         self.th.copy_(self.th.new_tensor([float(t) for t in thresholds]))
@@ -276,6 +293,13 @@ class GraphRunner:
         if x is not None:
             self.x.copy_(x)
         self.graph.replay()
+        if self.timed:
+            start, marks, end = self.out.events
+            end.synchronize()
+            t = [start.elapsed_time(m) for m in marks] + [start.elapsed_time(end)]
+            site = self.out.released_site.cpu().numpy()
+            self.out.release_ms = np.asarray(t)[np.clip(site, 0, len(marks))]
+            self.out.batch_ms = t[-1]
         return self.out
 
 

@@ -123,9 +123,28 @@ def profile_pipeline(pipe, example, *, repeats: int = 5) -> ModelProfile:
     return ModelProfile(nodes, list(zip(nodes, nodes[1:])), lat, ramp, nodes[-1], name="live")
 
 
+def _graph_runner(pipe, bsz: int, example, thresholds):
+    """The pipeline's timed feedback-mode graph for batch size `bsz`, captured on
+    first use and kept on the pipeline (one graph per batch size the server forms)."""
+    cache = pipe.__dict__.setdefault("_live_graphs", {})
+    run = cache.get(bsz)
+    if run is None:
+        run = pipe.capture(example[:bsz], thresholds, timed=True)
+        run.version = None
+        cache[bsz] = run
+    return run
+
+
 def serve_live(pipe, requests, arrivals_ms, profile: ModelProfile, thresholds, params: LiveParams,
-               *, tune_on_trigger: bool = True) -> LiveReport:
-    """Serve `requests` [n, ...] (CUDA tensor) arriving at `arrivals_ms` (sorted)."""
+               *, tune_on_trigger: bool = True, graphs: bool = False) -> LiveReport:
+    """Serve `requests` [n, ...] (CUDA tensor) arriving at `arrivals_ms` (sorted).
+
+    graphs: every batch is one replay of a CUDA graph captured per batch size
+    (EEPipeline.capture(timed=True)): busy time and per-ramp release times come
+    from event nodes inside the graph, so a batch costs its GPU time instead of
+    the eager pipeline's per-kernel launch overhead. Decisions are the same
+    kernels on the same thresholds (a retune is copied into every graph's
+    device threshold vector before its next replay)."""
     torch = nat.torch_cuda()
     n = int(requests.shape[0])
     arrivals_ms = np.asarray(arrivals_ms, dtype=np.float64)
@@ -143,6 +162,7 @@ def serve_live(pipe, requests, arrivals_ms, profile: ModelProfile, thresholds, p
     rows: list[LiveRow] = []
     batches: list[LiveBatch] = []
     tunes: list[dict] = []
+    version = 0  # bumped by every retune; a graph copies the thresholds when behind
     i = 0
     free_at = float(arrivals_ms[0])
     first = float(arrivals_ms[0])
@@ -152,7 +172,14 @@ def serve_live(pipe, requests, arrivals_ms, profile: ModelProfile, thresholds, p
         j = i
         while j < n and j - i < params.max_batch and arrivals_ms[j] <= start:
             j += 1
-        res = pipe.run(requests[i:j], th_dev, mode="feedback", timed=True)
+        if graphs:
+            run = _graph_runner(pipe, j - i, requests, config.thresholds)
+            if run.version != version:
+                run.th.copy_(th_dev)
+                run.version = version
+            res = run.run(requests[i:j])
+        else:
+            res = pipe.run(requests[i:j], th_dev, mode="feedback", timed=True)
         busy = float(res.batch_ms)
         err = res.ramp_err.double().cpu().numpy()
         lab = res.ramp_label.cpu().numpy()
@@ -189,6 +216,7 @@ def serve_live(pipe, requests, arrivals_ms, profile: ModelProfile, thresholds, p
                               "accuracy": res_t.accuracy})
                 config = config.with_thresholds(new)
                 th_dev.copy_(th_dev.new_tensor(new))
+                version += 1
         i = j
     bits = [r.correct for r in rows]
     makespan = last_end - first

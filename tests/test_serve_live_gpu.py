@@ -14,7 +14,8 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def test_closed_loop_decisions_and_retunes_match_reference(cuda):
+@pytest.mark.parametrize("graphs", [False, True], ids=["eager", "graphs"])
+def test_closed_loop_decisions_and_retunes_match_reference(cuda, graphs):
     torch = cuda
     from paper_2312_05385_b200 import ee_infer
     from paper_2312_05385_b200.serve_live import LiveParams, profile_pipeline, serve_live
@@ -31,8 +32,9 @@ def test_closed_loop_decisions_and_retunes_match_reference(cuda):
     arrivals = np.cumsum(np.random.default_rng(4).exponential(0.05, size=n))
     params = LiveParams(max_batch=32, acc_constraint=0.97,
                         tuner=TunerParams(acc_loss_budget=0.05, accuracy_window=16, tuning_history=96))
-    rep = serve_live(pipe, x, arrivals, prof, th0, params)
+    rep = serve_live(pipe, x, arrivals, prof, th0, params, graphs=graphs)
     assert len(rep.rows) == n
+    assert all(b.busy_ms > 0 for b in rep.batches)
     sites = [s for s in __import__("paper_2312_05385_b200.graph", fromlist=["x"]).find_feasible_sites(prof)
              if s.position in {f"st{j}" for j in pipe.ramp_order}]
     R = len(sites)

@@ -11,9 +11,9 @@ from paper_2312_05385_b200.tuner import TunerParams
 
 torch.backends.cudnn.benchmark = True  # every batch shape 1..32 is autotuned in the warm-up below
 pipe, m = ee_infer.resnet18_cifar()
-# same backbone form as tools/bench_ee.py: BatchNorm folded, bf16, channels_last
-ee_infer.fold_batchnorm(m)
-m.to(memory_format=torch.channels_last).to(torch.bfloat16)
+# same backbone form as tools/bench_ee.py: BatchNorm folded, bf16, channels_last,
+# the blocks on the repo's kernels
+ee_infer.prepare_bf16(m, True)
 n = int(os.environ.get("N", 2048))
 g = torch.Generator(device="cuda").manual_seed(0)
 x = torch.randn(n, 3, 32, 32, generator=g, device="cuda").to(torch.bfloat16).contiguous(
@@ -31,7 +31,15 @@ arr = np.cumsum(np.random.default_rng(1).exponential(1.0 / rate, size=n))
 params = LiveParams(max_batch=32, acc_constraint=0.95, tuner=TunerParams(acc_loss_budget=0.02))
 serve_live(pipe, x[:256], arr[:256], prof, th0, params)  # warm
 t0 = time.perf_counter()
-rep = serve_live(pipe, x, arr, prof, th0, params)
+eager = serve_live(pipe, x, arr, prof, th0, params)
+wall_eager = time.perf_counter() - t0
+# every batch as one replay of a graph captured per batch size (captured here,
+# outside the measured loop, for every size 1..32 the server can form)
+for bsz in range(1, 33):
+    serve_live(pipe, x[:bsz], np.zeros(bsz), prof, th0, params, tune_on_trigger=False, graphs=True)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+rep = serve_live(pipe, x, arr, prof, th0, params, graphs=True)
 wall = time.perf_counter() - t0
 vanilla_ms = prof.model_latency(32)
 print(json.dumps({
@@ -40,4 +48,10 @@ print(json.dumps({
     "p50_ms": rep.p50_ms, "throughput_rps": rep.throughput_rps, "accuracy_vs_final": rep.accuracy,
     "exit_rate": float(np.mean([r.exit_site is not None for r in rep.rows])),
     "batches": len(rep.batches), "retunes": len(rep.tunes),
-    "vanilla_batch32_ms_profile": vanilla_ms, "host_wall_s": wall}))
+    "vanilla_batch32_ms_profile": vanilla_ms, "host_wall_s": wall,
+    "batches_as": "one CUDA graph replay per batch (captured per batch size; busy and release times from "
+                  "event nodes in the graph)",
+    "mean_batch_ms": float(np.mean([b.busy_ms for b in rep.batches])),
+    "eager": {"p50_ms": eager.p50_ms, "throughput_rps": eager.throughput_rps, "batches": len(eager.batches),
+              "retunes": len(eager.tunes), "mean_batch_ms": float(np.mean([b.busy_ms for b in eager.batches])),
+              "host_wall_s": wall_eager, "batches_as": "eager pipeline, CUDA events per ramp"}}))
