@@ -20,7 +20,11 @@ row-major [B*H*W, C] matrix, so
     epilogue; the stem's max pool is one NHWC pass (ee_maxpool_nhwc_bf16);
   * anything else (output channels not a multiple of 8) stays on cuDNN without
     a bias and takes bias / ReLU / shortcut in ONE fused NHWC pass
-    (ee_bias_act_bf16).
+    (ee_bias_act_bf16);
+  * the classifier (global average pool + fc): for up to 256 classes ONE
+    kernel, the fused ramp head (k_exit_fused: pool in fp32, fp32 FC over the
+    bf16 weight) asked for its logits only; wider heads pool with
+    k_pool_nhwc and run the fc on the tcgen05 GEMM. Logits are fp32.
 
 route_resnet() rebinds the forward of every block of a prepared torchvision
 ResNet in place, so an EEPipeline built on the model's modules picks it up.
@@ -33,7 +37,7 @@ from __future__ import annotations
 
 from paper_2312_05385_b200 import _native as nat
 from paper_2312_05385_b200.errors import ParameterError
-from paper_2312_05385_b200.heads import gemm
+from paper_2312_05385_b200.heads import ExitController, gemm, pool_bf16
 
 ACT = {None: 0, "relu": 3}
 _CONV_WORK: dict = {}  # conv shape -> ee_conv_workspace_size
@@ -260,6 +264,7 @@ def route_resnet(model):
                 blk.forward = BottleneckTC(blk)
             else:
                 blk.forward = BasicBlockTC(blk)
+    route_classifier(model)
     stem = Conv(model.conv1)
     model.conv1.forward = lambda x: stem(x, act="relu")
     model.relu.forward = lambda x: x  # applied by the stem's epilogue (blocks use their own)
@@ -271,3 +276,40 @@ def route_resnet(model):
         mp.forward = lambda x: maxpool(x, k, st, pd) if x.dtype == torch.bfloat16 and x.shape[1] % 8 == 0 \
             else torch.nn.functional.max_pool2d(x, k, st, pd)
     return model
+
+
+class ClassifierTC:
+    """avgpool + flatten + fc of a ResNet on the repo's kernels (bound to the
+    avgpool module; the fc module becomes the identity). A map that is not
+    channels_last bf16 keeps the library path."""
+
+    def __init__(self, model):
+        import torch
+
+        fc = model.fc
+        self.fc = fc
+        self.w = fc.weight.detach().to(torch.bfloat16).contiguous()
+        self.b = None if fc.bias is None else fc.bias.detach().float().contiguous()
+        self.fused = ExitController(self.w, self.b) if fc.out_features <= 256 else None
+        self.pool = model.avgpool.__class__.forward.__get__(model.avgpool)
+
+    def __call__(self, x):
+        import torch
+
+        if not (x.dim() == 4 and x.dtype == torch.bfloat16 and x.shape[1] % 8 == 0
+                and x.is_contiguous(memory_format=torch.channels_last)):
+            return self.fc.__class__.forward(self.fc, torch.flatten(self.pool(x), 1))
+        if self.fused is not None:  # pool + FC in one kernel; nobody "exits" (err < -1 never holds)
+            return self.fused(x, -1.0, want_logits=True, compact=False).logits
+        return gemm(pool_bf16(x), self.w, self.b, out_bf16=False)
+
+
+def route_classifier(model):
+    """Rebind a ResNet's avgpool to ClassifierTC (returns logits [B, classes]) and
+    its fc to the identity: both the model's own forward (avgpool -> flatten ->
+    fc) and an EEPipeline's final Sequential(avgpool, Flatten, fc) then run it."""
+    head = ClassifierTC(model)
+    model.avgpool.forward = head
+    model.fc.forward = lambda x: x if x.dim() == 2 and x.shape[1] == head.fc.out_features \
+        else head.fc.__class__.forward(head.fc, x)
+    return head
