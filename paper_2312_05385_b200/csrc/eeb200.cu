@@ -2557,6 +2557,13 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
   if (c % 4) return fail(EE_ERR_ARG, "channels must be a multiple of 4");
   if (!d_x || !d_out) return fail(EE_ERR_ARG, "null pointer");
   if (reinterpret_cast<uintptr_t>(d_x) % (x_bf16 ? 8 : 16)) return fail(EE_ERR_ARG, "misaligned map");
+  if (x_bf16 && hw <= 64 && c % 8 == 0 && reinterpret_cast<uintptr_t>(d_x) % 16 == 0) {
+    const dim3 g2((unsigned)ceil_div(c, 256), (unsigned)b);
+    pool::k_pool_nhwc_small<<<g2, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint16_t*>(d_x), c, hw,
+                                                                 static_cast<uint16_t*>(d_out));
+    EE_LAUNCH_CHECK();
+    return EE_OK;
+  }
   const dim3 grid((unsigned)ceil_div(c, 64), (unsigned)b);
   if (x_bf16)
     pool::k_pool_nhwc<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
@@ -3055,12 +3062,21 @@ __global__ void __launch_bounds__(256) k_add_layernorm_warp(
   const int nv = d / 8;
   const uint4* hr = reinterpret_cast<const uint4*>(h + row * d);
   float v[VPL][8];
-  uint4 hv[VPL], yv[VPL];
+  uint4 hv[VPL], yv[VPL], gv[VPL], bv[VPL];
+  // every load of the row (h, y) and of gamma / beta is issued up front: the
+  // scale/shift operands are not another dependent round trip per vector
+  // after the two reductions
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int t = lane + 32 * i;
     hv[i] = t < nv ? hr[t] : make_uint4(0u, 0u, 0u, 0u);
     if (y) yv[i] = t < nv ? reinterpret_cast<const uint4*>(y + row * d)[t] : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int t = lane + 32 * i;
+    gv[i] = t < nv ? __ldg(reinterpret_cast<const uint4*>(gamma) + t) : make_uint4(0u, 0u, 0u, 0u);
+    bv[i] = t < nv ? __ldg(reinterpret_cast<const uint4*>(beta) + t) : make_uint4(0u, 0u, 0u, 0u);
   }
   float s = 0.f;
 #pragma unroll
@@ -3099,8 +3115,7 @@ __global__ void __launch_bounds__(256) k_add_layernorm_warp(
   for (int i = 0; i < VPL; ++i) {
     const int t = lane + 32 * i;
     if (t >= nv) continue;
-    const uint4 gv = reinterpret_cast<const uint4*>(gamma)[t], bv = reinterpret_cast<const uint4*>(beta)[t];
-    const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
+    const uint32_t gw[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w}, bw[4] = {bv[i].x, bv[i].y, bv[i].z, bv[i].w};
     uint32_t o[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -3133,6 +3148,8 @@ int ee_add_layernorm_bf16(void* d_h, const void* d_y, const void* d_gamma, const
       k_add_layernorm_warp<1><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
     else if (vpl <= 2)
       k_add_layernorm_warp<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
+    else if (vpl <= 3)
+      k_add_layernorm_warp<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
     else if (vpl <= 4)
       k_add_layernorm_warp<4><<<blocks, 256, 0, (cudaStream_t)stream>>>(hh, yy, g, bb, (float)eps, d, rows, xx);
     else

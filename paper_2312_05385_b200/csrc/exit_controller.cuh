@@ -206,16 +206,18 @@ __global__ void __launch_bounds__(THREADS)
           acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
         }
       };
-      constexpr int DEPTH = 8;  // loads issued before any is consumed
-      int p = p_begin + sl;
-      for (; p + (DEPTH - 1) * SS < p_end; p += DEPTH * SS) {
+      // DEPTH loads issued before any is consumed; the last batch is predicated
+      // (zeros for absent positions leave the fp32 sums unchanged) so a short
+      // slice is one round of loads, not a dependent load per position
+      constexpr int DEPTH = 8;
+      for (int p = p_begin + sl; p < p_end; p += DEPTH * SS) {
         V v[DEPTH];
 #pragma unroll
-        for (int i = 0; i < DEPTH; ++i) v[i] = __ldg(reinterpret_cast<const V*>(base + (int64_t)(p + i * SS) * C));
+        for (int i = 0; i < DEPTH; ++i)
+          v[i] = p + i * SS < p_end ? __ldg(reinterpret_cast<const V*>(base + (int64_t)(p + i * SS) * C)) : V{};
 #pragma unroll
         for (int i = 0; i < DEPTH; ++i) add(v[i]);
       }
-      for (; p < p_end; p += SS) add(__ldg(reinterpret_cast<const V*>(base + (int64_t)p * C)));
     }
     part[threadIdx.x] = acc;
     __syncthreads();

@@ -77,4 +77,48 @@ __global__ void __launch_bounds__(256) k_pool_nhwc(const T* __restrict__ x, int 
   }
 }
 
+// Small channels_last maps (HW <= 64, e.g. the 7 x 7 layer4 output of a
+// ResNet-50), bf16, C % 8 == 0: a CTA covers 256 channels of one image as 32
+// groups of 8 channels (one 16-byte load per position) x 8 position slices;
+// every slice's loads (<= 8 positions) are in flight at once and the slices
+// meet in shared memory in slice order. The generic kernel above spends
+// 8192 tiny CTAs on a 256 x 2048 x 7 x 7 map with a dependent load chain each.
+__global__ void __launch_bounds__(256) k_pool_nhwc_small(const uint16_t* __restrict__ x, int C, int HW,
+                                                         uint16_t* __restrict__ out) {
+  __shared__ float part[8][256 + 4];
+  const int g = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int b = blockIdx.y, c0 = blockIdx.x * 256 + 8 * g;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < C) {
+    const uint16_t* base = x + ((int64_t)b * HW) * C + c0;
+    uint4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int p = sl + 8 * i;
+      v[i] = p < HW ? __ldcs(reinterpret_cast<const uint4*>(base + (int64_t)p * C)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[2 * e] += __uint_as_float(w[e] << 16);
+        a[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) part[sl][8 * g + e] = a[e];
+  __syncthreads();
+  const int c = blockIdx.x * 256 + (int)threadIdx.x;
+  if (c < C) {
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc += part[r][threadIdx.x];
+    uint32_t u = __float_as_uint(acc / (float)HW);
+    u += 0x7FFF + ((u >> 16) & 1);  // round to nearest even bf16
+    out[(int64_t)b * C + c] = (uint16_t)(u >> 16);
+  }
+}
+
 }  // namespace pool

@@ -143,7 +143,8 @@ def test_add_layernorm_matches_torch(cuda):
 
     g = torch.Generator(device="cuda").manual_seed(4)
     # rows >= 64 and d <= 2048 take the warp-per-row kernel (BERT 8192 x 768)
-    for rows, d in ((32, 1024), (7, 64), (160, 1024), (8192, 768), (100, 2048), (70, 24), (65, 4096)):
+    for rows, d in ((32, 1024), (7, 64), (160, 1024), (8192, 768), (100, 2048), (70, 24), (65, 4096),
+                    (64, 520), (96, 776)):
         h = torch.randn(rows, d, generator=g, device="cuda").to(torch.bfloat16)
         y = torch.randn(rows, d, generator=g, device="cuda").to(torch.bfloat16)
         gamma = (1 + 0.1 * torch.randn(d, generator=g, device="cuda")).to(torch.bfloat16)
