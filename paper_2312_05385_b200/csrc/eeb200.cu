@@ -2578,6 +2578,13 @@ int ee_pool_nhwc_bf16(const void* d_x, int32_t x_bf16, int64_t b, int32_t c, int
 }  // extern "C"
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+// two fp32 -> packed bf16x2 (lo in the low half), one cvt.rn instruction: the
+// same bits as torch's CUDA bf16 conversion (__float2bfloat16, NaN -> 0x7FFF)
+__device__ __forceinline__ uint32_t bf2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 __device__ __forceinline__ uint32_t bf_round(float f) {  // fp32 -> bf16 bits, nearest even
   uint32_t u = __float_as_uint(f);
   if ((u & 0x7f800000u) == 0x7f800000u) return (u >> 16) | ((u & 0xffffu) ? 0x40u : 0u);  // inf/NaN
@@ -3088,7 +3095,7 @@ __global__ void __launch_bounds__(256) k_add_layernorm_warp(
       uint32_t o[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        o[k] = bf_round(bf_lo(hw[k]) + bf_lo(yw[k])) | (bf_round(bf_hi(hw[k]) + bf_hi(yw[k])) << 16);
+        o[k] = bf2(bf_lo(hw[k]) + bf_lo(yw[k]), bf_hi(hw[k]) + bf_hi(yw[k]));
       if (t < nv) reinterpret_cast<uint4*>(h + row * d)[t] = make_uint4(o[0], o[1], o[2], o[3]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) v[i][2 * k] = bf_lo(o[k]), v[i][2 * k + 1] = bf_hi(o[k]);
@@ -3121,7 +3128,7 @@ __global__ void __launch_bounds__(256) k_add_layernorm_warp(
     for (int k = 0; k < 4; ++k) {
       const float a = (v[i][2 * k] - mean) * rstd * bf_lo(gw[k]) + bf_lo(bw[k]);
       const float b = (v[i][2 * k + 1] - mean) * rstd * bf_hi(gw[k]) + bf_hi(bw[k]);
-      o[k] = bf_round(a) | (bf_round(b) << 16);
+      o[k] = bf2(a, b);
     }
     reinterpret_cast<uint4*>(x + row * d)[t] = make_uint4(o[0], o[1], o[2], o[3]);
   }
