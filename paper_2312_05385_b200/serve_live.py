@@ -33,10 +33,10 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from paper_2312_05385_b200 import _native as nat
-from paper_2312_05385_b200.engine import EEConfig
+from paper_2312_05385_b200.engine import EEConfig, WindowEvaluator
 from paper_2312_05385_b200.errors import ParameterError
 from paper_2312_05385_b200.graph import ModelProfile, find_feasible_sites
-from paper_2312_05385_b200.trace import RampSignal, RequestRecord
+from paper_2312_05385_b200.trace import RampSignal, RequestRecord, WindowArrays
 from paper_2312_05385_b200.tuner import AccuracyMonitor, TunerParams, should_trigger, tune
 
 
@@ -159,6 +159,13 @@ def serve_live(pipe, requests, arrivals_ms, profile: ModelProfile, thresholds, p
     config = EEConfig(tuple(zip(sites, [float(t) for t in thresholds])))
     monitor = AccuracyMonitor(params.tuner.accuracy_window)
     history: list[RequestRecord] = []
+    # the history's columns, kept as a ring in step with `history` (same rows,
+    # same order), so a retune builds its device window from arrays instead of
+    # re-packing every RequestRecord (trace.window_arrays: ~0.8 ms per 1,000)
+    cap = max(1, params.tuner.tuning_history)
+    ring_err = np.empty((cap, R))
+    ring_ok = np.ones((cap, R + 1), dtype=np.uint8)
+    ring_start = 0
     rows: list[LiveRow] = []
     batches: list[LiveBatch] = []
     tunes: list[dict] = []
@@ -188,6 +195,7 @@ def serve_live(pipe, requests, arrivals_ms, profile: ModelProfile, thresholds, p
         rel_label = res.released_label.cpu().numpy()
         recs = []
         served = []
+        ok = (lab == fin[None, :]).T  # [batch, R] released label at ramp r == final label
         for q in range(j - i):
             rid = i + q
             sig = {sites[r].position: RampSignal(float(err[r, q]), int(lab[r, q])) for r in range(R)}
@@ -195,21 +203,30 @@ def serve_live(pipe, requests, arrivals_ms, profile: ModelProfile, thresholds, p
             recs.append(rec)
             site = int(rel_site[q])
             correct = bool(rel_label[q] == fin[q])
-            served.append((start + float(res.release_ms[q]), rid, rec, site, correct))
+            served.append((start + float(res.release_ms[q]), rid, rec, site, correct, q))
         batches.append(LiveBatch(start, busy, tuple(config.thresholds), recs, rel_site.copy()))
         served.sort(key=lambda t: (t[0], t[1]))  # release order feeds the monitor (serving.py:260)
         free_at = start + busy
         last_end = free_at
-        for release, rid, rec, site, correct in served:
+        for release, rid, rec, site, correct, q in served:
             queue = start - rec.arrival_ms
             rows.append(LiveRow(rid, rec.arrival_ms, queue, release - start, release - rec.arrival_ms,
                                 sites[site].position if site < R else None, correct, j - i))
             monitor.push(correct)
             history.append(rec)
+            slot = (ring_start + len(history) - 1) % cap
+            ring_err[slot] = err[:, q]
+            ring_ok[slot, :R] = ok[q]
             if len(history) > params.tuner.tuning_history:
                 history.pop(0)
+                ring_start = (ring_start + 1) % cap
             if tune_on_trigger and R and should_trigger(monitor, params.acc_constraint):
-                res_t = tune(history, sites, params.tuner, profile)
+                n_h = len(history)
+                order = (ring_start + np.arange(n_h)) % cap  # oldest first, as `history`
+                ev = WindowEvaluator.from_arrays(
+                    WindowArrays(ring_err[order], ring_ok[order]), sites, profile, batch=1,
+                    records=history)
+                res_t = tune(history, sites, params.tuner, profile, evaluator=ev)
                 new = res_t.threshold_vector(sites)
                 tunes.append({"after_request": rid, "history": list(history),
                               "thresholds": new, "savings_ms": res_t.savings_ms,
