@@ -283,7 +283,8 @@ struct PairCfg {
 template <int BN, int ACT, bool OUT_BF16, bool IM2COL = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias,
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
+                const float* __restrict__ bias,
                 const uint16_t* __restrict__ res, int M, int N, int K, const ConvGeom G) {
   using Cfg = PairCfg<BN>;
   constexpr int ST = Cfg::STAGES;
@@ -294,6 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   unsigned char* epi_smem = smem + ST * Cfg::STAGE;
   float* bias_smem = reinterpret_cast<float*>(epi_smem + Cfg::EPI);
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t rbar[16];  // residual box landed: epilogue warp x staging buffer
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -323,6 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       mbar_init(&tfull_bar[a], 1);   // one multicast MMA commit
       mbar_init(&tempty_bar[a], 16);  // the 16 epilogue warps of the pair (leader's copy used)
     }
+    for (int b = 0; b < 16; ++b) mbar_init(&rbar[b], 1);  // lane 0's expect_tx
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 accumulators
@@ -394,23 +397,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     int buf = 0;
     constexpr int NCH = BN / CW;  // chunks per tile; half h takes chunks [h*NCH/2 ...)
     const int c_lo = h * (NCH / 2) * CW, c_hi = h ? BN : (NCH / 2) * CW;
-    // the residual rows this lane adds in tile t, pulled into L2 ahead of use (one
-    // prefetch per 128-byte line) while the tile's MMAs still run
-    auto prefetch_res = [&](int t) {
-      if (res == nullptr || !OUT_BF16 || t >= tiles) return;
-      const int row = tile_m(t) * 256 + (int)rank * 128 + q * 32 + lane, nb = tile_n(t) * BN;
-      if (row >= M) return;
-      for (int cb = c_lo; cb < c_hi; cb += 64)
-        if (nb + cb < N)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(res + (int64_t)row * N + nb + cb));
+    // Residual (a ResNet shortcut, bf16 output only): lane 0 TMA-loads the next
+    // chunk's 32 x 64 residual box into the staging buffer that chunk will use
+    // (swizzled exactly like the output this warp writes there), one chunk ahead,
+    // so the residual arrives as one bulk request while this chunk drains; each
+    // lane then reads its own row from shared memory and overwrites it with the
+    // output. Every chunk alternates the two staging buffers.
+    const bool tres = res != nullptr && OUT_BF16;
+    uint64_t* rb = rbar + (warp - 2) * 2;
+    uint32_t rpar = 0;  // bit b: parity of the next wait on rb[b]
+    auto issue_res = [&](int t, int c0, int b) {  // lane 0
+      mbar_expect_tx(&rb[b], 4096);
+      tma_load(stage0 + b * 4096, &tmR, &rb[b], tile_n(t) * BN + c0,
+               tile_m(t) * 256 + (int)rank * 128 + q * 32);
     };
-    prefetch_res(pair);
+    if (tres && pair < tiles && c_lo < c_hi && lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmR)) : "memory");
+      issue_res(pair, c_lo, 0);
+    }
     for (int t = pair; t < tiles; t += pairs, ++ai) {
       const uint32_t a = ai & 1;
       const int row0 = tile_m(t) * 256 + (int)rank * 128 + q * 32;
       const int n0 = tile_n(t) * BN;
       const int rowoff = tile_rowoff(t);  // split-K: this split's region of the partial map
-      prefetch_res(t + pairs);  // one tile ahead (two measured slower: 224 vs 221 us, layer1)
       mbar_wait(&tfull_bar[a], (ai >> 1) & 1);
       fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
@@ -423,34 +432,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
 #pragma unroll 1
       for (int c0 = c_lo; c0 < c_hi; c0 += CW) {
         uint32_t v[CW];
+        if (tres && lane == 0) {  // the next chunk's residual into the other buffer
+          const bool last = c0 + CW >= c_hi;
+          const int tn = last ? t + pairs : t;
+          // the store that last read that buffer (two chunks ago) must be done with it
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          if (tn < tiles) issue_res(tn, last ? c_lo : c0 + CW, buf ^ 1);
+        }
         if constexpr (CW == 64) {
           tmem_ld32_nowait(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
           tmem_ld32_nowait(tbase + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
         } else {
           tmem_ld32_nowait(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
         }
-        // residual row segment of this lane (row0 + lane, CW columns), loaded
-        // while the TMEM read is in flight (bf16 output: CW = 64 = 8 x 16 B)
-        uint4 rv[CW / 8];
-        const bool has_res = res != nullptr && OUT_BF16;
-        if (has_res) {
-          const int row = row0 + lane, col = n0 + c0;
-          const bool in = row < M && col < N;
-          const uint4* rp = reinterpret_cast<const uint4*>(res + (int64_t)row * N + col);
-#pragma unroll
-          for (int i = 0; i < CW / 8; ++i)
-            rv[i] = in && col + 8 * i < N ? __ldg(rp + i) : make_uint4(0u, 0u, 0u, 0u);
-        }
         tmem_wait_ld();
-        if (has_res) {  // v += residual (fp32), before the bias / activation
+        const uint32_t sb = smem_u32(stage0 + buf * 4096 + lane * 128);
+        if (tres) {  // v += residual (fp32), before the bias / activation
+          mbar_wait(&rb[buf], (rpar >> buf) & 1u);
+          rpar ^= 1u << buf;
 #pragma unroll
-          for (int i = 0; i < CW / 8; ++i) {
-            const uint32_t w4[4] = {rv[i].x, rv[i].y, rv[i].z, rv[i].w};
+          for (int c = 0; c < CW / 8; ++c) {
+            uint32_t w4[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
+                         : "r"(sb + ((c ^ (lane & 7)) << 4))
+                         : "memory");
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              v[8 * i + 2 * e] = __float_as_uint(__uint_as_float(v[8 * i + 2 * e]) + __uint_as_float(w4[e] << 16));
-              v[8 * i + 2 * e + 1] =
-                  __float_as_uint(__uint_as_float(v[8 * i + 2 * e + 1]) + __uint_as_float(w4[e] & 0xffff0000u));
+              v[8 * c + 2 * e] = __float_as_uint(__uint_as_float(v[8 * c + 2 * e]) + __uint_as_float(w4[e] << 16));
+              v[8 * c + 2 * e + 1] =
+                  __float_as_uint(__uint_as_float(v[8 * c + 2 * e + 1]) + __uint_as_float(w4[e] & 0xffff0000u));
             }
           }
         }
@@ -459,7 +470,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty_bar[a]);
         }
-        if (n0 + c0 >= N) continue;  // fully out of range (TMA would clip anyway)
+        if (n0 + c0 >= N) {  // fully out of range (TMA would clip anyway)
+          // with a residual every chunk alternates the buffers (its zero-filled
+          // box was consumed above); without one only stored chunks do
+          if (tres) buf ^= 1;
+          continue;
+        }
         // bias for these CW columns through a warp-private smem row, read back
         // as broadcast float4s
         float f[CW];
@@ -484,7 +500,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         // the staging buffer we are about to overwrite: its store must have read it
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
-        const uint32_t sb = smem_u32(stage0 + buf * 4096 + lane * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this row, SWIZZLE_128B position
           uint4 w;
@@ -848,7 +863,10 @@ cudaError_t launch_pair(const void* a, const void* w, const float* bias, const u
     return cudaErrorInvalidValue;
   const int tiles = ((m + 255) / 256) * ((n + BN - 1) / BN);
   const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
-  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, res, m, n, k,
+  CUtensorMap tr = tc;  // the residual [m, n] bf16, boxed like the output
+  if (res && BF && !make_map(&tr, res, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, n, 64, 32))
+    return cudaErrorInvalidValue;
+  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tr, bias, res, m, n, k,
                                                                  gemm3::ConvGeom{0, 0, 0, 0, 0, 0, 1, 0});
   return cudaGetLastError();
 }
@@ -922,7 +940,10 @@ cudaError_t launch_conv(const void* x, const void* w, const float* bias, const u
     if (e != cudaSuccess) return e;
     if (!make_map(&tc, y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, cout, 64, 32)) return cudaErrorInvalidValue;
     const int pairs = std::max(1, std::min(tiles, max_pairs(kern, Cfg::SMEM)));
-    kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, bias, res, m, cout, k, g);
+    CUtensorMap tr = tc;
+    if (res && !make_map(&tr, res, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, cout, 64, 32))
+      return cudaErrorInvalidValue;
+    kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tr, bias, res, m, cout, k, g);
     return cudaGetLastError();
   }
   auto kern = gemm3::k_gemm_pair<BN, 0, false, true>;  // fp32 partials, no epilogue math
@@ -935,7 +956,7 @@ cudaError_t launch_conv(const void* x, const void* w, const float* bias, const u
   if (!make_map(&tc, part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (int64_t)S * mt * 256, cout, 32, 32))
     return cudaErrorInvalidValue;
   const int pairs = std::max(1, std::min(tiles * S, max_pairs(kern, Cfg::SMEM)));
-  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, nullptr, nullptr, m, cout, k, g);
+  kern<<<dim3(2 * pairs), gemm3::PAIR_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tc, nullptr, nullptr, m, cout, k, g);
   e = cudaGetLastError();
   if (e == cudaSuccess) {
     const int64_t nv = (int64_t)m * (cout / 8);
