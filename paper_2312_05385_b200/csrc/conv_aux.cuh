@@ -107,4 +107,48 @@ __global__ void k_maxpool_nhwc(const uint4* __restrict__ x, int h, int w, int cv
   }
 }
 
+// k_maxpool_nhwc for a fixed K x K window (the ResNet stem's 3 x 3): every tap's
+// 16-byte load is issued before the first max (the generic loop above waits on
+// one load per tap); taps outside the image are skipped in the same order, so
+// the result is the same bits.
+template <int K>
+__global__ void __launch_bounds__(256) k_maxpool_nhwc_k(const uint4* __restrict__ x, int h, int w, int cv,
+                                                        int stride, int pad, int ho, int wo, int64_t nvec,
+                                                        uint4* __restrict__ out) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = v / cv;
+    const int cc = (int)(v - pix * cv);
+    const int64_t img = pix / ((int64_t)ho * wo);
+    const int rem = (int)(pix - img * ho * wo);
+    const int oh = rem / wo, ow = rem - oh * wo;
+    uint4 q[K * K];
+    bool ok[K * K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int ih = oh * stride - pad + r;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const int iw = ow * stride - pad + s;
+        ok[r * K + s] = ih >= 0 && ih < h && iw >= 0 && iw < w;
+        q[r * K + s] = ok[r * K + s] ? __ldg(x + ((img * h + ih) * w + iw) * cv + cc) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    float mx[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < K * K; ++t) {
+      const uint32_t qw[4] = {q[t].x, q[t].y, q[t].z, q[t].w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx[e] = ok[t] ? fmaxf(mx[e], bf_f(qw[e >> 1], e & 1)) : mx[e];
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      o[e] = (__float_as_uint(mx[2 * e]) >> 16) | (__float_as_uint(mx[2 * e + 1]) & 0xffff0000u);
+    out[v] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 }  // namespace convaux

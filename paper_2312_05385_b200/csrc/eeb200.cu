@@ -3029,8 +3029,12 @@ int ee_maxpool_nhwc_bf16(const void* d_x, int64_t n, int32_t h, int32_t w, int32
   const int ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
   const int64_t nv = n * ho * wo * (c / 8);
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(nv, 256), (int64_t)sm_count() * 16);
-  convaux::k_maxpool_nhwc<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<const uint4*>(d_x), h, w, c / 8, k, stride, pad, ho, wo, nv, static_cast<uint4*>(d_out));
+  if (k == 3)
+    convaux::k_maxpool_nhwc_k<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const uint4*>(d_x), h, w, c / 8, stride, pad, ho, wo, nv, static_cast<uint4*>(d_out));
+  else
+    convaux::k_maxpool_nhwc<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const uint4*>(d_x), h, w, c / 8, k, stride, pad, ho, wo, nv, static_cast<uint4*>(d_out));
   EE_LAUNCH_CHECK();
   return EE_OK;
 }

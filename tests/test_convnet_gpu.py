@@ -71,7 +71,8 @@ def test_routed_conv_matches_fp32(cuda, k, stride, cin, cout, hw, b, act, with_r
     assert err <= 1e-2 * scale, (err, scale)
 
 
-@pytest.mark.parametrize("b,c,hw,k,stride,pad", [(2, 64, 112, 3, 2, 1), (3, 24, 17, 3, 2, 1), (1, 8, 9, 2, 2, 0)])
+@pytest.mark.parametrize("b,c,hw,k,stride,pad", [(2, 64, 112, 3, 2, 1), (3, 24, 17, 3, 2, 1), (1, 8, 9, 2, 2, 0),
+                                               (2, 16, 10, 3, 1, 1), (1, 8, 7, 3, 2, 0)])
 def test_maxpool_nhwc_matches_torch(cuda, b, c, hw, k, stride, pad):
     g = torch.Generator(device="cuda").manual_seed(c + hw)
     x = _bf(torch.randn(b, c, hw, hw, generator=g, device="cuda"))
