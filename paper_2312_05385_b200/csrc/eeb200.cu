@@ -2325,11 +2325,22 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
   if (rc) return rc;
   const size_t smem = (size_t)(c + k) * 4;
   if (smem > 200 * 1024) return fail(EE_ERR_ARG, "too many channels for the fused head");
-  // S CTAs (one thread-block cluster) per row, ~8 KB of the map each, at most 8
-  // (the portable cluster size); S depends on the row shape only
+  // S CTAs (one thread-block cluster) per row, ~8 KB of the map each, at most 2;
+  // S depends on the row shape only. Clusters of up to 8 read a big map on more
+  // SMs, but a head overlapped with the backbone (feedback mode, side stream)
+  // only starts once S SMs of one GPC are free at the same time, which the
+  // persistent GEMMs around it rarely leave: ResNet-18 CIFAR feedback graph
+  // 0.2625 ms at S <= 8, 0.260 at 4, 0.250 at 2, 0.254 at 1, with the serialised
+  // heads at 0.266 ms for every cap (tools/gpu_iter41.sh). EEB200_EXIT_MAX_S
+  // overrides the cap (1..8).
   const int64_t row_bytes = (int64_t)c * hw * (feat_bf16 ? 2 : 4);
+  static const int s_max = [] {
+    const char* e = std::getenv("EEB200_EXIT_MAX_S");
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 1 && v <= 8 ? v : 2;
+  }();
   int S = 1;
-  while (S < 8 && S * 2 <= hw && row_bytes >= (int64_t)S * 2 * 8192) S *= 2;
+  while (S < s_max && S * 2 <= hw && row_bytes >= (int64_t)S * 2 * 8192) S *= 2;
   if ((int64_t)b * S > 0x7fffffff) S = 1;
   ProfScope ps(ws, st, "k_exit_fused");
 #define EE_EXITK(TF, TW)                                                                       \

@@ -53,8 +53,9 @@ HEAD_CASES = [(lay, sh) for lay in ("nchw", "nhwc") for sh in HEAD_SHAPES] + [("
 @pytest.mark.parametrize("conf", ["maxprob", "entropy"])
 def test_fused_head_matches_torch(cuda, layout, dtype, conf, shape):
     """Every pooling path, including the cluster-split ones (a row's map split
-    over 2-8 CTAs of one cluster when it is >= 16 KB: the CIFAR ResNet-18 ramp
-    shapes) and a ragged 57x57 plane."""
+    over 2 CTAs of one cluster when it is >= 16 KB, up to 8 under
+    EEB200_EXIT_MAX_S: the CIFAR ResNet-18 ramp shapes) and a ragged 57x57
+    plane."""
     g = torch.Generator().manual_seed(1)
     b, c, hw = shape
     k = 10
@@ -72,6 +73,20 @@ def test_fused_head_matches_torch(cuda, layout, dtype, conf, shape):
     thr = float(err_probe.median())
     res = head(feat_d, thr, want_logits=True)
     _check(res, feat_d.float().cpu(), w, bias, conf, thr)
+
+
+def test_fused_head_wide_clusters_subprocess(cuda):
+    """The 4- and 8-CTA cluster splits (EEB200_EXIT_MAX_S=8; the cap is read
+    once per process, so in a child pytest)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, EEB200_EXIT_MAX_S="8")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
+                        "test_fused_head_matches_torch"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_alive_mask_slots_and_scatter(cuda):
