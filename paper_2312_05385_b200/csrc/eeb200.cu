@@ -2331,7 +2331,7 @@ int ee_exit_controller(ee_workspace* ws, const void* d_feat, int32_t feat_bf16, 
   // only starts once S SMs of one GPC are free at the same time, which the
   // persistent GEMMs around it rarely leave: ResNet-18 CIFAR feedback graph
   // 0.2625 ms at S <= 8, 0.260 at 4, 0.250 at 2, 0.254 at 1, with the serialised
-  // heads at 0.266 ms for every cap (tools/gpu_iter41.sh). EEB200_EXIT_MAX_S
+  // heads at 0.266 ms for every cap (tools/sweep_ramp_cluster.sh). EEB200_EXIT_MAX_S
   // overrides the cap (1..8).
   const int64_t row_bytes = (int64_t)c * hw * (feat_bf16 ? 2 : 4);
   static const int s_max = [] {
