@@ -308,6 +308,8 @@ def route_classifier(model):
     """Rebind a ResNet's avgpool to ClassifierTC (returns logits [B, classes]) and
     its fc to the identity: both the model's own forward (avgpool -> flatten ->
     fc) and an EEPipeline's final Sequential(avgpool, Flatten, fc) then run it."""
+    if model.fc.in_features == model.fc.out_features:
+        return None  # the fc could not tell logits from features: keep the library path
     head = ClassifierTC(model)
     model.avgpool.forward = head
     model.fc.forward = lambda x: x if x.dim() == 2 and x.shape[1] == head.fc.out_features \

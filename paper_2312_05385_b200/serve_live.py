@@ -127,11 +127,12 @@ def _graph_runner(pipe, bsz: int, example, thresholds):
     """The pipeline's timed feedback-mode graph for batch size `bsz`, captured on
     first use and kept on the pipeline (one graph per batch size the server forms)."""
     cache = pipe.__dict__.setdefault("_live_graphs", {})
-    run = cache.get(bsz)
+    key = (bsz, tuple(example.shape[1:]), example.dtype, example.stride()[1:])
+    run = cache.get(key)
     if run is None:
         run = pipe.capture(example[:bsz], thresholds, timed=True)
         run.version = None
-        cache[bsz] = run
+        cache[key] = run
     return run
 
 
