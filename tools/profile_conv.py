@@ -14,6 +14,12 @@ if which == "3x3":
     c = convnet.Conv(conv)
     for _ in range(3):
         y = c(x, act="relu")
+elif which == "1x1_64":  # layer1 bottleneck conv1: 256 -> 64 channels (a 64-wide tile)
+    conv = torch.nn.Conv2d(256, 64, 1).cuda().to(torch.bfloat16).to(memory_format=CL)
+    x = torch.randn(256, 256, 56, 56, generator=g, device="cuda").to(torch.bfloat16).contiguous(memory_format=CL)
+    c = convnet.Conv(conv)
+    for _ in range(3):
+        y = c(x, act="relu")
 else:
     conv = torch.nn.Conv2d(64, 256, 1).cuda().to(torch.bfloat16).to(memory_format=CL)
     x = torch.randn(256, 64, 56, 56, generator=g, device="cuda").to(torch.bfloat16).contiguous(memory_format=CL)
