@@ -38,3 +38,17 @@ for tag, m, n, k in (("l1_conv1", 802816, 64, 256), ("stem", 3211264, 64, 168), 
         out[name + "_same"] = bool(torch.equal(y, ref))
     out["bytes_mb"] = round((m * k + m * n) * 2 / 1e6, 1)
     print(json.dumps(out))
+
+# the 64-wide 3x3 implicit GEMM (layer1, B=256, 56x56) warm, against cuDNN on the same operands
+from paper_2312_05385_b200 import convnet
+
+CL = torch.channels_last
+for cin, cout, hw in ((64, 64, 56), (128, 128, 28), (256, 256, 14)):
+    conv = torch.nn.Conv2d(cin, cout, 3, 1, 1).cuda().to(torch.bfloat16).to(memory_format=CL)
+    x = torch.randn(256, cin, hw, hw, device="cuda").to(torch.bfloat16).contiguous(memory_format=CL)
+    c = convnet.Conv(conv)
+    ours = timeit(lambda: c(x, act="relu"))
+    lib = timeit(lambda: torch.relu(conv(x)))
+    fl = 2 * 256 * hw * hw * cout * cin * 9
+    print(json.dumps({"tag": f"conv3x3_{cin}_{hw}", "ours_us": round(ours, 2), "cudnn_relu_us": round(lib, 2),
+                      "ours_tflops": round(fl / ours / 1e6, 1)}))
